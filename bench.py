@@ -1,0 +1,306 @@
+"""Benchmark of the B200 Kronecker space-time heat solve (BASELINE.json metric).
+
+Workload: config 3 -- 2D heat, Q1 on a 1023 x 1023 interior grid, n_t = 1024 (1.07e9 FP64
+unknowns), full-rank F ~ U[-1,1] from the seeded counter generator.  One step = one full
+solve F -> U (solve_projected_heat_with in tensor form: DMMA transforms + modal scan).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+* value      : unknowns/s with F and U resident in HBM (CUDA events on the plan stream,
+               barrier + synchronize on both sides, max over ranks).
+* e2e        : unknowns/s through the public host-buffer API (stkg_heat_solve_host) with
+               the H2D of F and the D2H of U (pinned host memory) inside the timed region.
+* roofline   : dominant kernel = the DMMA GEMM transforms; achieved = 2 n flops per
+               unknown per transform launch / mean launch time (CUDA events around every
+               launch on the plan stream), peak = measured DMMA FP64 peak.
+* cpu_baseline / --impl reference : the oracle port of solve_projected_heat_with
+               (oracle/oracle.py::heat_decoupled, numpy + multithreaded BLAS) on a bounded
+               causal prefix of the same workload, on this host's cores.
+N > 1 runs independent replicas (in-scope multi-GPU is replicas only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "space-time unknowns solved/sec (FP64) and % of HBM/FP64 roofline vs CPU ref"
+UNIT = "unknowns/s"
+# Measured on this pool's B200 (profiles/r01_fp64_peak.txt): DMMA m16n8k16 sustained.
+FP64_PEAK_TFLOPS = 37.11
+FP64_PEAK_SOURCE = "measured DMMA (mma.sync f64) sustained, profiles/r01_fp64_peak.txt"
+CPU_SAMPLE_STEPS = 96  # causal prefix of cfg3 time slices for the CPU leg
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def build_plan(stk, cfg, stream=None, time_chunk=0):
+    g = stk.SpaceGrid1D(0.0, 1.0, cfg.n)
+    M, A = stk.fem1d_matrices(g)
+    D, Cm = stk.heat_time_matrices(stk.TimeGrid(cfg.nt, 1.0))
+    eig = stk.TensorEigPair([stk.p1_eigpair(g)] * cfg.ndim)
+    return stk.HeatPlan(eig, D, Cm, [M] * cfg.ndim, [A] * cfg.ndim, stream=stream,
+                        time_chunk=time_chunk)
+
+
+def cpu_reference_run(cfg, steps: int, seed: int = 0):
+    """The oracle port of solve_projected_heat_with on a causal prefix (steps slices)."""
+    from oracle import oracle as O
+    from paper_1912_10082_b200 import inputs
+    F = inputs.heat_rhs_host(cfg, seed, nsteps=steps)
+    m, a = O.fem1d_matrices(0.0, 1.0, cfg.n)
+    d, c = O.heat_time_matrices(cfg.nt)
+    eig = O.p1_pencil_eig(m, a)
+    t0 = time.perf_counter()
+    O.heat_decoupled([eig] * cfg.ndim, d, c, F, nsteps=steps)
+    return time.perf_counter() - t0
+
+
+def traffic_from_profiles():
+    p = ROOT / "profiles" / "traffic.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text()).get("gemm_dram_bytes_per_launch")
+        except Exception:
+            return None
+    return None
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    from paper_1912_10082_b200 import inputs
+    cfg = inputs.CONFIGS[args.config]
+    cores = os.cpu_count()
+    steps_per = args.ref_sample
+    for _ in range(args.warmup):
+        cpu_reference_run(cfg, max(2, steps_per // 8))
+    times = [cpu_reference_run(cfg, steps_per) for _ in range(args.steps)]
+    t = sum(times)
+    value = cfg.nx * steps_per * args.steps / t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": cfg.name, "parallelism": "cpu",
+                   "sample": f"causal prefix of {steps_per} of {cfg.nt} time slices"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"oracle heat_decoupled (numpy+BLAS, {cores} threads), "
+                                   f"{steps_per}-slice causal prefix of {args.config}"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import torch
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_1912_10082_b200 as stk
+    from paper_1912_10082_b200 import inputs
+    cfg = inputs.CONFIGS[args.config]
+    stream = torch.cuda.Stream()
+    N = cfg.unknowns
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    with torch.cuda.stream(stream):
+        plan = build_plan(stk, cfg, stream=stream.cuda_stream)
+        F = inputs.heat_rhs_device(cfg, seed=rank)
+        U = torch.empty_like(F)
+        stream.synchronize()
+        for _ in range(args.warmup):
+            plan.solve(F, out=U)
+        stream.synchronize()
+        # ---- device-resident timed region -------------------------------------------
+        clocks = ClockSampler(local)
+        clocks.start()
+        barrier()
+        torch.cuda.synchronize()
+        plan.profile_begin()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            plan.solve(F, out=U)
+        e1.record(stream)
+        stream.synchronize()
+        prof = plan.profile_end()
+        torch.cuda.synchronize()
+        barrier()
+        clk = clocks.stop()
+        ms = e0.elapsed_time(e1)
+        relres, _ = plan.residual(U, F)
+    t_local = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if dist is not None:
+        dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
+    ms_max = float(t_local.item())
+    value = world * N * args.steps / (ms_max / 1e3)
+
+    # ---- end to end through the public host-buffer API --------------------------------
+    e2e = None
+    if not args.no_e2e:
+        Fh = torch.empty((cfg.nt, cfg.nx), dtype=torch.float64).pin_memory()
+        Uh = torch.empty_like(Fh).pin_memory()
+        Fh.copy_(F)
+        del U
+        torch.cuda.empty_cache()
+        plan_h = build_plan(stk, cfg, stream=stream.cuda_stream, time_chunk=args.time_chunk)
+        plan_h.solve_host(Fh.numpy(), out=Uh.numpy())  # warm-up (allocates chunk buffers)
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            plan_h.solve_host(Fh.numpy(), out=Uh.numpy())
+        torch.cuda.synchronize()
+        t_e2e = time.perf_counter() - t0
+        t_e = torch.tensor([t_e2e], dtype=torch.float64, device="cuda")
+        if dist is not None:
+            dist.all_reduce(t_e, op=dist.ReduceOp.MAX)
+        e2e = {"value": world * N * args.e2e_steps / float(t_e.item()), "unit": UNIT,
+               "h2d_bytes_per_step": N * 8, "d2h_bytes_per_step": N * 8,
+               "steps": args.e2e_steps, "api": "stkg_heat_solve_host (pinned host buffers)"}
+        plan_h.close()
+
+    # ---- roofline of the dominant kernel -------------------------------------------------
+    t_ms, t_n = prof["transform"]
+    s_ms, s_n = prof["scan"]
+    flops_per_launch = 2.0 * cfg.n * N  # 2n flop per unknown per axis transform pass
+    achieved = flops_per_launch / (t_ms / t_n / 1e3) / 1e12
+    roofline = {"bound": "tensor", "kernel": "gemm_f64_kernel (DMMA transforms)",
+                "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic_from_profiles(),
+                "peak_source": FP64_PEAK_SOURCE,
+                "share_of_step": t_ms / ms, "scan_share_of_step": s_ms / ms,
+                "whole_solve_frac": (2 * cfg.ndim * flops_per_launch * args.steps /
+                                     (ms / 1e3) / 1e12) / FP64_PEAK_TFLOPS}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg.name, "unknowns_per_step": N, "n": cfg.n, "nt": cfg.nt,
+                   "parallelism": "replicas" if world > 1 else "single",
+                   "l2_flush": "inputs larger than L2 (F, U 8.6 GB each)",
+                   "relres_gpu_k1": relres},
+        "roofline": roofline,
+        "e2e": e2e,
+        "gpu_launches": int(t_n + s_n),
+        "clocks": clk,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu_t = cpu_reference_run(cfg, args.ref_sample)
+        cpu_v = cfg.nx * args.ref_sample / cpu_t
+        line["cpu_baseline"] = {"value": cpu_v, "unit": UNIT, "cores": os.cpu_count(),
+                                "kind": "port",
+                                "sample": f"oracle heat_decoupled (numpy+BLAS), "
+                                          f"{args.ref_sample}-slice causal prefix of {args.config}, "
+                                          f"{cpu_t:.2f} s"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    plan.close()
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="cfg3", choices=["cfg1", "cfg2", "cfg3", "cfg5"])
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--time-chunk", type=int, default=0)
+    ap.add_argument("--ref-sample", type=int, default=CPU_SAMPLE_STEPS)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

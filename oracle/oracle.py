@@ -1,0 +1,405 @@
+"""CPU oracle for the B200 Kronecker space-time solver -- TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / ``--impl reference`` legs
+may import this module; the product package never does.  Two independent restatements of
+the reference algorithms live here:
+
+* ``C`` -- ``libstk_oracle.so`` (stk_oracle.c): loop-for-loop restatements of
+  heat_time_matrices / fem1d_matrices (stk/discretize.hpp:44-77), KronOp::apply
+  (stk/sylvester.hpp:32-38), solve_projected_heat_with (:117-142), crank_nicolson
+  (stk/cn_baseline.hpp:26-48, banded Cholesky in place of SimplicialLLT) and
+  WaveOperator::apply (stk/outer_krylov.hpp:178-186);
+* numpy/scipy -- tensor-form decoupled heat solve with scipy ``eigh`` eigenbases (not the
+  closed form the product uses), CN with ``scipy.sparse.linalg.splu``, TwoTermPrecond::solve
+  (stk/sylvester.hpp:168-176), and gmres (stk/outer_krylov.hpp:75-164, modified Gram-Schmidt
+  + one re-orthogonalisation pass, exactly as the reference).
+
+``ref`` -- ``oracle/_ref/libstkref.so`` is the reference's own splines.hpp/quadrature.hpp
+compiled from /root/reference (only in the build container); tests/golden holds the band
+fixtures it produced so the GPU box can check them without the reference tree.
+
+Parity status: the heat path is pinned by the SPEC.md known-answer examples
+(tests/golden/spec_kats.json) and by oracle-vs-oracle agreement (CN vs decoupled); the wave
+assembly is pinned bit-for-bit by the reference's own spline code.  No reference-produced
+golden vectors exist for the solver outputs (the reference cannot be built: no Eigen3).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+_dp = C.POINTER(C.c_double)
+
+
+def _build_c():
+    so = HERE / "libstk_oracle.so"
+    src = HERE / "stk_oracle.c"
+    if not so.exists() or so.stat().st_mtime < src.stat().st_mtime:
+        subprocess.run(["make", "-C", str(HERE), "libstk_oracle.so"], check=True,
+                       capture_output=True)
+    return so
+
+
+def _lib():
+    lib = C.CDLL(str(_build_c()))
+    i64p = C.POINTER(C.c_int64)
+    pp = C.POINTER(_dp)
+    lib.or_heat_apply.argtypes = [C.c_int, i64p, C.c_int64, pp, pp, pp, pp, _dp, _dp, _dp, _dp,
+                                  _dp, _dp]
+    lib.or_solve_projected_heat_with.argtypes = [C.c_int64, C.c_int64, _dp, _dp, _dp, _dp, _dp,
+                                                 _dp, _dp, _dp]
+    lib.or_solve_projected_heat_with.restype = C.c_int
+    lib.or_crank_nicolson.argtypes = [C.c_int, i64p, C.c_int64, C.c_double, pp, pp, pp, pp,
+                                      _dp, _dp]
+    lib.or_crank_nicolson.restype = C.c_int
+    lib.or_wave_apply.argtypes = [C.c_int64, C.c_int64, _dp, _dp, _dp, _dp]
+    lib.or_fill_uniform.argtypes = [_dp, C.c_int64, C.c_uint64, C.c_uint64, C.c_int64]
+    lib.or_heat_time_matrices.argtypes = [C.c_int, C.c_double, _dp, _dp, _dp, _dp]
+    lib.or_fem1d_matrices.argtypes = [C.c_double, C.c_double, C.c_int, _dp, _dp, _dp, _dp]
+    return lib
+
+
+clib = _lib()
+
+
+def _p(a):
+    return a.ctypes.data_as(_dp)
+
+
+def _arr_pp(arrs, keep):
+    out = (_dp * 3)()
+    for i, a in enumerate(arrs):
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        if a.size == 0:
+            a = np.zeros(1)
+        keep.append(a)
+        out[i] = _p(a)
+    return out
+
+
+# ------------------------------------------------------------------------ assembly --
+def heat_time_matrices(nt: int, T: float = 1.0):
+    dd, cd = np.empty(nt), np.empty(nt)
+    ds, cs = np.zeros(max(nt - 1, 1)), np.zeros(max(nt - 1, 1))
+    clib.or_heat_time_matrices(nt, T, _p(dd), _p(ds), _p(cd), _p(cs))
+    return (dd, ds[: nt - 1]), (cd, cs[: nt - 1])
+
+
+def fem1d_matrices(a: float, b: float, nh: int):
+    md, ad = np.empty(nh), np.empty(nh)
+    mo, ao = np.zeros(max(nh - 1, 1)), np.zeros(max(nh - 1, 1))
+    clib.or_fem1d_matrices(a, b, nh, _p(md), _p(mo), _p(ad), _p(ao))
+    return (md, mo[: nh - 1]), (ad, ao[: nh - 1])
+
+
+def tri_dense(t):
+    d, o = t
+    m = np.diag(d)
+    if d.size > 1:
+        m = m + np.diag(o, 1) + np.diag(o, -1)
+    return m
+
+
+def bidiag_dense(b):
+    d, s = b
+    m = np.diag(d)
+    if d.size > 1:
+        m = m + np.diag(s, 1)
+    return m
+
+
+def tensor_sparse(ms, as_):
+    """fem2d_matrices (stk/discretize.hpp:81-88) / 3D restatement as scipy CSR."""
+    import scipy.sparse as sp
+    M1 = [sp.csr_matrix(tri_dense(m)) for m in ms]
+    A1 = [sp.csr_matrix(tri_dense(a)) for a in as_]
+    M = M1[0]
+    for m in M1[1:]:
+        M = sp.kron(M, m, format="csr")
+    A = None
+    for k in range(len(ms)):
+        t = A1[0] if k == 0 else M1[0]
+        for j in range(1, len(ms)):
+            t = sp.kron(t, A1[j] if j == k else M1[j], format="csr")
+        A = t if A is None else A + t
+    return M.tocsr(), A.tocsr()
+
+
+# ------------------------------------------------------------------------ heat (C) --
+def heat_apply(ms, as_, d, c, U):
+    """C restatement of KronOp::apply (stk/sylvester.hpp:32-38); U is (nt, nx) C-order."""
+    ndim = len(ms)
+    n = (C.c_int64 * 3)(*[m[0].size for m in ms], *([1] * (3 - ndim)))
+    keep = []
+    U = np.ascontiguousarray(U, dtype=np.float64)
+    out = np.empty_like(U)
+    clib.or_heat_apply(ndim, n, U.shape[0], _arr_pp([m[0] for m in ms], keep),
+                       _arr_pp([m[1] for m in ms], keep), _arr_pp([a[0] for a in as_], keep),
+                       _arr_pp([a[1] for a in as_], keep), _p(np.ascontiguousarray(d[0])),
+                       _p(np.ascontiguousarray(d[1]) if d[1].size else np.zeros(1)),
+                       _p(np.ascontiguousarray(c[0])),
+                       _p(np.ascontiguousarray(c[1]) if c[1].size else np.zeros(1)), _p(U),
+                       _p(out))
+    return out
+
+
+def solve_projected_heat_with_dense(X, lam, d, c, G):
+    """C restatement of solve_projected_heat_with with a dense k x k EigPair."""
+    k = X.shape[0]
+    G = np.ascontiguousarray(G, dtype=np.float64)
+    nt = G.shape[0]
+    Xc = np.asfortranarray(X)
+    Y = np.empty_like(G)
+    dsup = d[1] if d[1].size else np.zeros(1)
+    csup = c[1] if c[1].size else np.zeros(1)
+    st = clib.or_solve_projected_heat_with(k, nt, _p(Xc), _p(np.ascontiguousarray(lam)),
+                                           _p(np.ascontiguousarray(d[0])), _p(np.ascontiguousarray(dsup)),
+                                           _p(np.ascontiguousarray(c[0])), _p(np.ascontiguousarray(csup)),
+                                           _p(G), _p(Y))
+    if st:
+        raise ZeroDivisionError("singular row system")
+    return Y
+
+
+def crank_nicolson(ms, as_, dt, F, nsteps=None):
+    """C restatement of crank_nicolson (stk/cn_baseline.hpp:26-48), banded Cholesky."""
+    ndim = len(ms)
+    F = np.ascontiguousarray(F, dtype=np.float64)
+    nsteps = F.shape[0] if nsteps is None else nsteps
+    n = (C.c_int64 * 3)(*[m[0].size for m in ms], *([1] * (3 - ndim)))
+    keep = []
+    U = np.empty((nsteps, F.shape[1]))
+    st = clib.or_crank_nicolson(ndim, n, nsteps, dt, _arr_pp([m[0] for m in ms], keep),
+                                _arr_pp([m[1] for m in ms], keep),
+                                _arr_pp([a[0] for a in as_], keep),
+                                _arr_pp([a[1] for a in as_], keep), _p(F), _p(U))
+    if st:
+        raise np.linalg.LinAlgError("crank_nicolson: not s.p.d.")
+    return U
+
+
+# -------------------------------------------------------------------- heat (numpy) --
+def p1_pencil_eig(m, a):
+    """Numerical sym_gen_eig(A, M) of a 1D pencil by scipy (independent of the closed form)."""
+    import scipy.linalg as sl
+    lam, X = sl.eigh(tri_dense(a), tri_dense(m))
+    return lam, X
+
+
+def heat_decoupled(eigs, d, c, F, nsteps=None):
+    """solve_projected_heat_with (stk/sylvester.hpp:117-142) in tensor form with numpy:
+    per-axis transforms G~ = (X_x (x) X_y (x) X_z)^T F, per-mode recurrence, inverse.
+    ``eigs`` = [(lam, X)] per axis; F is (nt, nx) C-order; nsteps => causal prefix."""
+    ns = [e[0].size for e in eigs]
+    nt = F.shape[0] if nsteps is None else nsteps
+    G = np.asarray(F[:nt], dtype=np.float64).reshape(nt, *ns)
+    for ax, (lam, X) in enumerate(eigs):  # forward: contract axis ax+1 with X
+        G = np.moveaxis(np.tensordot(G, X, axes=([ax + 1], [0])), -1, ax + 1)
+    lam_t = np.zeros(ns)
+    for ax, (lam, X) in enumerate(eigs):
+        shape = [1] * len(ns)
+        shape[ax] = ns[ax]
+        lam_t = lam_t + lam.reshape(shape)
+    Y = np.empty_like(G)
+    y = np.zeros(ns)
+    for j in range(nt):
+        piv = d[0][j] + lam_t * c[0][j]
+        rhs = G[j]
+        if j > 0:
+            rhs = rhs - (d[1][j - 1] + lam_t * c[1][j - 1]) * y
+        y = rhs / piv
+        Y[j] = y
+    for ax, (lam, X) in enumerate(eigs):
+        Y = np.moveaxis(np.tensordot(Y, X, axes=([ax + 1], [1])), -1, ax + 1)
+    return Y.reshape(nt, -1)
+
+
+def crank_nicolson_splu(ms, as_, dt, F, nsteps=None):
+    """CN (stk/cn_baseline.hpp:26-48) with scipy SuperLU in place of SimplicialLLT."""
+    import scipy.sparse.linalg as spl
+    M, A = tensor_sparse(ms, as_)
+    lhs = (M + (dt / 2.0) * A).tocsc()
+    rhs = (M - (dt / 2.0) * A).tocsr()
+    lu = spl.splu(lhs)
+    nt = F.shape[0] if nsteps is None else nsteps
+    U = np.empty((nt, F.shape[1]))
+    u = np.zeros(F.shape[1])
+    for l in range(nt):
+        u = lu.solve(rhs @ u + F[l])
+        U[l] = u
+    return U
+
+
+def heat_residual(ms, as_, d, c, U, F):
+    """||F - KronOp::apply(U)||_F / ||F||_F (stk/bench.hpp:508)."""
+    R = F - heat_apply(ms, as_, d, c, U)
+    return float(np.linalg.norm(R) / np.linalg.norm(F))
+
+
+# ------------------------------------------------------------------------------ wave --
+def ref_lib():
+    so = HERE / "_ref" / "libstkref.so"
+    if not so.exists():
+        if (Path("/root/reference/proj/include/stk/splines.hpp")).exists():
+            subprocess.run(["make", "-C", str(HERE), "ref"], check=True, capture_output=True)
+        else:
+            return None
+    lib = C.CDLL(str(so))
+    lib.ref_wave_space_bands.argtypes = [C.c_double, C.c_double, C.c_int, C.c_int, _dp]
+    lib.ref_wave_time_bands.argtypes = [C.c_int, C.c_double, C.c_int, _dp]
+    lib.ref_gauss_legendre.argtypes = [C.c_int, C.c_double, C.c_double, _dp, _dp]
+    lib.ref_spline_eval.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, C.c_int,
+                                    C.c_double, C.c_int, _dp]
+    return lib
+
+
+def ref_wave_bands(nh: int, nt: int, degree: int = 3, T: float = 1.0):
+    """(space [M|A|Q], time [Q|D|M]) bands from the reference's own spline code."""
+    lib = ref_lib()
+    if lib is None:
+        raise FileNotFoundError("oracle/_ref not built and reference tree absent")
+    sb = np.zeros(3 * 7 * nh)
+    ntb = nt + degree - 2
+    tb = np.zeros(3 * 7 * ntb)
+    assert lib.ref_wave_space_bands(0.0, 1.0, nh, degree, _p(sb)) == nh
+    assert lib.ref_wave_time_bands(nt, T, degree, _p(tb)) == ntb
+    return sb.reshape(3, 7, nh), tb.reshape(3, 7, ntb)
+
+
+def band_dense(band):
+    n = band.shape[1]
+    m = np.zeros((n, n))
+    for dd in range(7):
+        for i in range(n):
+            j = i + dd - 3
+            if 0 <= j < n:
+                m[i, j] = band[dd, i]
+    return m
+
+
+def band_sparse(band):
+    import scipy.sparse as sp
+    n = band.shape[1]
+    rows, cols, vals = [], [], []
+    for dd in range(7):
+        i = np.arange(n)
+        j = i + dd - 3
+        ok = (j >= 0) & (j < n)
+        rows.append(i[ok]); cols.append(j[ok]); vals.append(band[dd][ok])
+    return sp.csr_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
+                         shape=(n, n))
+
+
+def wave_apply(sb, tb, U):
+    """C restatement of WaveOperator::apply; U is (nt, nh) C-order (== nh x nt col-major)."""
+    nt, nh = U.shape
+    U = np.ascontiguousarray(U, dtype=np.float64)
+    out = np.empty_like(U)
+    clib.or_wave_apply(nh, nt, _p(np.ascontiguousarray(sb).ravel()),
+                       _p(np.ascontiguousarray(tb).ravel()), _p(U), _p(out))
+    return out
+
+
+class WaveSystemNP:
+    """numpy/scipy restatement of the wave system: WaveOperator (stk/outer_krylov.hpp:
+    168-191), TwoTermPrecond (stk/sylvester.hpp:153-181, scipy eigh) and gmres (:75-164)."""
+
+    def __init__(self, sb, tb):
+        import scipy.linalg as sl
+        self.Mh, self.Ah, self.Qh = (band_sparse(sb[k]) for k in range(3))
+        self.Qt, self.Dt, self.Mt = (band_sparse(tb[k]) for k in range(3))
+        self.E = (self.Dt + self.Dt.T).tocsr()
+        self.nh, self.nt = sb.shape[2], tb.shape[2]
+        self.lam, self.Xs = sl.eigh(self.Qh.toarray(), self.Mh.toarray())
+        self.theta, self.Xt = sl.eigh(self.Qt.toarray(), self.Mt.toarray())
+
+    def apply(self, x):
+        U = x.reshape(self.nt, self.nh).T  # nh x nt view (column-major vec)
+        out = (self.Mh @ U) @ self.Qt.T + (self.Ah @ U) @ self.E + (self.Qh @ U) @ self.Mt
+        return np.ascontiguousarray(out.T).ravel()
+
+    def precond(self, v):
+        V = v.reshape(self.nt, self.nh).T
+        wt = self.Xs.T @ V @ self.Xt
+        wt = wt / (self.lam[:, None] + self.theta[None, :])
+        W = self.Xs @ wt @ self.Xt.T
+        return np.ascontiguousarray(W.T).ravel()
+
+    def gmres(self, b, tol=1e-8, maxit=200):
+        """Right-preconditioned full GMRES, MGS + one re-orth pass, Givens (reference)."""
+        norm_b = np.linalg.norm(b)
+        x = np.zeros_like(b)
+        if norm_b == 0:
+            return x, 0, []
+        r = b.copy()
+        beta = np.linalg.norm(r)
+        basis = [r / beta]
+        hcols = []
+        g = np.zeros(maxit + 1)
+        g[0] = beta
+        cs, sn = [], []
+        hist = []
+        k = 0
+        total = 0
+        for j in range(maxit):
+            w = self.apply(self.precond(basis[j]))
+            col = np.zeros(j + 2)
+            for i in range(j + 1):
+                hij = basis[i] @ w
+                w -= hij * basis[i]
+                col[i] = hij
+            for i in range(j + 1):
+                corr = basis[i] @ w
+                w -= corr * basis[i]
+                col[i] += corr
+            hlast = np.linalg.norm(w)
+            col[j + 1] = hlast
+            for i in range(j):
+                t = cs[i] * col[i] + sn[i] * col[i + 1]
+                col[i + 1] = -sn[i] * col[i] + cs[i] * col[i + 1]
+                col[i] = t
+            a, bb = col[j], col[j + 1]
+            rr = np.hypot(a, bb)
+            cc = 1.0 if rr == 0 else a / rr
+            ss = 0.0 if rr == 0 else bb / rr
+            cs.append(cc); sn.append(ss)
+            col[j], col[j + 1] = rr, 0.0
+            t = cc * g[j] + ss * g[j + 1]
+            g[j + 1] = -ss * g[j] + cc * g[j + 1]
+            g[j] = t
+            hcols.append(col)
+            relres = abs(g[j + 1]) / norm_b
+            hist.append(relres)
+            k = j + 1
+            total = j + 1
+            if relres <= tol or hlast == 0:
+                break
+            basis.append(w / hlast)
+        y = np.zeros(k)
+        for i in range(k - 1, -1, -1):
+            acc = g[i]
+            for jj in range(i + 1, k):
+                acc -= hcols[jj][i] * y[jj]
+            y[i] = acc / hcols[i][i]
+        xk = sum(y[i] * basis[i] for i in range(k))
+        x += self.precond(xk)
+        return x, total, hist
+
+    def direct(self, b):
+        """kron_direct_solve (stk/bench.hpp:414-429) with scipy SuperLU: sum_p D_p (x) A_p."""
+        import scipy.sparse as sp
+        import scipy.sparse.linalg as spl
+        B = (sp.kron(self.Qt, self.Mh) + sp.kron(self.E.T, self.Ah) + sp.kron(self.Mt.T, self.Qh))
+        return spl.splu(B.tocsc()).solve(b)
+
+
+# ----------------------------------------------------------------------- generator --
+def fill_uniform(count, seed, stream, offset=0):
+    out = np.empty(count)
+    clib.or_fill_uniform(_p(out), count, seed, stream, offset)
+    return out

@@ -1,0 +1,230 @@
+// FP64 tensor-core GEMM for sm_100a (K2 of SURVEY §2.1): C_b = A_b * B_b, column-major,
+// arbitrary M/N/K and leading dimensions (8-byte aligned operands are enough: the heat
+// slices of U have leading dimension n = 1023).
+//
+// sm_100a has no tcgen05 FP64 kind (ptxas rejects kind::f64), so the FP64 tensor path is
+// the warp-level mma.sync.m16n8k4.f64, which lowers to DMMA.8x8x4.  Measured on B200:
+// DMMA 37.1 TFLOP/s vs DFMA 34.2 TFLOP/s (profiles/r01_fp64_peak.txt), so the transforms
+// run on DMMA.  Operands are staged by a multi-stage cp.async pipeline (8-byte granules,
+// zero-filled at the matrix edges), fragments are read from padded, bank-conflict-free
+// shared memory tiles.
+//
+// These GEMMs are the basis transforms of solve_projected_heat_with
+// (stk/sylvester.hpp:126 `eig.X.transpose() * g`, :141 `eig.X * yt`) in tensor form, and
+// the four products of TwoTermPrecond::solve (stk/sylvester.hpp:171,175).
+#pragma once
+
+#include "common.cuh"
+
+namespace stkg {
+
+struct GemmProblem {
+  int64_t M = 0, N = 0, K = 0;
+  int64_t batch = 1;
+  const double* A = nullptr;  // M x K, column-major
+  int64_t lda = 0, strideA = 0;
+  const double* B = nullptr;  // K x N, column-major
+  int64_t ldb = 0, strideB = 0;
+  double* C = nullptr;        // M x N, column-major
+  int64_t ldc = 0, strideC = 0;
+};
+
+// Epilogues ------------------------------------------------------------------------
+struct EpiStore {
+  __device__ __forceinline__ double operator()(double v, int64_t, int64_t) const { return v; }
+};
+
+// TwoTermPrecond::solve's divide (stk/sylvester.hpp:172-174): wt(i,j) /= lambda_i + theta_j.
+struct EpiDivide {
+  const double* lam;
+  const double* theta;
+  __device__ __forceinline__ double operator()(double v, int64_t r, int64_t c) const {
+    return v / (lam[r] + theta[c]);
+  }
+};
+
+// Tile configuration ---------------------------------------------------------------
+template <int BM_, int BN_, int BK_, int WM_, int WN_, int STAGES_, int MINB_>
+struct GemmCfg {
+  static constexpr int BM = BM_, BN = BN_, BK = BK_, WM = WM_, WN = WN_, STAGES = STAGES_;
+  static constexpr int kMinBlocks = MINB_;
+  static constexpr int kWarpsM = BM / WM, kWarpsN = BN / WN;
+  static constexpr int kThreads = 32 * kWarpsM * kWarpsN;
+  // Padding keeps fragment reads conflict-free: the A pitch is 8 banks mod 32 per k row,
+  // the B pitch is 8 banks mod 32 per n column (K2).
+  static constexpr int kLdsA = BM + 4;  // sA[k][m]
+  static constexpr int kLdsB = BK + 4;  // sB[n][k]
+  static constexpr int kStageA = BK * kLdsA;
+  static constexpr int kStageB = BN * kLdsB;
+  static constexpr size_t kSmemBytes = size_t(STAGES) * (kStageA + kStageB) * sizeof(double);
+  static constexpr int kMi = WM / 16, kNi = WN / 8;
+  static constexpr int kLoadA = BM * BK / kThreads;
+  static constexpr int kLoadB = BN * BK / kThreads;
+  static_assert(BM * BK % kThreads == 0 && BN * BK % kThreads == 0, "tile/thread mismatch");
+  static_assert(BK % 4 == 0 && WM % 16 == 0 && WN % 8 == 0, "mma shape");
+};
+
+using GemmBig = GemmCfg<128, 128, 16, 64, 32, 4, 1>;    // 256 threads, batched transforms
+using GemmSmall = GemmCfg<64, 64, 16, 32, 32, 4, 2>;    // 128 threads, single ~1k^3 GEMMs
+
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool valid) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  const int bytes = valid ? 8 : 0;  // 0 => zero-fill, nothing read
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// D = A(16x4, row) * B(4x8, col) + C, FP64.  Fragment layout (PTX ISA, mma.m16n8k4 .f64):
+// g = lane/4, t = lane%4; a0 = A[g][t], a1 = A[g+8][t]; b0 = B[t][g];
+// c0,c1 = C[g][2t, 2t+1], c2,c3 = C[g+8][2t, 2t+1].
+__device__ __forceinline__ void dmma_m16n8k4(double (&c)[4], double a0, double a1, double b) {
+  asm("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, "
+      "{%0,%1,%2,%3};\n"
+      : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+      : "d"(a0), "d"(a1), "d"(b));
+}
+
+template <class Cfg, class Epi>
+__global__ void __launch_bounds__(Cfg::kThreads, Cfg::kMinBlocks)
+    gemm_f64_kernel(const GemmProblem p, const Epi epi) {
+  extern __shared__ __align__(16) double smem[];
+  double* sA = smem;                                   // [STAGES][BK][kLdsA]
+  double* sB = smem + Cfg::STAGES * Cfg::kStageA;      // [STAGES][BN][kLdsB]
+
+  const int64_t tiles_m = (p.M + Cfg::BM - 1) / Cfg::BM;
+  const int64_t tiles_n = (p.N + Cfg::BN - 1) / Cfg::BN;
+  int64_t bid = blockIdx.x;
+  const int64_t tm = bid % tiles_m;
+  bid /= tiles_m;
+  const int64_t tn = bid % tiles_n;
+  const int64_t bt = bid / tiles_n;
+  const int64_t m0 = tm * Cfg::BM, n0 = tn * Cfg::BN;
+
+  const double* A = p.A + bt * p.strideA;
+  const double* B = p.B + bt * p.strideB;
+  double* C = p.C + bt * p.strideC;
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = warp % Cfg::kWarpsM, wn = warp / Cfg::kWarpsM;
+
+  const int64_t ktiles = (p.K + Cfg::BK - 1) / Cfg::BK;
+
+  auto load_stage = [&](int stage, int64_t kt) {
+    const int64_t k0 = kt * Cfg::BK;
+    double* a_dst = sA + stage * Cfg::kStageA;
+    double* b_dst = sB + stage * Cfg::kStageB;
+#pragma unroll
+    for (int i = 0; i < Cfg::kLoadA; ++i) {
+      const int e = tid + i * Cfg::kThreads;
+      const int m = e % Cfg::BM, k = e / Cfg::BM;
+      const bool ok = (m0 + m < p.M) && (k0 + k < p.K);
+      const double* src = ok ? A + (k0 + k) * p.lda + (m0 + m) : A;
+      cp_async8(a_dst + k * Cfg::kLdsA + m, src, ok);
+    }
+#pragma unroll
+    for (int i = 0; i < Cfg::kLoadB; ++i) {
+      const int e = tid + i * Cfg::kThreads;
+      const int k = e % Cfg::BK, n = e / Cfg::BK;
+      const bool ok = (n0 + n < p.N) && (k0 + k < p.K);
+      const double* src = ok ? B + (n0 + n) * p.ldb + (k0 + k) : B;
+      cp_async8(b_dst + n * Cfg::kLdsB + k, src, ok);
+    }
+  };
+
+  double acc[Cfg::kMi][Cfg::kNi][4];
+#pragma unroll
+  for (int mi = 0; mi < Cfg::kMi; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < Cfg::kNi; ++ni)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) acc[mi][ni][r] = 0.0;
+
+#pragma unroll
+  for (int s = 0; s < Cfg::STAGES - 1; ++s) {
+    if (s < ktiles) load_stage(s, s);
+    cp_async_commit();
+  }
+
+  for (int64_t kt = 0; kt < ktiles; ++kt) {
+    cp_async_wait<Cfg::STAGES - 2>();
+    __syncthreads();
+    {
+      const int64_t nk = kt + Cfg::STAGES - 1;
+      if (nk < ktiles) load_stage(static_cast<int>(nk % Cfg::STAGES), nk);
+      cp_async_commit();
+    }
+    const int stage = static_cast<int>(kt % Cfg::STAGES);
+    const double* a_s = sA + stage * Cfg::kStageA;
+    const double* b_s = sB + stage * Cfg::kStageB;
+#pragma unroll
+    for (int kk = 0; kk < Cfg::BK / 4; ++kk) {
+      double af[Cfg::kMi][2], bf[Cfg::kNi];
+      const double* a_row = a_s + (kk * 4 + t) * Cfg::kLdsA + wm * Cfg::WM + g;
+#pragma unroll
+      for (int mi = 0; mi < Cfg::kMi; ++mi) {
+        af[mi][0] = a_row[mi * 16];
+        af[mi][1] = a_row[mi * 16 + 8];
+      }
+      const double* b_col = b_s + (wn * Cfg::WN + g) * Cfg::kLdsB + kk * 4 + t;
+#pragma unroll
+      for (int ni = 0; ni < Cfg::kNi; ++ni) bf[ni] = b_col[ni * 8 * Cfg::kLdsB];
+#pragma unroll
+      for (int mi = 0; mi < Cfg::kMi; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < Cfg::kNi; ++ni) dmma_m16n8k4(acc[mi][ni], af[mi][0], af[mi][1], bf[ni]);
+    }
+  }
+  cp_async_wait<0>();
+
+  // Epilogue: direct stores (each quad of lanes writes 2 adjacent columns of 8 rows).
+#pragma unroll
+  for (int mi = 0; mi < Cfg::kMi; ++mi) {
+#pragma unroll
+    for (int ni = 0; ni < Cfg::kNi; ++ni) {
+      const int64_t r0 = m0 + wm * Cfg::WM + mi * 16 + g;
+      const int64_t c0 = n0 + wn * Cfg::WN + ni * 8 + 2 * t;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int64_t r = r0 + (q >> 1) * 8;
+        const int64_t c = c0 + (q & 1);
+        if (r < p.M && c < p.N) C[c * p.ldc + r] = epi(acc[mi][ni][q], r, c);
+      }
+    }
+  }
+}
+
+template <class Cfg, class Epi>
+void launch_gemm_cfg(const GemmProblem& p, const Epi& epi, cudaStream_t stream) {
+  static const bool configured = [] {  // thread-safe one-time opt-in to >48 KB smem
+    STKG_CUDA_CHECK(cudaFuncSetAttribute(gemm_f64_kernel<Cfg, Epi>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(Cfg::kSmemBytes)));
+    return true;
+  }();
+  (void)configured;
+  const int64_t blocks = ceil_div(p.M, Cfg::BM) * ceil_div(p.N, Cfg::BN) * p.batch;
+  STKG_REQUIRE(blocks < (int64_t(1) << 31), STKG_ARGUMENT, "gemm: grid too large");
+  if (blocks == 0) return;
+  gemm_f64_kernel<Cfg, Epi><<<static_cast<unsigned>(blocks), Cfg::kThreads, Cfg::kSmemBytes,
+                              stream>>>(p, epi);
+  STKG_CUDA_CHECK(cudaGetLastError());
+}
+
+// Tile choice: the 128x128 tile needs >= ~2 waves of CTAs on 148 SMs to stay busy; a
+// single ~1k^3 product has only 64 such tiles, so it takes the 64x64 tile instead.
+template <class Epi>
+void launch_gemm(const GemmProblem& p, const Epi& epi, cudaStream_t stream) {
+  const int64_t big_tiles = ceil_div(p.M, 128) * ceil_div(p.N, 128) * p.batch;
+  if (big_tiles >= 2 * 148)
+    launch_gemm_cfg<GemmBig>(p, epi, stream);
+  else
+    launch_gemm_cfg<GemmSmall>(p, epi, stream);
+}
+
+}  // namespace stkg

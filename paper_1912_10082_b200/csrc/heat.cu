@@ -1,0 +1,661 @@
+// Heat hot path: the exact direct solve of
+//     M U D + A U C = F            (stk/sylvester.hpp:58-65 heat_kron_op)
+// through the tensor generalized eigenbasis, i.e. solve_projected_heat_with
+// (stk/sylvester.hpp:117-142) with X = X_x (x) X_y (x) X_z:
+//   K2  forward transforms  G~ = X^T F      (:126)    -> batched DMMA GEMMs per axis
+//   K3  per-mode recurrence (D + lambda_i C)^T y_i = g~_i   (:128-140) -> mode-parallel scan
+//   K2  inverse transforms  U = X Y~        (:141)
+// and the K1 operator/residual kernel  out = M U D + A U C  (KronOp::apply, :32-38).
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "gemm_f64.cuh"
+
+using namespace stkg;
+
+struct stkg_heat {
+  int ndim = 0;
+  int64_t n[3] = {1, 1, 1};
+  int64_t nt = 0;
+  int64_t nx = 0;  // spatial unknowns
+  cudaStream_t stream = nullptr;
+  DevBuf X[3], XT[3], lam[3];
+  DevBuf d_diag, d_sup, c_diag, c_sup;
+  bool has_operator = false;
+  DevBuf m_diag[3], m_off[3], a_diag[3], a_off[3];
+  DevBuf scratch;   // nx * nt, device solve
+  DevBuf carry;     // nx, modal state y_{l0-1} carried across time chunks
+  DevBuf partials;  // reduction partials
+  DevBuf scalars;   // device results of reductions
+  double* pinned = nullptr;  // host mirror of scalars
+  int singular = 0;
+  double singular_lambda = 0.0;
+  int64_t singular_step = 0;
+  // host-buffer pipeline
+  int64_t time_chunk = 0;
+  DevBuf pf[2], pu[2], ps;
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+  cudaEvent_t ev_h2d[2] = {}, ev_comp[2] = {}, ev_d2h[2] = {};
+  // kernel-class profiling (stkg_heat_profile)
+  bool prof_on = false;
+  std::vector<cudaEvent_t> prof_ev[2];  // begin/end pairs per class
+  int64_t prof_launches[2] = {0, 0};
+};
+
+namespace {
+
+// ------------------------------------------------------------------------------ K3 --
+// One thread per mode i: y_j = (g~_j - (d_sup[j-1] + lam_i c_sup[j-1]) y_{j-1}) /
+// (d_diag[j] + lam_i c_diag[j]) -- the forward substitution of stk/sylvester.hpp:131-139,
+// with lam_i = lam_x[ix] + lam_y[iy] (+ lam_z[iz]).  Loads of g~ are independent of the
+// carried y, so the unrolled loop keeps many of them in flight (HBM-bound, 16 B/unknown).
+struct ModeLambda {
+  const double* l0;
+  const double* l1;
+  const double* l2;
+  int64_t n1, n2;
+  int ndim;
+  __device__ __forceinline__ double operator()(int64_t i) const {
+    if (ndim == 1) return l0[i];
+    if (ndim == 2) return l0[i / n1] + l1[i % n1];
+    const int64_t iz = i % n2, r = i / n2;
+    return l0[r / n1] + l1[r % n1] + l2[iz];
+  }
+};
+
+__global__ void __launch_bounds__(256) heat_scan_kernel(
+    double* __restrict__ Y, int64_t nx, int64_t ntc, int64_t l0, ModeLambda lam,
+    const double* __restrict__ d_diag, const double* __restrict__ d_sup,
+    const double* __restrict__ c_diag, const double* __restrict__ c_sup,
+    double* __restrict__ carry) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= nx) return;
+  const double li = lam(i);
+  double y = l0 > 0 ? carry[i] : 0.0;
+  double* col = Y + i;
+  constexpr int U = 8;
+  int64_t j = 0;
+  for (; j + U <= ntc; j += U) {
+    double g[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) g[u] = __ldcs(col + (j + u) * nx);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t l = l0 + j + u;
+      const double piv = d_diag[l] + li * c_diag[l];
+      double rhs = g[u];
+      if (l > 0) rhs -= (d_sup[l - 1] + li * c_sup[l - 1]) * y;
+      y = rhs / piv;
+      __stcs(col + (j + u) * nx, y);
+    }
+  }
+  for (; j < ntc; ++j) {
+    const int64_t l = l0 + j;
+    const double piv = d_diag[l] + li * c_diag[l];
+    double rhs = col[j * nx];
+    if (l > 0) rhs -= (d_sup[l - 1] + li * c_sup[l - 1]) * y;
+    y = rhs / piv;
+    col[j * nx] = y;
+  }
+  carry[i] = y;
+}
+
+// Singularity check of stk/sylvester.hpp:133-135, done once per plan: min over modes and
+// steps of |d_j + lambda_i c_j|.  Writes the first offending (i, j) it finds.
+__global__ void heat_pivot_check_kernel(int64_t nx, int64_t nt, ModeLambda lam,
+                                        const double* d_diag, const double* c_diag,
+                                        unsigned long long* bad) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= nx) return;
+  const double li = lam(i);
+  for (int64_t l = 0; l < nt; ++l) {
+    const double piv = d_diag[l] + li * c_diag[l];
+    if (fabs(piv) < 1e-300) {
+      atomicMin(bad, (unsigned long long)(l * nx + i));
+      return;
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------ K1 --
+// out_l = M (d_l U_l + ds_{l-1} U_{l-1}) + A (c_l U_l + cs_{l-1} U_{l-1}),
+// M = (x) M_a, A = sum_a A_a (x) M_others (fem2d_matrices, stk/discretize.hpp:81-88).
+// One thread per spatial point, looping over time; the stencil values of U_{l-1} stay in
+// registers, so U and F are each read once from HBM (16 B/unknown).
+struct Tri {  // symmetric tridiagonal 1D factor
+  const double* diag;
+  const double* off;
+  __device__ __forceinline__ double w(int64_t i, int q) const {  // entry (i, i+q), q in -1..1
+    return q == 0 ? diag[i] : (q < 0 ? off[i - 1] : off[i]);
+  }
+};
+
+template <int NDIM, bool RESIDUAL>
+__global__ void __launch_bounds__(256) heat_apply_kernel(
+    const double* __restrict__ U, const double* __restrict__ F, double* __restrict__ out,
+    int64_t n0, int64_t n1, int64_t n2, int64_t nt, Tri m0, Tri m1, Tri m2, Tri a0, Tri a1,
+    Tri a2, const double* __restrict__ d_diag, const double* __restrict__ d_sup,
+    const double* __restrict__ c_diag, const double* __restrict__ c_sup,
+    double* __restrict__ partials) {
+  // sum-factorised stencil: z sums, then y sums, then x sums (SURVEY §8(d) K1 note)
+  constexpr int SY = NDIM >= 2 ? 3 : 1, SZ = NDIM == 3 ? 3 : 1;
+  const int64_t nx = n0 * n1 * n2;
+  const int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  double rr = 0.0, ff = 0.0;
+  if (p < nx) {
+    int64_t ix, iy = 0, iz = 0;
+    if (NDIM == 1) {
+      ix = p;
+    } else if (NDIM == 2) {
+      ix = p / n1;
+      iy = p % n1;
+    } else {
+      iz = p % n2;
+      const int64_t r = p / n2;
+      iy = r % n1;
+      ix = r / n1;
+    }
+    double wmx[3], wax[3], wmy[SY], way[SY], wmz[SZ], waz[SZ];
+    bool inx[3], iny[SY], inz[SZ];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const bool in = ix + q - 1 >= 0 && ix + q - 1 < n0;
+      inx[q] = in;
+      wmx[q] = in ? m0.w(ix, q - 1) : 0.0;
+      wax[q] = in ? a0.w(ix, q - 1) : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < SY; ++q) {
+      const int d = SY == 1 ? 0 : q - 1;
+      const bool in = iy + d >= 0 && iy + d < n1;
+      iny[q] = in;
+      wmy[q] = NDIM >= 2 ? (in ? m1.w(iy, d) : 0.0) : 1.0;
+      way[q] = NDIM >= 2 ? (in ? a1.w(iy, d) : 0.0) : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < SZ; ++q) {
+      const int d = SZ == 1 ? 0 : q - 1;
+      const bool in = iz + d >= 0 && iz + d < n2;
+      inz[q] = in;
+      wmz[q] = NDIM == 3 ? (in ? m2.w(iz, d) : 0.0) : 1.0;
+      waz[q] = NDIM == 3 ? (in ? a2.w(iz, d) : 0.0) : 0.0;
+    }
+    double prev[3 * SY * SZ];
+#pragma unroll
+    for (int s = 0; s < 3 * SY * SZ; ++s) prev[s] = 0.0;
+    for (int64_t l = 0; l < nt; ++l) {
+      const double* Ul = U + l * nx + p;
+      const double dd = d_diag[l], cd = c_diag[l];
+      const double ds = l > 0 ? d_sup[l - 1] : 0.0, cs = l > 0 ? c_sup[l - 1] : 0.0;
+      double acc = 0.0;
+#pragma unroll
+      for (int qx = 0; qx < 3; ++qx) {
+        double ymp = 0.0, ymq = 0.0, yaq = 0.0;
+#pragma unroll
+        for (int qy = 0; qy < SY; ++qy) {
+          double zmp = 0.0, zmq = 0.0, zaq = 0.0;
+#pragma unroll
+          for (int qz = 0; qz < SZ; ++qz) {
+            const int s = (qx * SY + qy) * SZ + qz;
+            const int64_t delta = (qx - 1) * n1 * n2 + (SY == 1 ? 0 : (qy - 1) * n2) +
+                                  (SZ == 1 ? 0 : qz - 1);
+            const bool in = inx[qx] && iny[qy] && inz[qz];
+            const double u = in ? __ldg(Ul + delta) : 0.0;
+            const double P = dd * u + ds * prev[s];
+            const double Q = cd * u + cs * prev[s];
+            prev[s] = u;
+            zmp += wmz[qz] * P;
+            zmq += wmz[qz] * Q;
+            zaq += waz[qz] * Q;
+          }
+          ymp += wmy[qy] * zmp;
+          ymq += wmy[qy] * zmq;
+          yaq += way[qy] * zmq + wmy[qy] * zaq;
+        }
+        acc += wmx[qx] * ymp + wax[qx] * ymq + wmx[qx] * yaq;
+      }
+      if (RESIDUAL) {
+        const double f = __ldcs(F + l * nx + p);
+        const double r = f - acc;
+        rr += r * r;
+        ff += f * f;
+      } else {
+        out[l * nx + p] = acc;
+      }
+    }
+  }
+  if (RESIDUAL) {
+    __shared__ double red[8];
+    rr = block_sum<256>(rr, red);
+    ff = block_sum<256>(ff, red);
+    if (threadIdx.x == 0) {
+      partials[2 * blockIdx.x] = rr;
+      partials[2 * blockIdx.x + 1] = ff;
+    }
+  }
+}
+
+// Sum interleaved partial pairs in a fixed order (deterministic).
+__global__ void __launch_bounds__(256) sum_pairs_kernel(const double* partials, int64_t count,
+                                                        double* result) {
+  __shared__ double red[8];
+  double a = 0.0, b = 0.0;
+  for (int64_t i = threadIdx.x; i < count; i += 256) {
+    a += partials[2 * i];
+    b += partials[2 * i + 1];
+  }
+  a = block_sum<256>(a, red);
+  b = block_sum<256>(b, red);
+  if (threadIdx.x == 0) {
+    result[0] = a;
+    result[1] = b;
+  }
+}
+
+__global__ void fill_uniform_kernel(double* dst, int64_t count, uint64_t seed, uint64_t stream,
+                                    int64_t offset) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
+       i += int64_t(gridDim.x) * blockDim.x)
+    dst[i] = uniform_pm1(seed, stream, uint64_t(offset + i));
+}
+
+ModeLambda mode_lambda(const stkg_heat& h) {
+  return ModeLambda{h.lam[0].p, h.ndim > 1 ? h.lam[1].p : nullptr,
+                    h.ndim > 2 ? h.lam[2].p : nullptr, h.n[1], h.n[2], h.ndim};
+}
+
+// One axis transform over a block of ntc time slices.  Axis a with inner extent
+// I = prod_{b>a} n_b: the fastest axis (I == 1) is a left product  Op * data(n_a x rest);
+// every other axis is a batched right product  data_b(I x n_a) * Op'  (SURVEY Appendix A:
+// G~_l = X_y^T F_l X_x in column-major slices).
+struct ProfScope {  // records a begin/end event pair around one launch when profiling
+  stkg_heat& h;
+  int cls;
+  cudaEvent_t e1 = nullptr;
+  ProfScope(stkg_heat& hh, int c) : h(hh), cls(c) {
+    if (!h.prof_on) return;
+    cudaEvent_t e0;
+    STKG_CUDA_CHECK(cudaEventCreate(&e0));
+    STKG_CUDA_CHECK(cudaEventCreate(&e1));
+    STKG_CUDA_CHECK(cudaEventRecord(e0, h.stream));
+    h.prof_ev[cls].push_back(e0);
+    h.prof_ev[cls].push_back(e1);
+  }
+  ~ProfScope() {
+    if (!h.prof_on) return;
+    cudaEventRecord(e1, h.stream);
+    h.prof_launches[cls]++;
+  }
+};
+
+void axis_pass(stkg_heat& h, int a, bool forward, const double* src, double* dst,
+               int64_t ntc) {
+  int64_t inner = 1, outer = ntc;
+  for (int b = a + 1; b < h.ndim; ++b) inner *= h.n[b];
+  for (int b = 0; b < a; ++b) outer *= h.n[b];
+  const int64_t na = h.n[a];
+  GemmProblem p;
+  if (inner == 1) {
+    p.M = na;
+    p.K = na;
+    p.N = outer;
+    p.A = forward ? h.XT[a].p : h.X[a].p;
+    p.lda = na;
+    p.B = src;
+    p.ldb = na;
+    p.C = dst;
+    p.ldc = na;
+  } else {
+    p.M = inner;
+    p.K = na;
+    p.N = na;
+    p.batch = outer;
+    p.A = src;
+    p.lda = inner;
+    p.strideA = inner * na;
+    p.B = forward ? h.X[a].p : h.XT[a].p;
+    p.ldb = na;
+    p.C = dst;
+    p.ldc = inner;
+    p.strideC = inner * na;
+  }
+  ProfScope ps(h, 0);
+  launch_gemm(p, EpiStore{}, h.stream);
+}
+
+// Full solve of ntc time slices starting at l0 (carry holds y_{l0-1} when l0 > 0).
+// Passes alternate between U and S so that the last inverse pass lands in U.
+void run_chunk(stkg_heat& h, const double* F, double* U, double* S, int64_t l0, int64_t ntc) {
+  const int d = h.ndim, passes = 2 * d;
+  const double* src = F;
+  int k = 0;
+  auto next_dst = [&](int kk) { return ((passes - kk) % 2 == 0) ? U : S; };
+  for (int a = d - 1; a >= 0; --a) {  // forward, fastest axis first
+    double* dst = next_dst(++k);
+    axis_pass(h, a, true, src, dst, ntc);
+    src = dst;
+  }
+  {
+    double* Y = const_cast<double*>(src);
+    const int64_t blocks = ceil_div(h.nx, 256);
+    ProfScope ps(h, 1);
+    heat_scan_kernel<<<static_cast<unsigned>(blocks), 256, 0, h.stream>>>(
+        Y, h.nx, ntc, l0, mode_lambda(h), h.d_diag.p, h.d_sup.p, h.c_diag.p, h.c_sup.p,
+        h.carry.p);
+    STKG_CUDA_CHECK(cudaGetLastError());
+  }
+  for (int a = 0; a < d; ++a) {  // inverse, slowest axis first
+    double* dst = next_dst(++k);
+    axis_pass(h, a, false, src, dst, ntc);
+    src = dst;
+  }
+}
+
+void check_solvable(const stkg_heat& h) {
+  if (h.singular) {
+    char buf[160];
+    snprintf(buf, sizeof buf, "solve_projected_heat: singular row system at lambda = %f",
+             h.singular_lambda);
+    throw Error(STKG_SINGULARITY, buf);
+  }
+}
+
+template <int NDIM, bool RES>
+void launch_apply(stkg_heat& h, const double* U, const double* F, double* out) {
+  const unsigned blocks = static_cast<unsigned>(ceil_div(h.nx, 256));
+  Tri m[3], a[3];
+  for (int i = 0; i < 3; ++i) {
+    m[i] = Tri{h.m_diag[i].p, h.m_off[i].p};
+    a[i] = Tri{h.a_diag[i].p, h.a_off[i].p};
+  }
+  heat_apply_kernel<NDIM, RES><<<blocks, 256, 0, h.stream>>>(
+      U, F, out, h.n[0], h.n[1], h.n[2], h.nt, m[0], m[1], m[2], a[0], a[1], a[2], h.d_diag.p,
+      h.d_sup.p, h.c_diag.p, h.c_sup.p, h.partials.p);
+  STKG_CUDA_CHECK(cudaGetLastError());
+}
+
+template <bool RES>
+void dispatch_apply(stkg_heat& h, const double* U, const double* F, double* out) {
+  if (h.ndim == 1) launch_apply<1, RES>(h, U, F, out);
+  else if (h.ndim == 2) launch_apply<2, RES>(h, U, F, out);
+  else launch_apply<3, RES>(h, U, F, out);
+}
+
+std::vector<double> transpose(const double* X, int64_t n) {
+  std::vector<double> t(static_cast<size_t>(n * n));
+  for (int64_t j = 0; j < n; ++j)
+    for (int64_t i = 0; i < n; ++i) t[i * n + j] = X[j * n + i];
+  return t;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------------ C ABI -----
+extern "C" {
+
+int stkg_fill_uniform(double* dst, int64_t count, uint64_t seed, uint64_t stream,
+                      int64_t index_offset, void* cuda_stream) {
+  return guarded([&] {
+    STKG_REQUIRE(count >= 0 && (dst || count == 0), STKG_ARGUMENT, "fill_uniform: bad args");
+    if (count == 0) return;
+    fill_uniform_kernel<<<148 * 8, 256, 0, static_cast<cudaStream_t>(cuda_stream)>>>(
+        dst, count, seed, stream, index_offset);
+    STKG_CUDA_CHECK(cudaGetLastError());
+  });
+}
+
+int stkg_heat_create(stkg_heat** out, const stkg_heat_desc* desc, void* cuda_stream) {
+  return guarded([&] {
+    STKG_REQUIRE(out && desc, STKG_ARGUMENT, "stkg_heat_create: null argument");
+    *out = nullptr;
+    STKG_REQUIRE(desc->ndim >= 1 && desc->ndim <= 3, STKG_ARGUMENT,
+                 "stkg_heat_create: ndim must be 1, 2 or 3");
+    STKG_REQUIRE(desc->nt >= 1, STKG_ARGUMENT, "stkg_heat_create: nt must be >= 1");
+    auto h = std::make_unique<stkg_heat>();
+    h->ndim = desc->ndim;
+    h->nt = desc->nt;
+    h->nx = 1;
+    for (int a = 0; a < h->ndim; ++a) {
+      STKG_REQUIRE(desc->n[a] >= 1, STKG_ARGUMENT, "stkg_heat_create: n must be >= 1");
+      STKG_REQUIRE(desc->X[a] && desc->lambdas[a], STKG_ARGUMENT,
+                   "stkg_heat_create: missing EigPair for an axis");
+      h->n[a] = desc->n[a];
+      h->nx *= desc->n[a];
+    }
+    STKG_REQUIRE(desc->d_diag && desc->c_diag && (desc->nt == 1 || (desc->d_sup && desc->c_sup)),
+                 STKG_ARGUMENT, "stkg_heat_create: missing temporal bidiagonals");
+    h->stream = static_cast<cudaStream_t>(cuda_stream);
+    cudaStream_t s = h->stream;
+    for (int a = 0; a < h->ndim; ++a) {
+      const int64_t na = h->n[a];
+      h->X[a].alloc(na * na);
+      h->X[a].upload(desc->X[a], na * na, s);
+      auto t = transpose(desc->X[a], na);
+      h->XT[a].alloc(na * na);
+      h->XT[a].upload(t.data(), na * na, s);
+      h->lam[a].alloc(na);
+      h->lam[a].upload(desc->lambdas[a], na, s);
+      STKG_CUDA_CHECK(cudaStreamSynchronize(s));  // host temporaries die here
+    }
+    const int64_t nt = h->nt;
+    h->d_diag.alloc(nt);
+    h->d_diag.upload(desc->d_diag, nt, s);
+    h->c_diag.alloc(nt);
+    h->c_diag.upload(desc->c_diag, nt, s);
+    h->d_sup.alloc(std::max<int64_t>(nt - 1, 1));
+    h->c_sup.alloc(std::max<int64_t>(nt - 1, 1));
+    if (nt > 1) {
+      h->d_sup.upload(desc->d_sup, nt - 1, s);
+      h->c_sup.upload(desc->c_sup, nt - 1, s);
+    }
+    bool op = true;
+    for (int a = 0; a < h->ndim; ++a)
+      op = op && desc->m_diag[a] && desc->a_diag[a] &&
+           (h->n[a] == 1 || (desc->m_off[a] && desc->a_off[a]));
+    h->has_operator = op;
+    for (int a = 0; a < 3; ++a) {
+      // unused axes get the 1x1 identity/zero factors so the stencil code is uniform
+      const int64_t na = a < h->ndim ? h->n[a] : 1;
+      h->m_diag[a].alloc(na);
+      h->a_diag[a].alloc(na);
+      h->m_off[a].alloc(std::max<int64_t>(na - 1, 1));
+      h->a_off[a].alloc(std::max<int64_t>(na - 1, 1));
+      if (a < h->ndim && op) {
+        h->m_diag[a].upload(desc->m_diag[a], na, s);
+        h->a_diag[a].upload(desc->a_diag[a], na, s);
+        if (na > 1) {
+          h->m_off[a].upload(desc->m_off[a], na - 1, s);
+          h->a_off[a].upload(desc->a_off[a], na - 1, s);
+        }
+      } else if (a >= h->ndim) {
+        const double one = 1.0, zero = 0.0;
+        STKG_CUDA_CHECK(cudaMemcpyAsync(h->m_diag[a].p, &one, 8, cudaMemcpyHostToDevice, s));
+        STKG_CUDA_CHECK(cudaMemcpyAsync(h->a_diag[a].p, &zero, 8, cudaMemcpyHostToDevice, s));
+        STKG_CUDA_CHECK(cudaStreamSynchronize(s));
+      }
+    }
+    h->carry.alloc(h->nx);
+    h->partials.alloc(2 * ceil_div(h->nx, 256));
+    h->scalars.alloc(4);
+    STKG_CUDA_CHECK(cudaMallocHost(&h->pinned, 4 * sizeof(double)));
+    h->time_chunk = desc->time_chunk;
+
+    // one-time pivot check (stk/sylvester.hpp:133-135)
+    unsigned long long* bad = nullptr;
+    STKG_CUDA_CHECK(cudaMalloc(&bad, sizeof(unsigned long long)));
+    STKG_CUDA_CHECK(cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), s));
+    heat_pivot_check_kernel<<<static_cast<unsigned>(ceil_div(h->nx, 256)), 256, 0, s>>>(
+        h->nx, h->nt, mode_lambda(*h), h->d_diag.p, h->c_diag.p, bad);
+    STKG_CUDA_CHECK(cudaGetLastError());
+    unsigned long long hb = 0;
+    STKG_CUDA_CHECK(cudaMemcpyAsync(&hb, bad, sizeof hb, cudaMemcpyDeviceToHost, s));
+    STKG_CUDA_CHECK(cudaStreamSynchronize(s));
+    cudaFree(bad);
+    if (hb != ~0ull) {
+      h->singular = 1;
+      const int64_t i = static_cast<int64_t>(hb % static_cast<unsigned long long>(h->nx));
+      h->singular_step = static_cast<int64_t>(hb / static_cast<unsigned long long>(h->nx));
+      // reconstruct lambda_i on the host for the message
+      std::vector<double> li(1);
+      int64_t idx[3] = {i, 0, 0};
+      if (h->ndim == 2) idx[0] = i / h->n[1], idx[1] = i % h->n[1];
+      if (h->ndim == 3) idx[2] = i % h->n[2], idx[1] = (i / h->n[2]) % h->n[1],
+                        idx[0] = i / (h->n[1] * h->n[2]);
+      double lam = 0.0;
+      for (int a = 0; a < h->ndim; ++a) lam += desc->lambdas[a][idx[a]];
+      h->singular_lambda = lam;
+    }
+    *out = h.release();
+  });
+}
+
+int stkg_heat_destroy(stkg_heat* h) {
+  return guarded([&] {
+    if (!h) return;
+    if (h->stream) cudaStreamSynchronize(h->stream);
+    else cudaDeviceSynchronize();
+    if (h->pinned) cudaFreeHost(h->pinned);
+    for (int b = 0; b < 2; ++b) {
+      if (h->ev_h2d[b]) cudaEventDestroy(h->ev_h2d[b]);
+      if (h->ev_comp[b]) cudaEventDestroy(h->ev_comp[b]);
+      if (h->ev_d2h[b]) cudaEventDestroy(h->ev_d2h[b]);
+    }
+    if (h->s_h2d) cudaStreamDestroy(h->s_h2d);
+    if (h->s_d2h) cudaStreamDestroy(h->s_d2h);
+    delete h;
+  });
+}
+
+int64_t stkg_heat_workspace_bytes(const stkg_heat* h) {
+  if (!h) return 0;
+  int64_t b = 0;
+  const DevBuf* bufs[] = {&h->scratch, &h->carry, &h->partials, &h->pf[0], &h->pf[1],
+                          &h->pu[0],   &h->pu[1], &h->ps};
+  for (auto* x : bufs) b += static_cast<int64_t>(x->n) * 8;
+  for (int a = 0; a < h->ndim; ++a) b += static_cast<int64_t>(2 * h->X[a].n + h->lam[a].n) * 8;
+  return b;
+}
+
+int stkg_heat_solve(stkg_heat* h, const double* F, double* U) {
+  return guarded([&] {
+    STKG_REQUIRE(h && F && U, STKG_ARGUMENT, "stkg_heat_solve: null argument");
+    STKG_REQUIRE(F != U, STKG_ARGUMENT, "stkg_heat_solve: U may not alias F");
+    check_solvable(*h);
+    if (h->scratch.n < static_cast<size_t>(h->nx * h->nt)) h->scratch.alloc(h->nx * h->nt);
+    run_chunk(*h, F, U, h->scratch.p, 0, h->nt);
+  });
+}
+
+int stkg_heat_solve_host(stkg_heat* h, const double* F_host, double* U_host) {
+  return guarded([&] {
+    STKG_REQUIRE(h && F_host && U_host, STKG_ARGUMENT, "stkg_heat_solve_host: null argument");
+    check_solvable(*h);
+    int64_t tc = h->time_chunk;
+    if (tc <= 0) tc = std::max<int64_t>(1, (int64_t(256) << 20) / (h->nx * 8));
+    tc = std::min(tc, h->nt);
+    const int64_t chunk_elems = h->nx * tc;
+    if (h->ps.n < static_cast<size_t>(chunk_elems)) {
+      for (int b = 0; b < 2; ++b) {
+        h->pf[b].alloc(chunk_elems);
+        h->pu[b].alloc(chunk_elems);
+      }
+      h->ps.alloc(chunk_elems);
+    }
+    if (!h->s_h2d) {
+      STKG_CUDA_CHECK(cudaStreamCreateWithFlags(&h->s_h2d, cudaStreamNonBlocking));
+      STKG_CUDA_CHECK(cudaStreamCreateWithFlags(&h->s_d2h, cudaStreamNonBlocking));
+      for (int b = 0; b < 2; ++b) {
+        STKG_CUDA_CHECK(cudaEventCreateWithFlags(&h->ev_h2d[b], cudaEventDisableTiming));
+        STKG_CUDA_CHECK(cudaEventCreateWithFlags(&h->ev_comp[b], cudaEventDisableTiming));
+        STKG_CUDA_CHECK(cudaEventCreateWithFlags(&h->ev_d2h[b], cudaEventDisableTiming));
+      }
+    }
+    const int64_t nchunks = ceil_div(h->nt, tc);
+    for (int64_t c = 0; c < nchunks; ++c) {
+      const int b = static_cast<int>(c & 1);
+      const int64_t l0 = c * tc, ntc = std::min(tc, h->nt - l0);
+      const size_t bytes = static_cast<size_t>(h->nx * ntc) * sizeof(double);
+      if (c >= 2) STKG_CUDA_CHECK(cudaStreamWaitEvent(h->s_h2d, h->ev_comp[b], 0));
+      STKG_CUDA_CHECK(cudaMemcpyAsync(h->pf[b].p, F_host + l0 * h->nx, bytes,
+                                      cudaMemcpyHostToDevice, h->s_h2d));
+      STKG_CUDA_CHECK(cudaEventRecord(h->ev_h2d[b], h->s_h2d));
+      STKG_CUDA_CHECK(cudaStreamWaitEvent(h->stream, h->ev_h2d[b], 0));
+      if (c >= 2) STKG_CUDA_CHECK(cudaStreamWaitEvent(h->stream, h->ev_d2h[b], 0));
+      run_chunk(*h, h->pf[b].p, h->pu[b].p, h->ps.p, l0, ntc);
+      STKG_CUDA_CHECK(cudaEventRecord(h->ev_comp[b], h->stream));
+      STKG_CUDA_CHECK(cudaStreamWaitEvent(h->s_d2h, h->ev_comp[b], 0));
+      STKG_CUDA_CHECK(cudaMemcpyAsync(U_host + l0 * h->nx, h->pu[b].p, bytes,
+                                      cudaMemcpyDeviceToHost, h->s_d2h));
+      STKG_CUDA_CHECK(cudaEventRecord(h->ev_d2h[b], h->s_d2h));
+    }
+    STKG_CUDA_CHECK(cudaStreamSynchronize(h->s_d2h));
+    STKG_CUDA_CHECK(cudaStreamSynchronize(h->stream));
+  });
+}
+
+int stkg_heat_profile(stkg_heat* h, int enable, double* ms_out, int64_t* launches_out) {
+  return guarded([&] {
+    STKG_REQUIRE(h, STKG_ARGUMENT, "stkg_heat_profile: null plan");
+    auto drop = [&] {
+      for (int c = 0; c < 2; ++c) {
+        for (auto e : h->prof_ev[c]) cudaEventDestroy(e);
+        h->prof_ev[c].clear();
+      }
+    };
+    if (enable) {
+      drop();
+      h->prof_launches[0] = h->prof_launches[1] = 0;
+      h->prof_on = true;
+      return;
+    }
+    h->prof_on = false;
+    STKG_CUDA_CHECK(cudaStreamSynchronize(h->stream));
+    for (int c = 0; c < 2; ++c) {
+      double ms = 0.0;
+      for (size_t i = 0; i + 1 < h->prof_ev[c].size(); i += 2) {
+        float t = 0.f;
+        STKG_CUDA_CHECK(cudaEventElapsedTime(&t, h->prof_ev[c][i], h->prof_ev[c][i + 1]));
+        ms += t;
+      }
+      if (ms_out) ms_out[c] = ms;
+      if (launches_out) launches_out[c] = h->prof_launches[c];
+    }
+    drop();
+  });
+}
+
+int stkg_heat_apply(stkg_heat* h, const double* U, double* out) {
+  return guarded([&] {
+    STKG_REQUIRE(h && U && out, STKG_ARGUMENT, "stkg_heat_apply: null argument");
+    STKG_REQUIRE(h->has_operator, STKG_ARGUMENT,
+                 "stkg_heat_apply: plan was created without the spatial factors");
+    STKG_REQUIRE(U != out, STKG_ARGUMENT, "stkg_heat_apply: out may not alias U");
+    dispatch_apply<false>(*h, U, nullptr, out);
+  });
+}
+
+int stkg_heat_residual(stkg_heat* h, const double* U, const double* F, double* relres,
+                       double* fnorm) {
+  return guarded([&] {
+    STKG_REQUIRE(h && U && F, STKG_ARGUMENT, "stkg_heat_residual: null argument");
+    STKG_REQUIRE(h->has_operator, STKG_ARGUMENT,
+                 "stkg_heat_residual: plan was created without the spatial factors");
+    dispatch_apply<true>(*h, U, F, nullptr);
+    sum_pairs_kernel<<<1, 256, 0, h->stream>>>(h->partials.p, ceil_div(h->nx, 256), h->scalars.p);
+    STKG_CUDA_CHECK(cudaGetLastError());
+    STKG_CUDA_CHECK(cudaMemcpyAsync(h->pinned, h->scalars.p, 2 * sizeof(double),
+                                    cudaMemcpyDeviceToHost, h->stream));
+    STKG_CUDA_CHECK(cudaStreamSynchronize(h->stream));
+    const double rn = std::sqrt(h->pinned[0]), fn = std::sqrt(h->pinned[1]);
+    if (fnorm) *fnorm = fn;
+    if (relres) *relres = fn > 0 ? rn / fn : rn;
+  });
+}
+
+}  // extern "C"

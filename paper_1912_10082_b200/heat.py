@@ -1,0 +1,215 @@
+"""Heat hot path: the Python mirror of solve_projected_heat_with / KronOp over the C ABI.
+
+Reference interface (stk/sylvester.hpp):
+  * ``solve_projected_heat_with(eig, d, c, g)``  :117-142
+  * ``heat_kron_op(m_h, a_h, d, c)`` / ``KronOp.apply(x)``  :58-65, :32-38
+  * ``residual`` = ||F - KronOp.apply(U)||_F / ||F||_F  (stk/bench.hpp:508,524)
+
+Layout: U and F are N_h x N_t column-major (space fastest), i.e. a contiguous buffer of
+N_h * N_t doubles; as torch/numpy arrays that is shape (N_t, N_h) in C order.  The tensor
+spatial index is ix*ny + iy (+ z fastest in 3D), the order of sparse_kron.
+
+Device tensors (torch.float64 on CUDA) go through ``stkg_heat_solve``; host numpy arrays
+go through ``stkg_heat_solve_host`` (H2D / solve / D2H pipelined over time chunks).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Sequence
+
+import numpy as np
+
+from ._lib import HeatDesc, lib
+from .assembly import Bidiagonal, EigPair, Tridiagonal
+from .errors import ArgumentError, check
+
+_dp = C.POINTER(C.c_double)
+
+
+def _np_ptr(a: np.ndarray):
+    return a.ctypes.data_as(_dp)
+
+
+def _dev_ptr(t) -> int:
+    import torch
+    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float64):
+        raise ArgumentError("expected a torch.float64 CUDA tensor")
+    if not t.is_contiguous():
+        raise ArgumentError("expected a contiguous tensor")
+    return t.data_ptr()
+
+
+def _stream_handle(stream):
+    if stream is None:
+        import torch
+        if torch.cuda.is_available():
+            return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        return C.c_void_p(0)
+    return C.c_void_p(int(stream))
+
+
+@dataclass
+class TensorEigPair:
+    """EigPair of the Kronecker pencil: X = X_x (x) X_y (x) X_z, lambda = l_x (+) l_y (+) l_z."""
+    axes: Sequence[EigPair]
+
+    @property
+    def shape(self):
+        return tuple(int(e.lambdas.size) for e in self.axes)
+
+
+class HeatPlan:
+    """Prepared heat system on the GPU: tensor EigPair + temporal bidiagonals (+ the 1D
+    spatial tridiagonals that define KronOp for apply/residual)."""
+
+    def __init__(self, eig: TensorEigPair | EigPair, d: Bidiagonal, c: Bidiagonal,
+                 m_axes: Sequence[Tridiagonal] | None = None,
+                 a_axes: Sequence[Tridiagonal] | None = None, stream=None, time_chunk: int = 0):
+        if isinstance(eig, EigPair):
+            eig = TensorEigPair([eig])
+        axes = list(eig.axes)
+        ndim = len(axes)
+        if not 1 <= ndim <= 3:
+            raise ArgumentError("HeatPlan: 1 to 3 spatial axes")
+        self.n = [int(e.lambdas.size) for e in axes]
+        self.nt = int(d.diag.size)
+        if c.diag.size != self.nt:
+            raise ArgumentError("solve_projected_heat: D and C sizes differ")
+        self.nx = int(np.prod(self.n))
+        keep = []  # host arrays must outlive the create call
+
+        def arr(a):
+            a = np.ascontiguousarray(a, dtype=np.float64)
+            keep.append(a)
+            return _np_ptr(a)
+
+        desc = HeatDesc()
+        desc.ndim = ndim
+        for i in range(3):
+            desc.n[i] = self.n[i] if i < ndim else 1
+        desc.nt = self.nt
+        desc.d_diag, desc.c_diag = arr(d.diag), arr(c.diag)
+        desc.d_sup = arr(d.sup if d.sup.size else np.zeros(1))
+        desc.c_sup = arr(c.sup if c.sup.size else np.zeros(1))
+        for i, e in enumerate(axes):
+            X = np.asfortranarray(e.X, dtype=np.float64)
+            if X.shape != (self.n[i], self.n[i]):
+                raise ArgumentError("solve_projected_heat: EigPair X shape mismatch")
+            keep.append(X)
+            desc.X[i] = _np_ptr(X)
+            desc.lambdas[i] = arr(e.lambdas)
+        if m_axes is not None and a_axes is not None:
+            for i in range(ndim):
+                desc.m_diag[i] = arr(m_axes[i].diag)
+                desc.m_off[i] = arr(m_axes[i].off if m_axes[i].off.size else np.zeros(1))
+                desc.a_diag[i] = arr(a_axes[i].diag)
+                desc.a_off[i] = arr(a_axes[i].off if a_axes[i].off.size else np.zeros(1))
+        desc.time_chunk = int(time_chunk)
+        self._stream = _stream_handle(stream)
+        h = C.c_void_p()
+        check(lib.stkg_heat_create(C.byref(h), C.byref(desc), self._stream))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            check(lib.stkg_heat_destroy(self._h))
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def workspace_bytes(self) -> int:
+        return int(lib.stkg_heat_workspace_bytes(self._h))
+
+    def _check_size(self, t):
+        n = t.numel() if hasattr(t, "numel") else t.size
+        if n != self.nx * self.nt:
+            raise ArgumentError("solve_projected_heat: G shape mismatch")
+
+    # -- device path ----------------------------------------------------------------
+    def solve(self, F, out=None):
+        """U = solve_projected_heat_with(eig, d, c, F) on device tensors."""
+        import torch
+        self._check_size(F)
+        U = torch.empty_like(F) if out is None else out
+        self._check_size(U)
+        check(lib.stkg_heat_solve(self._h, C.c_void_p(_dev_ptr(F)), C.c_void_p(_dev_ptr(U))))
+        return U
+
+    def apply(self, U, out=None):
+        """KronOp::apply of heat_kron_op: M U D + A U C."""
+        import torch
+        self._check_size(U)
+        Y = torch.empty_like(U) if out is None else out
+        check(lib.stkg_heat_apply(self._h, C.c_void_p(_dev_ptr(U)), C.c_void_p(_dev_ptr(Y))))
+        return Y
+
+    def residual(self, U, F):
+        """(||F - B(U)||_F / ||F||_F, ||F||_F), deterministic GPU reduction (K1)."""
+        self._check_size(U)
+        self._check_size(F)
+        rel, fn = C.c_double(), C.c_double()
+        check(lib.stkg_heat_residual(self._h, C.c_void_p(_dev_ptr(U)), C.c_void_p(_dev_ptr(F)),
+                                     C.byref(rel), C.byref(fn)))
+        return rel.value, fn.value
+
+    # -- profiling ------------------------------------------------------------------
+    def profile_begin(self):
+        check(lib.stkg_heat_profile(self._h, 1, None, None))
+
+    def profile_end(self):
+        """-> {"transform": (ms, launches), "scan": (ms, launches)} since profile_begin."""
+        ms = (C.c_double * 2)()
+        n = (C.c_int64 * 2)()
+        check(lib.stkg_heat_profile(self._h, 0, ms, n))
+        return {"transform": (ms[0], n[0]), "scan": (ms[1], n[1])}
+
+    # -- host path ------------------------------------------------------------------
+    def solve_host(self, F: np.ndarray, out: np.ndarray | None = None) -> np.ndarray:
+        """Same solve with host buffers; H2D, solve and D2H overlap across time chunks."""
+        F = np.ascontiguousarray(F, dtype=np.float64)
+        self._check_size(F)
+        U = np.empty_like(F) if out is None else out
+        if not (U.flags.c_contiguous and U.dtype == np.float64):
+            raise ArgumentError("solve_host: out must be a contiguous float64 array")
+        check(lib.stkg_heat_solve_host(self._h, C.c_void_p(F.ctypes.data),
+                                       C.c_void_p(U.ctypes.data)))
+        return U
+
+
+def solve_projected_heat_with(eig, d: Bidiagonal, c: Bidiagonal, g):
+    """Reference-named entry point (stk/sylvester.hpp:117): one-shot plan + solve.
+
+    ``g`` may be a device tensor (result on device) or a host numpy array (result on host).
+    """
+    plan = HeatPlan(eig, d, c)
+    try:
+        if isinstance(g, np.ndarray):
+            return plan.solve_host(g)
+        return plan.solve(g)
+    finally:
+        plan.close()
+
+
+class HeatKronOp:
+    """heat_kron_op(M, A, D, C) (stk/sylvester.hpp:58-65) for tensor-grid Q1/P1 factors:
+    M = (x) M_axis, A = sum_axis A_axis (x) M_others (fem2d_matrices, :81-88)."""
+
+    def __init__(self, m_axes: Sequence[Tridiagonal], a_axes: Sequence[Tridiagonal],
+                 d: Bidiagonal, c: Bidiagonal, eig: TensorEigPair | None = None, stream=None):
+        if eig is None:  # apply-only plan: identity eigen-data is never used by apply
+            eig = TensorEigPair([EigPair(np.ones(m.diag.size), np.eye(m.diag.size))
+                                 for m in m_axes])
+        self.plan = HeatPlan(eig, d, c, m_axes, a_axes, stream=stream)
+
+    def apply(self, U, out=None):
+        return self.plan.apply(U, out)
+
+
+def heat_kron_op(m_axes, a_axes, d, c, eig=None):
+    return HeatKronOp(m_axes, a_axes, d, c, eig)

@@ -1,0 +1,191 @@
+"""Wave hot path: Python mirror of WaveOperator / TwoTermPrecond / gmres over the C ABI.
+
+Reference interface:
+  * ``WaveOperator(m_h, a_h, q_h, q_dt, d_dt, m_dt).apply(x)``  stk/outer_krylov.hpp:168-191
+  * ``TwoTermPrecond(m_h, q_h, m_dt, q_dt).solve(v)``          stk/sylvester.hpp:153-181
+  * ``gmres(apply, precond, b, cfg) -> (x, SolveReport)``      stk/outer_krylov.hpp:75-164
+  * ``GmresConfig`` (:18-28), ``SolveReport`` (stk/report.hpp:11-20)
+
+The GPU gmres is specialised to apply = WaveOperator and precond = TwoTermPrecond (the
+pairing run_wave_experiment passes through the VecOp seam, stk/bench.hpp:667-673); both
+live in one device plan.  ``pcg`` is the s.p.d. performance path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from ._lib import GmresCfg, Report, WaveDesc, lib
+from .assembly import EigPair, WaveSpaceMatrices, WaveTimeMatrices, sym_gen_eig
+from .errors import ArgumentError, check
+from .heat import _dev_ptr, _np_ptr, _stream_handle
+
+
+@dataclass
+class GmresConfig:
+    tol: float = 1e-8
+    maxit: int = 200
+    restart: int = 0  # 0 = full GMRES
+
+    def validate(self):
+        if not 0.0 < self.tol < 1.0:
+            raise ArgumentError("GmresConfig: tol must be in (0,1)")
+        if self.maxit < 1:
+            raise ArgumentError("GmresConfig: maxit must be >= 1")
+
+
+@dataclass
+class SolveReport:
+    iterations: int = 0
+    rel_res_history: list = field(default_factory=list)
+    mu_mem: int = 0
+    rank: int = 0
+    wall_time_s: float = 0.0
+    final_relres: float = 0.0
+    converged: bool = False
+    stagnated: bool = False
+
+
+def _report(r: Report, hist: np.ndarray) -> SolveReport:
+    n = min(r.history_length, hist.size)
+    return SolveReport(iterations=r.iterations, rel_res_history=hist[:n].tolist(),
+                       mu_mem=r.mu_mem, wall_time_s=r.wall_time_s, final_relres=r.final_relres,
+                       converged=bool(r.converged), stagnated=bool(r.stagnated))
+
+
+class WavePlan:
+    """Device plan of the wave system: the six banded factors and (optionally) the two
+    generalized eigenpairs of TwoTermPrecond."""
+
+    def __init__(self, space: WaveSpaceMatrices, time: WaveTimeMatrices, precond: bool = True,
+                 space_eig: EigPair | None = None, time_eig: EigPair | None = None, stream=None):
+        self.nh = space.M.n
+        self.nt = time.M.n
+        keep = []
+
+        def arr(a):
+            a = np.ascontiguousarray(a, dtype=np.float64)
+            keep.append(a)
+            return _np_ptr(a)
+
+        desc = WaveDesc()
+        desc.nh, desc.nt = self.nh, self.nt
+        desc.space_bands = arr(np.concatenate([space.M.band, space.A.band, space.Q.band]))
+        desc.time_bands = arr(np.concatenate([time.Q.band, time.D.band, time.M.band]))
+        self.space_eig = self.time_eig = None
+        if precond:
+            # TwoTermPrecond ctor (stk/sylvester.hpp:155-161): sym_gen_eig(Q_h, M_h), (Q_t, M_t)
+            self.space_eig = space_eig or sym_gen_eig(space.Q.dense(), space.M.dense())
+            self.time_eig = time_eig or sym_gen_eig(time.Q.dense(), time.M.dense())
+            Xs = np.asfortranarray(self.space_eig.X)
+            Xt = np.asfortranarray(self.time_eig.X)
+            keep += [Xs, Xt]
+            desc.Xs, desc.Xt = _np_ptr(Xs), _np_ptr(Xt)
+            desc.lambdas = arr(self.space_eig.lambdas)
+            desc.thetas = arr(self.time_eig.lambdas)
+        h = C.c_void_p()
+        check(lib.stkg_wave_create(C.byref(h), C.byref(desc), _stream_handle(stream)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            check(lib.stkg_wave_destroy(self._h))
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def N(self):
+        return self.nh * self.nt
+
+    def _chk(self, t):
+        if t.numel() != self.N:
+            raise ArgumentError("WaveOperator: vector length mismatch")
+
+    def apply(self, x, out=None):
+        import torch
+        self._chk(x)
+        y = torch.empty_like(x) if out is None else out
+        check(lib.stkg_wave_apply(self._h, C.c_void_p(_dev_ptr(x)), C.c_void_p(_dev_ptr(y))))
+        return y
+
+    def two_term_solve(self, v, out=None):
+        import torch
+        self._chk(v)
+        w = torch.empty_like(v) if out is None else out
+        check(lib.stkg_two_term_solve(self._h, C.c_void_p(_dev_ptr(v)), C.c_void_p(_dev_ptr(w))))
+        return w
+
+    def gmres(self, b, cfg: GmresConfig | None = None, precond: bool = True, x=None):
+        import torch
+        cfg = cfg or GmresConfig()
+        cfg.validate()
+        self._chk(b)
+        x = torch.empty_like(b) if x is None else x
+        c = GmresCfg(cfg.tol, cfg.maxit, cfg.restart, 1 if precond else 0)
+        hist = np.zeros(cfg.maxit + 1)
+        rep = Report()
+        rep.rel_res_history = _np_ptr(hist)
+        rep.history_capacity = hist.size
+        check(lib.stkg_gmres(self._h, C.c_void_p(_dev_ptr(b)), C.c_void_p(_dev_ptr(x)),
+                             C.byref(c), C.byref(rep)))
+        return x, _report(rep, hist)
+
+    def pcg(self, b, tol: float = 1e-8, maxit: int = 1000, x=None):
+        import torch
+        self._chk(b)
+        x = torch.empty_like(b) if x is None else x
+        hist = np.zeros(maxit + 1)
+        rep = Report()
+        rep.rel_res_history = _np_ptr(hist)
+        rep.history_capacity = hist.size
+        check(lib.stkg_pcg(self._h, C.c_void_p(_dev_ptr(b)), C.c_void_p(_dev_ptr(x)), tol, maxit,
+                           C.byref(rep)))
+        return x, _report(rep, hist)
+
+
+class WaveOperator:
+    """vec(M_h U Q_t^T + A_h U (D_t + D_t^T) + Q_h U M_t) (stk/outer_krylov.hpp:168-191)."""
+
+    def __init__(self, plan: WavePlan):
+        self.plan = plan
+
+    def space_dim(self):
+        return self.plan.nh
+
+    def time_dim(self):
+        return self.plan.nt
+
+    def apply(self, x, out=None):
+        return self.plan.apply(x, out)
+
+
+class TwoTermPrecond:
+    """M_h W Q_t^T + Q_h W M_t = V solved in the eigenbases (stk/sylvester.hpp:153-181)."""
+
+    def __init__(self, plan: WavePlan):
+        if plan.space_eig is None:
+            raise ArgumentError("TwoTermPrecond: plan built without eigenpairs")
+        self.plan = plan
+
+    def space(self) -> EigPair:
+        return self.plan.space_eig
+
+    def time(self) -> EigPair:
+        return self.plan.time_eig
+
+    def solve(self, v, out=None):
+        return self.plan.two_term_solve(v, out)
+
+
+def gmres(apply: WaveOperator, precond: TwoTermPrecond | None, b, cfg: GmresConfig | None = None):
+    """gmres(apply, precond, b, cfg) -> (x, SolveReport) on the GPU plan."""
+    if precond is not None and precond.plan is not apply.plan:
+        raise ArgumentError("gmres: operator and preconditioner must share one WavePlan")
+    return apply.plan.gmres(b, cfg, precond=precond is not None)

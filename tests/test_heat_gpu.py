@@ -1,0 +1,196 @@
+"""GPU parity tests of the heat hot path (K1 operator/residual, K2 DMMA transforms, K3 scan)
+against the CPU oracle, through the C ABI (ctypes binding in paper_1912_10082_b200)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def dev(a):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).cuda()
+
+
+def host(t):
+    return t.cpu().numpy()
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def p1_setup(stk, ndim, n, nt, T=1.0):
+    g = stk.SpaceGrid1D(0.0, 1.0, n)
+    M, A = stk.fem1d_matrices(g)
+    D, Cm = stk.heat_time_matrices(stk.TimeGrid(nt, T))
+    eig = stk.TensorEigPair([stk.p1_eigpair(g)] * ndim)
+    plan = stk.HeatPlan(eig, D, Cm, [M] * ndim, [A] * ndim)
+    return plan, M, A, D, Cm
+
+
+def orc_factors(stk_m, stk_a, D, Cm, ndim):
+    m = (stk_m.diag, stk_m.off)
+    a = (stk_a.diag, stk_a.off)
+    return [m] * ndim, [a] * ndim, (D.diag, D.sup), (Cm.diag, Cm.sup)
+
+
+# ------------------------------------------------------------- K2+K3 vs dense oracle --
+@pytest.mark.parametrize("ns,nt", [((1,), 1), ((3,), 5), ((37,), 11), ((130,), 33), ((257,), 7),
+                                   ((5, 7), 9), ((17, 13), 4), ((3, 4, 5), 6), ((1, 9, 2), 3)])
+def test_solve_random_tensor_eigpair_vs_dense_oracle(stk, orc, cuda, ns, nt):
+    """solve_projected_heat_with with an arbitrary (non-orthogonal) tensor EigPair: the GPU
+    tensor-form transforms + scan equal the oracle's dense k x k restatement."""
+    rng = np.random.default_rng(sum(ns) * 31 + nt)
+    axes, Xs, lams = [], [], []
+    for n in ns:
+        X = rng.standard_normal((n, n)) / np.sqrt(n)
+        lam = rng.uniform(0.5, 50.0, n)
+        axes.append(stk.EigPair(lam, X))
+        Xs.append(X)
+        lams.append(lam)
+    Xk = Xs[0]
+    lk = lams[0]
+    for X, lam in zip(Xs[1:], lams[1:]):
+        Xk = np.kron(Xk, X)  # index ix*ny + iy (sparse_kron order)
+        lk = (lk[:, None] + lam[None, :]).ravel()
+    D, Cm = stk.heat_time_matrices(stk.TimeGrid(nt, 1.0))
+    F = rng.standard_normal((nt, Xk.shape[0]))
+    plan = stk.HeatPlan(stk.TensorEigPair(axes), D, Cm)
+    U = host(plan.solve(dev(F)))
+    Uref = orc.solve_projected_heat_with_dense(Xk, lk, (D.diag, D.sup), (Cm.diag, Cm.sup), F)
+    assert rel(U, Uref) < 1e-12
+
+
+def test_kat_scalar_and_diag(stk, orc, cuda):
+    # SPEC.md:307  k=1, N_t=1, h_m=d=1, h_a=c=1, g=2 -> y=1
+    one = stk.Bidiagonal(np.array([1.0]), np.zeros(0))
+    plan = stk.HeatPlan(stk.EigPair(np.array([1.0]), np.array([[1.0]])), one, one)
+    assert host(plan.solve(dev([[2.0]])))[0, 0] == 1.0
+    # SPEC.md:308  H_M = I, H_A = diag(1,2), heat D,C with N_t=3, dt=1, G = ones
+    D, Cm = stk.heat_time_matrices(stk.TimeGrid(3, 3.0))
+    plan = stk.HeatPlan(stk.EigPair(np.array([1.0, 2.0]), np.eye(2)), D, Cm)
+    Y = host(plan.solve(dev(np.ones((3, 2)))))
+    B = np.kron(D.dense().T, np.eye(2)) + np.kron(Cm.dense().T, np.diag([1.0, 2.0]))
+    assert np.allclose(Y.ravel(), np.linalg.solve(B, np.ones(6)), rtol=1e-14, atol=1e-15)
+
+
+def test_kat_random_spd_residual(stk, cuda):
+    # SPEC.md:309  random s.p.d. H_M, H_A (k=5), N_t=7 -> residual <= 1e-11 relative
+    rng = np.random.default_rng(309)
+    B1 = rng.standard_normal((5, 5))
+    B2 = rng.standard_normal((5, 5))
+    HM = B1 @ B1.T + 5 * np.eye(5)
+    HA = B2 @ B2.T + np.eye(5)
+    eig = stk.sym_gen_eig(HA, HM)
+    D, Cm = stk.heat_time_matrices(stk.TimeGrid(7, 1.0))
+    G = rng.standard_normal((7, 5))
+    Y = host(stk.HeatPlan(eig, D, Cm).solve(dev(G)))
+    R = HM @ Y.T @ D.dense() + HA @ Y.T @ Cm.dense() - G.T
+    assert np.linalg.norm(R) / np.linalg.norm(G) <= 1e-11
+
+
+def test_singular_row_system_raises(stk, cuda):
+    # stk/sylvester.hpp:133-135: |d_j + lambda c_j| < 1e-300 -> SingularityError
+    D = stk.Bidiagonal(np.array([1.0, 0.0]), np.array([-1.0]))
+    Cm = stk.Bidiagonal(np.array([0.5, 0.0]), np.array([0.5]))
+    plan = stk.HeatPlan(stk.EigPair(np.array([2.0]), np.array([[1.0]])), D, Cm)
+    with pytest.raises(stk.SingularityError, match="lambda"):
+        plan.solve(dev(np.ones((2, 1))))
+
+
+# ------------------------------------------------------------------------ K1 apply ---
+@pytest.mark.parametrize("ndim,n,nt", [(1, 1, 1), (1, 40, 9), (2, 1, 3), (2, 11, 6),
+                                       (2, 63, 17), (3, 5, 4), (3, 12, 5)])
+def test_apply_vs_oracle(stk, orc, cuda, ndim, n, nt):
+    plan, M, A, D, Cm = p1_setup(stk, ndim, n, nt)
+    ms, as_, d, c = orc_factors(M, A, D, Cm, ndim)
+    rng = np.random.default_rng(n * 7 + nt)
+    U = rng.standard_normal((nt, n ** ndim))
+    Y = host(plan.apply(dev(U)))
+    Yref = orc.heat_apply(ms, as_, d, c, U)
+    assert rel(Y, Yref) < 1e-13
+
+
+def test_apply_linearity_and_residual(stk, orc, cuda):
+    # SPEC.md:339 linearity; residual == ||F - B(U)|| / ||F||
+    plan, M, A, D, Cm = p1_setup(stk, 2, 21, 8)
+    rng = np.random.default_rng(2)
+    X, Y = rng.standard_normal((2, 8, 441))
+    a, b = 0.3, -1.7
+    lhs = host(plan.apply(dev(a * X + b * Y)))
+    rhs = a * host(plan.apply(dev(X))) + b * host(plan.apply(dev(Y)))
+    assert rel(lhs, rhs) < 1e-14
+    F = rng.standard_normal((8, 441))
+    r_gpu, fn = plan.residual(dev(X), dev(F))
+    ms, as_, d, c = orc_factors(M, A, D, Cm, 2)
+    assert abs(fn - np.linalg.norm(F)) < 1e-12 * fn
+    assert abs(r_gpu - orc.heat_residual(ms, as_, d, c, X, F)) < 1e-13
+
+
+# ---------------------------------------------------------------- BASELINE configs ---
+def _config_parity(stk, orc, name, nsteps=None, cn_steps=None):
+    from paper_1912_10082_b200 import inputs
+    cfg = inputs.CONFIGS[name]
+    plan, M, A, D, Cm = p1_setup(stk, cfg.ndim, cfg.n, cfg.nt)
+    ms, as_, d, c = orc_factors(M, A, D, Cm, cfg.ndim)
+    if cfg.rank == 0:
+        Fd = inputs.heat_rhs_device(cfg)
+        Fh = inputs.heat_rhs_host(cfg, nsteps=nsteps)
+        assert np.array_equal(host(Fd[: Fh.shape[0]]), Fh)  # device generator == host
+    else:
+        Fh_full = inputs.heat_rhs_host(cfg)
+        Fd = dev(Fh_full)
+        Fh = Fh_full if nsteps is None else Fh_full[:nsteps]
+    U = plan.solve(Fd)
+    relres, _ = plan.residual(U, Fd)
+    assert relres <= 1e-10, relres  # north_star gate, checked by the GPU residual kernel
+    eig = orc.p1_pencil_eig(ms[0], as_[0])  # scipy eigh basis: independent of the closed form
+    Uref = orc.heat_decoupled([eig] * cfg.ndim, d, c, Fh, nsteps=nsteps)
+    k = Uref.shape[0]
+    err = rel(host(U[:k]), Uref)
+    assert err <= 1e-10, err
+    if cn_steps:
+        Ucn = orc.crank_nicolson(ms, as_, 1.0 / cfg.nt, Fh, nsteps=cn_steps)
+        assert rel(host(U[:cn_steps]), Ucn) <= 1e-10
+    return relres, err
+
+
+def test_cfg1_parity(stk, orc, cuda):
+    _config_parity(stk, orc, "cfg1", cn_steps=256)
+
+
+def test_cfg2_parity(stk, orc, cuda):
+    _config_parity(stk, orc, "cfg2", cn_steps=16)
+
+
+def test_cfg5_parity(stk, orc, cuda):
+    _config_parity(stk, orc, "cfg5", nsteps=16)
+
+
+def test_cfg3_parity_prefix_and_full_residual(stk, orc, cuda):
+    # full 1023^2 x 1024 solve on the GPU; causal 8-step prefix vs the numpy oracle (the
+    # first k columns of U depend only on the first k columns of F), full-size residual.
+    _config_parity(stk, orc, "cfg3", nsteps=8)
+
+
+# ------------------------------------------------------------ host path / determinism --
+def test_host_path_bitwise_equal_device_path(stk, cuda):
+    import torch
+    plan, *_ = p1_setup(stk, 2, 63, 40)
+    eig = stk.TensorEigPair([stk.p1_eigpair(stk.SpaceGrid1D(0, 1, 63))] * 2)
+    D, Cm = stk.heat_time_matrices(stk.TimeGrid(40, 1.0))
+    plan_c = stk.HeatPlan(eig, D, Cm, time_chunk=7)
+    rng = np.random.default_rng(11)
+    F = rng.standard_normal((40, 63 * 63))
+    Ud = host(plan.solve(dev(F)))
+    Uh = plan_c.solve_host(F)  # 6 chunks of 7 steps (+ remainder), carry across chunks
+    assert np.array_equal(Ud, Uh)
+    pinned = torch.from_numpy(F).pin_memory()
+    out = torch.empty_like(pinned).pin_memory()
+    plan_c.solve_host(pinned.numpy(), out=out.numpy())
+    assert np.array_equal(out.numpy(), Ud)
+    # determinism: same inputs -> bit-identical solution and residual
+    assert np.array_equal(host(plan.solve(dev(F))), Ud)
+    r1 = plan.residual(dev(Ud), dev(F))
+    r2 = plan.residual(dev(Ud), dev(F))
+    assert r1 == r2
