@@ -50,22 +50,31 @@ struct GemmCfg {
   static constexpr int kMinBlocks = MINB_;
   static constexpr int kWarpsM = BM / WM, kWarpsN = BN / WN;
   static constexpr int kThreads = 32 * kWarpsM * kWarpsN;
-  // Padding keeps fragment reads conflict-free: the A pitch is 8 banks mod 32 per k row,
-  // the B pitch is 8 banks mod 32 per n column (K2).
-  static constexpr int kLdsA = BM + 4;  // sA[k][m]
-  static constexpr int kLdsB = BK + 4;  // sB[n][k]
+  // Both tiles are stored k-major, sA[k][perm(m)], sB[k][perm(n)], where perm interleaves
+  // rows r and r+8 of every 16-row group (perm(r) = 16*(r/16) + 2*(r%8) + (r/8)%2) so that
+  // a thread's two fragment values are one 16-byte shared load.  The pitch (tile + 4
+  // doubles) is 8 banks mod 32 per k row: the 128-bit fragment loads are conflict-free.
+  static constexpr int kLdsA = BM + 4;
+  static constexpr int kLdsB = BN + 4;
   static constexpr int kStageA = BK * kLdsA;
-  static constexpr int kStageB = BN * kLdsB;
+  static constexpr int kStageB = BK * kLdsB;
   static constexpr size_t kSmemBytes = size_t(STAGES) * (kStageA + kStageB) * sizeof(double);
   static constexpr int kMi = WM / 16, kNi = WN / 8;
   static constexpr int kLoadA = BM * BK / kThreads;
   static constexpr int kLoadB = BN * BK / kThreads;
   static_assert(BM * BK % kThreads == 0 && BN * BK % kThreads == 0, "tile/thread mismatch");
-  static_assert(BK % 4 == 0 && WM % 16 == 0 && WN % 8 == 0, "mma shape");
+  static_assert(BK % 4 == 0 && WM % 16 == 0 && WN % 16 == 0, "mma shape");
 };
 
-using GemmBig = GemmCfg<128, 128, 16, 64, 32, 4, 1>;    // 256 threads, batched transforms
-using GemmSmall = GemmCfg<64, 64, 16, 32, 32, 4, 2>;    // 128 threads, single ~1k^3 GEMMs
+// 64x64x32 tiles, 4 warps of 32x32, 2 stages, 3 CTAs/SM: the independent CTAs' barrier and
+// load phases interleave on each SM, which keeps the DMMA pipe busier than one 256-thread
+// 128x128 CTA.  Config sweep on B200 (tools/microbench/gemm_bench.cu,
+// profiles/r01_gemm_config_sweep.txt): 32.9 / 32.6 / 26.4 TFLOP/s on the heat left,
+// heat batched-right and single 1k^3 (wave preconditioner) shapes vs 28.5 / 28.5 / 12.0
+// for 128x128x16.
+using GemmTile = GemmCfg<64, 64, 32, 32, 32, 2, 3>;
+
+__host__ __device__ constexpr int perm16(int r) { return (r & ~15) | ((r & 7) << 1) | ((r >> 3) & 1); }
 
 __device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool valid) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -113,27 +122,49 @@ __global__ void __launch_bounds__(Cfg::kThreads, Cfg::kMinBlocks)
   const int g = lane >> 2, t = lane & 3;
   const int wm = warp % Cfg::kWarpsM, wn = warp / Cfg::kWarpsM;
 
+  // Per-thread load geometry, fixed for the whole K loop: thread tid copies A rows
+  // (m = tid % BM, k = tid / BM + i * kRowsA) and B entries (k = tid % BK,
+  // n = tid / BK + i * kColsB).  Only one 64-bit product per stage is left in the loop.
+  constexpr int kRowsA = Cfg::kThreads / Cfg::BM;
+  constexpr int kColsB = Cfg::kThreads / Cfg::BK;
+  static_assert(Cfg::kThreads % Cfg::BM == 0 && Cfg::kThreads % Cfg::BK == 0, "load geometry");
+  const int am = tid % Cfg::BM, ak = tid / Cfg::BM;
+  const int bk = tid % Cfg::BK, bn = tid / Cfg::BK;
+  const bool a_row_ok = m0 + am < p.M;
+  uint32_t b_col_ok = 0;
+#pragma unroll
+  for (int i = 0; i < Cfg::kLoadB; ++i)
+    if (n0 + bn + i * kColsB < p.N) b_col_ok |= 1u << i;
+  const double* a_src = A + (a_row_ok ? m0 + am : 0) + int64_t(ak) * p.lda;
+  const double* b_src = B + (b_col_ok & 1u ? (n0 + bn) * p.ldb : 0) + bk;
+  const int64_t a_step = int64_t(kRowsA) * p.lda;
+  const int64_t b_step = int64_t(kColsB) * p.ldb;
+  const int a_dst = ak * Cfg::kLdsA + perm16(am);
+  // B entries: n = bn + i * kColsB with bn < kColsB (a power of two): the bits of bn and of
+  // i * kColsB are disjoint and perm16 is a bit permutation, so perm16(n) splits into
+  // perm16(bn) + perm16(i * kColsB), a compile-time offset per i.
+  static_assert((kColsB & (kColsB - 1)) == 0, "kColsB must be a power of two");
+  const int b_dst = bk * Cfg::kLdsB + perm16(bn);
+
   const int64_t ktiles = (p.K + Cfg::BK - 1) / Cfg::BK;
+  const int64_t kfull = p.K / Cfg::BK;
 
   auto load_stage = [&](int stage, int64_t kt) {
     const int64_t k0 = kt * Cfg::BK;
-    double* a_dst = sA + stage * Cfg::kStageA;
-    double* b_dst = sB + stage * Cfg::kStageB;
+    const bool full = kt < kfull;
+    double* sa = sA + stage * Cfg::kStageA + a_dst;
+    double* sb = sB + stage * Cfg::kStageB + b_dst;
+    const double* pa = a_src + k0 * p.lda;
+    const double* pb = b_src + k0;
 #pragma unroll
     for (int i = 0; i < Cfg::kLoadA; ++i) {
-      const int e = tid + i * Cfg::kThreads;
-      const int m = e % Cfg::BM, k = e / Cfg::BM;
-      const bool ok = (m0 + m < p.M) && (k0 + k < p.K);
-      const double* src = ok ? A + (k0 + k) * p.lda + (m0 + m) : A;
-      cp_async8(a_dst + k * Cfg::kLdsA + m, src, ok);
+      const bool ok = a_row_ok && (full || k0 + ak + i * kRowsA < p.K);
+      cp_async8(sa + i * kRowsA * Cfg::kLdsA, ok ? pa + i * a_step : A, ok);
     }
 #pragma unroll
     for (int i = 0; i < Cfg::kLoadB; ++i) {
-      const int e = tid + i * Cfg::kThreads;
-      const int k = e % Cfg::BK, n = e / Cfg::BK;
-      const bool ok = (n0 + n < p.N) && (k0 + k < p.K);
-      const double* src = ok ? B + (n0 + n) * p.ldb + (k0 + k) : B;
-      cp_async8(b_dst + n * Cfg::kLdsB + k, src, ok);
+      const bool ok = ((b_col_ok >> i) & 1u) && (full || k0 + bk < p.K);
+      cp_async8(sb + perm16(i * kColsB), ok ? pb + i * b_step : B, ok);
     }
   };
 
@@ -151,33 +182,48 @@ __global__ void __launch_bounds__(Cfg::kThreads, Cfg::kMinBlocks)
     cp_async_commit();
   }
 
+  // fragments double-buffered across the k4 sub-steps of a stage
+  double af[2][Cfg::kMi][2], bf[2][Cfg::kNi];
+  auto load_frags = [&](int buf, const double* a_s, const double* b_s, int kk) {
+    const double* a_row = a_s + (kk * 4 + t) * Cfg::kLdsA + wm * Cfg::WM + 2 * g;
+#pragma unroll
+    for (int mi = 0; mi < Cfg::kMi; ++mi) {  // rows g, g+8 of the 16-row group
+      const double2 v = *reinterpret_cast<const double2*>(a_row + mi * 16);
+      af[buf][mi][0] = v.x;
+      af[buf][mi][1] = v.y;
+    }
+    const double* b_row = b_s + (kk * 4 + t) * Cfg::kLdsB + wn * Cfg::WN + 2 * g;
+#pragma unroll
+    for (int nj = 0; nj < Cfg::kNi / 2; ++nj) {  // columns g + 16 nj, g + 16 nj + 8
+      const double2 v = *reinterpret_cast<const double2*>(b_row + nj * 16);
+      bf[buf][2 * nj] = v.x;
+      bf[buf][2 * nj + 1] = v.y;
+    }
+  };
+
   for (int64_t kt = 0; kt < ktiles; ++kt) {
     cp_async_wait<Cfg::STAGES - 2>();
     __syncthreads();
-    {
-      const int64_t nk = kt + Cfg::STAGES - 1;
-      if (nk < ktiles) load_stage(static_cast<int>(nk % Cfg::STAGES), nk);
-      cp_async_commit();
-    }
     const int stage = static_cast<int>(kt % Cfg::STAGES);
     const double* a_s = sA + stage * Cfg::kStageA;
     const double* b_s = sB + stage * Cfg::kStageB;
+    load_frags(0, a_s, b_s, 0);
 #pragma unroll
     for (int kk = 0; kk < Cfg::BK / 4; ++kk) {
-      double af[Cfg::kMi][2], bf[Cfg::kNi];
-      const double* a_row = a_s + (kk * 4 + t) * Cfg::kLdsA + wm * Cfg::WM + g;
-#pragma unroll
-      for (int mi = 0; mi < Cfg::kMi; ++mi) {
-        af[mi][0] = a_row[mi * 16];
-        af[mi][1] = a_row[mi * 16 + 8];
-      }
-      const double* b_col = b_s + (wn * Cfg::WN + g) * Cfg::kLdsB + kk * 4 + t;
-#pragma unroll
-      for (int ni = 0; ni < Cfg::kNi; ++ni) bf[ni] = b_col[ni * 8 * Cfg::kLdsB];
+      const int cur = kk & 1;
+      if (kk + 1 < Cfg::BK / 4) load_frags(cur ^ 1, a_s, b_s, kk + 1);
 #pragma unroll
       for (int mi = 0; mi < Cfg::kMi; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < Cfg::kNi; ++ni) dmma_m16n8k4(acc[mi][ni], af[mi][0], af[mi][1], bf[ni]);
+        for (int ni = 0; ni < Cfg::kNi; ++ni)
+          dmma_m16n8k4(acc[mi][ni], af[cur][mi][0], af[cur][mi][1], bf[cur][ni]);
+      if (kk == 0) {
+        // refill the stage consumed in the previous iteration while the tensor pipe
+        // works through the first sub-step's DMMAs
+        const int64_t nk = kt + Cfg::STAGES - 1;
+        if (nk < ktiles) load_stage(static_cast<int>(nk % Cfg::STAGES), nk);
+        cp_async_commit();
+      }
     }
   }
   cp_async_wait<0>();
@@ -216,15 +262,9 @@ void launch_gemm_cfg(const GemmProblem& p, const Epi& epi, cudaStream_t stream) 
   STKG_CUDA_CHECK(cudaGetLastError());
 }
 
-// Tile choice: the 128x128 tile needs >= ~2 waves of CTAs on 148 SMs to stay busy; a
-// single ~1k^3 product has only 64 such tiles, so it takes the 64x64 tile instead.
 template <class Epi>
 void launch_gemm(const GemmProblem& p, const Epi& epi, cudaStream_t stream) {
-  const int64_t big_tiles = ceil_div(p.M, 128) * ceil_div(p.N, 128) * p.batch;
-  if (big_tiles >= 2 * 148)
-    launch_gemm_cfg<GemmBig>(p, epi, stream);
-  else
-    launch_gemm_cfg<GemmSmall>(p, epi, stream);
+  launch_gemm_cfg<GemmTile>(p, epi, stream);
 }
 
 }  // namespace stkg
