@@ -170,6 +170,24 @@ typedef struct stkg_report {       /* SolveReport (stk/report.hpp:11-20) */
   int history_length;
 } stkg_report;
 
+/* ------------------------------------------------------- generic Krylov solvers --- */
+/* Device-vector operator callback: the VecOp of stk/outer_krylov.hpp:30, i.e. the seam
+ * run_wave_experiment passes lambdas through (stk/bench.hpp:667-673).  y = op(x) for
+ * device vectors of length n, enqueued on cuda_stream; return STKG_OK or a status code
+ * (a non-zero status aborts the solve and is returned by the solver). */
+typedef int (*stkg_vec_op)(void* user, const double* x, double* y, void* cuda_stream);
+
+/* gmres (stk/outer_krylov.hpp:75-164) over arbitrary device operators: right
+ * preconditioning (precond may be NULL), full or restarted, Gram-Schmidt with one
+ * re-orthogonalisation pass, Givens least squares, true final residual.  b, x device. */
+int stkg_gmres_op(int64_t n, stkg_vec_op apply, void* apply_user, stkg_vec_op precond,
+                  void* precond_user, const double* b, double* x, const stkg_gmres_config* cfg,
+                  stkg_report* report, void* cuda_stream);
+/* Preconditioned CG over device operators (both must be s.p.d.). */
+int stkg_pcg_op(int64_t n, stkg_vec_op apply, void* apply_user, stkg_vec_op precond,
+                void* precond_user, const double* b, double* x, double tol, int maxit,
+                stkg_report* report, void* cuda_stream);
+
 int stkg_wave_create(stkg_wave** plan, const stkg_wave_desc* desc, void* cuda_stream);
 int stkg_wave_destroy(stkg_wave* plan);
 /* WaveOperator::apply (stk/outer_krylov.hpp:178-186):

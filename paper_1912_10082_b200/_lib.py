@@ -67,6 +67,8 @@ class Report(C.Structure):
     ]
 
 
+VEC_OP = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p)
+
 # name -> (restype, argtypes); must list every symbol include/stk_gpu.h declares
 SIGNATURES = {
     "stkg_last_error_message": (C.c_char_p, []),
@@ -96,6 +98,10 @@ SIGNATURES = {
     "stkg_heat_apply": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "stkg_heat_residual": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, c_double_p, c_double_p]),
     "stkg_heat_profile": (C.c_int, [C.c_void_p, C.c_int, c_double_p, C.POINTER(C.c_int64)]),
+    "stkg_gmres_op": (C.c_int, [C.c_int64, VEC_OP, C.c_void_p, VEC_OP, C.c_void_p, C.c_void_p,
+                                C.c_void_p, C.POINTER(GmresCfg), C.POINTER(Report), C.c_void_p]),
+    "stkg_pcg_op": (C.c_int, [C.c_int64, VEC_OP, C.c_void_p, VEC_OP, C.c_void_p, C.c_void_p,
+                              C.c_void_p, C.c_double, C.c_int, C.POINTER(Report), C.c_void_p]),
     "stkg_wave_create": (C.c_int, [C.POINTER(C.c_void_p), C.POINTER(WaveDesc), C.c_void_p]),
     "stkg_wave_destroy": (C.c_int, [C.c_void_p]),
     "stkg_wave_apply": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),

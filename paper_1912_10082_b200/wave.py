@@ -6,18 +6,20 @@ Reference interface:
   * ``gmres(apply, precond, b, cfg) -> (x, SolveReport)``      stk/outer_krylov.hpp:75-164
   * ``GmresConfig`` (:18-28), ``SolveReport`` (stk/report.hpp:11-20)
 
-The GPU gmres is specialised to apply = WaveOperator and precond = TwoTermPrecond (the
-pairing run_wave_experiment passes through the VecOp seam, stk/bench.hpp:667-673); both
-live in one device plan.  ``pcg`` is the s.p.d. performance path.
+``gmres`` takes either the plan objects (apply = WaveOperator, precond = TwoTermPrecond, the
+pairing run_wave_experiment passes through the VecOp seam, stk/bench.hpp:667-673; both
+live in one device plan) or arbitrary callables on device vectors (``stkg_gmres_op``).
+``pcg`` is the s.p.d. performance path.
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 from dataclasses import dataclass, field
 
 import numpy as np
 
-from ._lib import GmresCfg, Report, WaveDesc, lib
+from ._lib import VEC_OP, GmresCfg, Report, WaveDesc, lib
 from .assembly import EigPair, WaveSpaceMatrices, WaveTimeMatrices, sym_gen_eig
 from .errors import ArgumentError, check
 from .heat import _dev_ptr, _np_ptr, _stream_handle
@@ -184,8 +186,60 @@ class TwoTermPrecond:
         return self.plan.two_term_solve(v, out)
 
 
-def gmres(apply: WaveOperator, precond: TwoTermPrecond | None, b, cfg: GmresConfig | None = None):
-    """gmres(apply, precond, b, cfg) -> (x, SolveReport) on the GPU plan."""
-    if precond is not None and precond.plan is not apply.plan:
-        raise ArgumentError("gmres: operator and preconditioner must share one WavePlan")
-    return apply.plan.gmres(b, cfg, precond=precond is not None)
+class _DevView:
+    """Zero-copy torch view of a raw device vector (via __cuda_array_interface__)."""
+
+    def __init__(self, ptr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8",
+                                         "data": (ptr, False), "version": 3, "strides": None}
+
+
+def _vec_op(fn, n):
+    import torch
+
+    def cb(user, x, y, stream):
+        try:
+            xs = torch.as_tensor(_DevView(x, n), device="cuda")
+            ys = torch.as_tensor(_DevView(y, n), device="cuda")
+            ctx = (torch.cuda.stream(torch.cuda.ExternalStream(stream)) if stream
+                   else contextlib.nullcontext())
+            with ctx:
+                out = fn(xs)
+                if out is not None and out.data_ptr() != y:
+                    ys.copy_(out.reshape(-1))
+            return 0
+        except ArgumentError:
+            return 1
+        except Exception:  # surfaced as NumericError by the solver
+            return 5
+    return VEC_OP(cb)
+
+
+def gmres(apply, precond, b, cfg: GmresConfig | None = None):
+    """gmres(apply, precond, b, cfg) -> (x, SolveReport) (stk/outer_krylov.hpp:75-164).
+
+    ``apply``/``precond`` are either the plan objects (WaveOperator, TwoTermPrecond of one
+    WavePlan: everything stays in the library) or arbitrary callables on torch CUDA vectors
+    -- the reference's VecOp seam (:30), run through ``stkg_gmres_op``."""
+    import torch
+    cfg = cfg or GmresConfig()
+    cfg.validate()
+    if isinstance(apply, WaveOperator) and (precond is None or isinstance(precond, TwoTermPrecond)):
+        if precond is not None and precond.plan is not apply.plan:
+            raise ArgumentError("gmres: operator and preconditioner must share one WavePlan")
+        return apply.plan.gmres(b, cfg, precond=precond is not None)
+    fa = apply.apply if hasattr(apply, "apply") else apply
+    fp = None if precond is None else (precond.solve if hasattr(precond, "solve") else precond)
+    n = b.numel()
+    x = torch.empty_like(b)
+    cb_a = _vec_op(fa, n)
+    cb_p = _vec_op(fp, n) if fp is not None else VEC_OP()
+    c = GmresCfg(cfg.tol, cfg.maxit, cfg.restart, 1 if fp is not None else 0)
+    hist = np.zeros(cfg.maxit + 1)
+    rep = Report()
+    rep.rel_res_history = _np_ptr(hist)
+    rep.history_capacity = hist.size
+    stream = torch.cuda.current_stream().cuda_stream
+    check(lib.stkg_gmres_op(n, cb_a, None, cb_p, None, C.c_void_p(_dev_ptr(b)),
+                            C.c_void_p(_dev_ptr(x)), C.byref(c), C.byref(rep), C.c_void_p(stream)))
+    return x, _report(rep, hist)

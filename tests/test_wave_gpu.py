@@ -157,3 +157,21 @@ def test_cfg4_pcg_and_gmres(stk, cuda):
     assert rg.final_relres < 1e-2
     hist = rg.rel_res_history
     assert all(h2 <= h1 * (1 + 1e-12) for h1, h2 in zip(hist, hist[1:]))
+
+
+def test_generic_gmres_callback_seam(stk, ref_bands, cuda):
+    """gmres over arbitrary VecOp callables (stk/outer_krylov.hpp:30,75) equals the plan path."""
+    import torch
+    sb, tb = ref_bands["space_16_3"], ref_bands["time_16_3"]
+    plan = plan_from_bands(stk, sb, tb)
+    b = dev(np.random.default_rng(9).standard_normal(sb.shape[2] * tb.shape[2]))
+    cfg = stk.GmresConfig(tol=1e-11, maxit=300)
+    x1, r1 = stk.gmres(stk.WaveOperator(plan), stk.TwoTermPrecond(plan), b, cfg)
+    x2, r2 = stk.gmres(lambda v: plan.apply(v), lambda v: plan.two_term_solve(v), b, cfg)
+    assert r1.iterations == r2.iterations and r2.converged
+    assert torch.equal(x1, x2)
+    # a plain diagonal operator through the callback seam (SPEC.md:454 analogue)
+    d = torch.arange(1.0, 6.0, dtype=torch.float64, device="cuda")
+    x, r = stk.gmres(lambda v: d * v, None, torch.ones(5, dtype=torch.float64, device="cuda"),
+                     stk.GmresConfig(tol=1e-12, maxit=10))
+    assert r.iterations <= 5 and torch.allclose(x, 1.0 / d, rtol=1e-12)
