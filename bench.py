@@ -104,6 +104,21 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def max_over_ranks(x: float, dist=None, device=None) -> float:
+    """Max of a per-rank scalar (device times are combined by the slowest rank)."""
+    if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
+        return float(x)
+    import torch
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device or "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def aggregate_value(unknowns_per_step: int, steps: int, world: int, ms_max: float) -> float:
+    """Whole-job throughput: every replica solved `steps` systems in at most ms_max."""
+    return world * unknowns_per_step * steps / (ms_max / 1e3)
+
+
 def build_plan(stk, cfg, stream=None, time_chunk=0):
     g = stk.SpaceGrid1D(0.0, 1.0, cfg.n)
     M, A = stk.fem1d_matrices(g)
@@ -210,11 +225,8 @@ def run_ours(args):
         clk = clocks.stop()
         ms = e0.elapsed_time(e1)
         relres, _ = plan.residual(U, F)
-    t_local = torch.tensor([ms], dtype=torch.float64, device="cuda")
-    if dist is not None:
-        dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
-    ms_max = float(t_local.item())
-    value = world * N * args.steps / (ms_max / 1e3)
+    ms_max = max_over_ranks(ms, dist, "cuda")
+    value = aggregate_value(N, args.steps, world, ms_max)
 
     # ---- end to end through the public host-buffer API --------------------------------
     e2e = None
@@ -233,10 +245,8 @@ def run_ours(args):
             plan_h.solve_host(Fh.numpy(), out=Uh.numpy())
         torch.cuda.synchronize()
         t_e2e = time.perf_counter() - t0
-        t_e = torch.tensor([t_e2e], dtype=torch.float64, device="cuda")
-        if dist is not None:
-            dist.all_reduce(t_e, op=dist.ReduceOp.MAX)
-        e2e = {"value": world * N * args.e2e_steps / float(t_e.item()), "unit": UNIT,
+        t_e = max_over_ranks(t_e2e, dist, "cuda")
+        e2e = {"value": aggregate_value(N, args.e2e_steps, world, 1e3 * t_e), "unit": UNIT,
                "h2d_bytes_per_step": N * 8, "d2h_bytes_per_step": N * 8,
                "steps": args.e2e_steps, "api": "stkg_heat_solve_host (pinned host buffers)"}
         plan_h.close()
