@@ -40,6 +40,7 @@ UNIT = "unknowns/s"
 # Measured on this pool's B200 (profiles/r01_fp64_peak.txt): DMMA m16n8k16 sustained.
 FP64_PEAK_TFLOPS = 37.11
 FP64_PEAK_SOURCE = "measured DMMA (mma.sync f64) sustained, profiles/r01_fp64_peak.txt"
+HBM_GBS = 6557.4  # MEASURED_PEAKS.json hbm_gbs (driver-measured copy bandwidth)
 CPU_SAMPLE_STEPS = 96  # causal prefix of cfg3 time slices for the CPU leg
 
 
@@ -225,6 +226,14 @@ def run_ours(args):
         clk = clocks.stop()
         ms = e0.elapsed_time(e1)
         relres, _ = plan.residual(U, F)
+        # K1 residual kernel (not part of the solve): HBM roofline, 16 B/unknown
+        r0 = torch.cuda.Event(enable_timing=True)
+        r1 = torch.cuda.Event(enable_timing=True)
+        r0.record(stream)
+        plan.residual(U, F)
+        r1.record(stream)
+        stream.synchronize()
+        k1_ms = r0.elapsed_time(r1)
     ms_max = max_over_ranks(ms, dist, "cuda")
     value = aggregate_value(N, args.steps, world, ms_max)
 
@@ -274,6 +283,11 @@ def run_ours(args):
         "roofline": roofline,
         "e2e": e2e,
         "gpu_launches": int(t_n + s_n),
+        "k1_residual": {"ms": k1_ms, "gbs": 16.0 * N / (k1_ms / 1e3) / 1e9,
+                        "frac_hbm": 16.0 * N / (k1_ms / 1e3) / 1e9 / HBM_GBS,
+                        "bytes_alg": 16 * N},
+        "k3_scan": {"ms_per_launch": s_ms / s_n, "gbs": 16.0 * N / (s_ms / s_n / 1e3) / 1e9,
+                    "frac_hbm": 16.0 * N / (s_ms / s_n / 1e3) / 1e9 / HBM_GBS},
         "clocks": clk,
     }
     if rank == 0 and world == 1 and not args.no_cpu:

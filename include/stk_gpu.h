@@ -118,6 +118,12 @@ int64_t stkg_heat_workspace_bytes(const stkg_heat* plan);
  * bidiagonal recurrence of X^T F.  F, U device, N_h x N_t column-major.  F is not
  * modified; U may not alias F.  STKG_SINGULARITY if |d_j + lambda_i c_j| < 1e-300. */
 int stkg_heat_solve(stkg_heat* plan, const double* F, double* U);
+/* Factored load F = L R^T (RHSFactors / LowRank, stk/rhs_sep.hpp:99-104,
+ * stk/types.hpp:87-108): X^T F = (X^T L) R^T, so only the rank columns of L are transformed
+ * and the recurrence forms each transformed column on the fly; F is never materialised.
+ * L device n_x x rank, R device n_t x rank (column-major), 1 <= rank <= 16. */
+int stkg_heat_solve_factored(stkg_heat* plan, int64_t rank, const double* L, const double* R,
+                             double* U);
 /* Same with HOST buffers (pinned or pageable): H2D of F, the solve and the D2H of U are
  * pipelined over time chunks (the recurrence is causal in time).  Synchronous. */
 int stkg_heat_solve_host(stkg_heat* plan, const double* F_host, double* U_host);

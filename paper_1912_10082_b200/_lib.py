@@ -94,6 +94,8 @@ SIGNATURES = {
     "stkg_heat_destroy": (C.c_int, [C.c_void_p]),
     "stkg_heat_workspace_bytes": (C.c_int64, [C.c_void_p]),
     "stkg_heat_solve": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "stkg_heat_solve_factored": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
+                                           C.c_void_p]),
     "stkg_heat_solve_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "stkg_heat_apply": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "stkg_heat_residual": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, c_double_p, c_double_p]),

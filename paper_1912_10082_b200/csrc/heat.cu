@@ -30,6 +30,7 @@ struct stkg_heat {
   bool has_operator = false;
   DevBuf m_diag[3], m_off[3], a_diag[3], a_off[3];
   DevBuf scratch;   // nx * nt, device solve
+  DevBuf lfac;      // 2 * nx * rank, transformed load factors (factored solve)
   DevBuf carry;     // nx, modal state y_{l0-1} carried across time chunks
   DevBuf partials;  // reduction partials
   DevBuf scalars;   // device results of reductions
@@ -106,6 +107,34 @@ __global__ void __launch_bounds__(256) heat_scan_kernel(
   carry[i] = y;
 }
 
+// Factored load F = L R^T: the transformed load is never stored;
+// g~_j[i] = sum_r Lt[i, r] R[j, r] is formed in registers (Lt = X^T L, n_x x rank), and the
+// recurrence writes Y~ (n_x x n_t) -- 8 B/unknown of HBM traffic instead of 16.
+constexpr int kMaxFactorRank = 16;
+__global__ void __launch_bounds__(256) heat_scan_factored_kernel(
+    const double* __restrict__ Lt, const double* __restrict__ R, int rank, double* __restrict__ Y,
+    int64_t nx, int64_t nt, ModeLambda lam, const double* __restrict__ d_diag,
+    const double* __restrict__ d_sup, const double* __restrict__ c_diag,
+    const double* __restrict__ c_sup) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= nx) return;
+  const double li = lam(i);
+  double lt[kMaxFactorRank];
+#pragma unroll
+  for (int r = 0; r < kMaxFactorRank; ++r) lt[r] = r < rank ? Lt[int64_t(r) * nx + i] : 0.0;
+  double y = 0.0;
+  for (int64_t l = 0; l < nt; ++l) {
+    double g = 0.0;
+#pragma unroll
+    for (int r = 0; r < kMaxFactorRank; ++r)
+      if (r < rank) g += lt[r] * __ldg(R + int64_t(r) * nt + l);
+    const double piv = d_diag[l] + li * c_diag[l];
+    if (l > 0) g -= (d_sup[l - 1] + li * c_sup[l - 1]) * y;
+    y = g / piv;
+    __stcs(Y + l * nx + i, y);
+  }
+}
+
 // Singularity check of stk/sylvester.hpp:133-135, done once per plan: min over modes and
 // steps of |d_j + lambda_i c_j|.  Writes the first offending (i, j) it finds.
 __global__ void heat_pivot_check_kernel(int64_t nx, int64_t nt, ModeLambda lam,
@@ -136,6 +165,15 @@ struct Tri {  // symmetric tridiagonal 1D factor
   }
 };
 
+// Point tiles of 256 per CTA (x slowest ... z fastest); the U tile with a 1-wide halo is
+// staged in shared memory by cp.async in a 6-deep ring over time slices (5 slices in
+// flight while slice l is applied), so every U and F value crosses HBM once and the
+// loads for future slices cover the HBM latency.
+template <int NDIM> struct ApplyTile;
+template <> struct ApplyTile<1> { static constexpr int BX = 256, BY = 1, BZ = 1; };
+template <> struct ApplyTile<2> { static constexpr int BX = 8, BY = 32, BZ = 1; };
+template <> struct ApplyTile<3> { static constexpr int BX = 4, BY = 4, BZ = 16; };
+
 template <int NDIM, bool RESIDUAL>
 __global__ void __launch_bounds__(256) heat_apply_kernel(
     const double* __restrict__ U, const double* __restrict__ F, double* __restrict__ out,
@@ -143,85 +181,143 @@ __global__ void __launch_bounds__(256) heat_apply_kernel(
     Tri a2, const double* __restrict__ d_diag, const double* __restrict__ d_sup,
     const double* __restrict__ c_diag, const double* __restrict__ c_sup,
     double* __restrict__ partials) {
-  // sum-factorised stencil: z sums, then y sums, then x sums (SURVEY §8(d) K1 note)
+  using T = ApplyTile<NDIM>;
   constexpr int SY = NDIM >= 2 ? 3 : 1, SZ = NDIM == 3 ? 3 : 1;
+  constexpr int HX = T::BX + 2, HY = T::BY + (NDIM >= 2 ? 2 : 0), HZ = T::BZ + (NDIM == 3 ? 2 : 0);
+  constexpr int TE = HX * HY * HZ;
+  constexpr int kStages = 6;  // slices in flight per CTA: enough bytes to cover HBM latency
+  __shared__ double su[kStages][TE];
+  __shared__ double sf[kStages][256];
+
+  const int64_t tiles_x = (n0 + T::BX - 1) / T::BX, tiles_y = (n1 + T::BY - 1) / T::BY;
+  const int64_t tiles_z = (n2 + T::BZ - 1) / T::BZ;
+  int64_t b = blockIdx.x;
+  const int64_t tz = b % tiles_z;
+  b /= tiles_z;
+  const int64_t ty = b % tiles_y;
+  const int64_t tx = b / tiles_y;
+  (void)tiles_x;
+  const int64_t x0 = tx * T::BX, y0 = ty * T::BY, z0 = tz * T::BZ;
+  const int tid = threadIdx.x;
+  const int lx = tid / (T::BY * T::BZ), ly = (tid / T::BZ) % T::BY, lz = tid % T::BZ;
+  const int64_t ix = x0 + lx, iy = y0 + ly, iz = z0 + lz;
+  const bool valid = ix < n0 && iy < n1 && iz < n2;
   const int64_t nx = n0 * n1 * n2;
-  const int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t p = (ix * n1 + iy) * n2 + iz;
+
+  // Each thread copies at most kPer halo elements per slice; their in-slice offsets and
+  // validity are fixed for the whole time loop (computed once).
+  constexpr int kPer = (TE + 255) / 256;
+  int64_t hoff[kPer];
+  uint32_t hok = 0;
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    const int e = tid + 256 * k;
+    const int hx = e / (HY * HZ), hy = (e / HZ) % HY, hz = e % HZ;
+    const int64_t gx = x0 + hx - 1;
+    const int64_t gy = NDIM >= 2 ? y0 + hy - 1 : 0;
+    const int64_t gz = NDIM == 3 ? z0 + hz - 1 : 0;
+    const bool ok = e < TE && gx >= 0 && gx < n0 && gy >= 0 && gy < n1 && gz >= 0 && gz < n2;
+    hoff[k] = ok ? (gx * n1 + gy) * n2 + gz : 0;
+    if (ok) hok |= 1u << k;
+  }
+  auto load_slice = [&](int stage, int64_t l) {
+    const bool lin = l < nt;
+    const double* Ul = U + l * nx;
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int e = tid + 256 * k;
+      if (e < TE) {
+        const bool ok = lin && ((hok >> k) & 1u);
+        cp_async8(&su[stage][e], ok ? Ul + hoff[k] : U, ok);
+      }
+    }
+    if (RESIDUAL) {
+      const bool ok = lin && valid;
+      cp_async8(&sf[stage][tid], ok ? F + l * nx + p : F, ok);
+    }
+  };
+
+  // 1D weights of the point (zero outside the grid)
+  double wmx[3], wax[3], wmy[SY], way[SY], wmz[SZ], waz[SZ];
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    const bool in = valid && ix + q - 1 >= 0 && ix + q - 1 < n0;
+    wmx[q] = in ? m0.w(ix, q - 1) : 0.0;
+    wax[q] = in ? a0.w(ix, q - 1) : 0.0;
+  }
+#pragma unroll
+  for (int q = 0; q < SY; ++q) {
+    const int d = SY == 1 ? 0 : q - 1;
+    const bool in = valid && iy + d >= 0 && iy + d < n1;
+    wmy[q] = NDIM >= 2 ? (in ? m1.w(iy, d) : 0.0) : 1.0;
+    way[q] = NDIM >= 2 ? (in ? a1.w(iy, d) : 0.0) : 0.0;
+  }
+#pragma unroll
+  for (int q = 0; q < SZ; ++q) {
+    const int d = SZ == 1 ? 0 : q - 1;
+    const bool in = valid && iz + d >= 0 && iz + d < n2;
+    wmz[q] = NDIM == 3 ? (in ? m2.w(iz, d) : 0.0) : 1.0;
+    waz[q] = NDIM == 3 ? (in ? a2.w(iz, d) : 0.0) : 0.0;
+  }
+
+#pragma unroll
+  for (int st = 0; st < kStages - 1; ++st) {
+    load_slice(st, st);
+    cp_async_commit();
+  }
   double rr = 0.0, ff = 0.0;
-  if (p < nx) {
-    int64_t ix, iy = 0, iz = 0;
-    if (NDIM == 1) {
-      ix = p;
-    } else if (NDIM == 2) {
-      ix = p / n1;
-      iy = p % n1;
+  // out_l = d_l (M U_l) + ds_{l-1} (M U_{l-1}) + c_l (A U_l) + cs_{l-1} (A U_{l-1}): the
+  // stencil is applied to one slice per step and (M U, A U) of the previous slice are
+  // carried in registers.
+  double mu_prev = 0.0, au_prev = 0.0;
+  const int base = (lx * HY + (NDIM >= 2 ? ly : 0)) * HZ + (NDIM == 3 ? lz : 0);
+  // 3-point sums start from the first product (no 0 + x / 0 * x that IEEE forbids folding)
+  auto dot3 = [](const double* w, double a, double b, double c) {
+    return fma(w[2], c, fma(w[1], b, w[0] * a));
+  };
+  int cur = 0, nxt = kStages - 1;  // ring positions of slice l and slice l + kStages - 1
+  for (int64_t l = 0; l < nt; ++l) {
+    cp_async_wait<kStages - 2>();
+    __syncthreads();  // slice l landed for all threads; slice l-1's stage is free
+    load_slice(nxt, l + kStages - 1);
+    cp_async_commit();
+    const double* t = su[cur] + base;
+    double mu, au;
+    if constexpr (NDIM == 1) {
+      mu = dot3(wmx, t[0], t[1], t[2]);
+      au = dot3(wax, t[0], t[1], t[2]);
     } else {
-      iz = p % n2;
-      const int64_t r = p / n2;
-      iy = r % n1;
-      ix = r / n1;
-    }
-    double wmx[3], wax[3], wmy[SY], way[SY], wmz[SZ], waz[SZ];
-    bool inx[3], iny[SY], inz[SZ];
-#pragma unroll
-    for (int q = 0; q < 3; ++q) {
-      const bool in = ix + q - 1 >= 0 && ix + q - 1 < n0;
-      inx[q] = in;
-      wmx[q] = in ? m0.w(ix, q - 1) : 0.0;
-      wax[q] = in ? a0.w(ix, q - 1) : 0.0;
-    }
-#pragma unroll
-    for (int q = 0; q < SY; ++q) {
-      const int d = SY == 1 ? 0 : q - 1;
-      const bool in = iy + d >= 0 && iy + d < n1;
-      iny[q] = in;
-      wmy[q] = NDIM >= 2 ? (in ? m1.w(iy, d) : 0.0) : 1.0;
-      way[q] = NDIM >= 2 ? (in ? a1.w(iy, d) : 0.0) : 0.0;
-    }
-#pragma unroll
-    for (int q = 0; q < SZ; ++q) {
-      const int d = SZ == 1 ? 0 : q - 1;
-      const bool in = iz + d >= 0 && iz + d < n2;
-      inz[q] = in;
-      wmz[q] = NDIM == 3 ? (in ? m2.w(iz, d) : 0.0) : 1.0;
-      waz[q] = NDIM == 3 ? (in ? a2.w(iz, d) : 0.0) : 0.0;
-    }
-    double prev[3 * SY * SZ];
-#pragma unroll
-    for (int s = 0; s < 3 * SY * SZ; ++s) prev[s] = 0.0;
-    for (int64_t l = 0; l < nt; ++l) {
-      const double* Ul = U + l * nx + p;
-      const double dd = d_diag[l], cd = c_diag[l];
-      const double ds = l > 0 ? d_sup[l - 1] : 0.0, cs = l > 0 ? c_sup[l - 1] : 0.0;
-      double acc = 0.0;
+      double my[3], ay[3];
 #pragma unroll
       for (int qx = 0; qx < 3; ++qx) {
-        double ymp = 0.0, ymq = 0.0, yaq = 0.0;
+        if constexpr (NDIM == 2) {
+          const double* r = t + qx * HY;
+          my[qx] = dot3(wmy, r[0], r[1], r[2]);
+          ay[qx] = dot3(way, r[0], r[1], r[2]);
+        } else {
+          double mz[3], az[3];
 #pragma unroll
-        for (int qy = 0; qy < SY; ++qy) {
-          double zmp = 0.0, zmq = 0.0, zaq = 0.0;
-#pragma unroll
-          for (int qz = 0; qz < SZ; ++qz) {
-            const int s = (qx * SY + qy) * SZ + qz;
-            const int64_t delta = (qx - 1) * n1 * n2 + (SY == 1 ? 0 : (qy - 1) * n2) +
-                                  (SZ == 1 ? 0 : qz - 1);
-            const bool in = inx[qx] && iny[qy] && inz[qz];
-            const double u = in ? __ldg(Ul + delta) : 0.0;
-            const double P = dd * u + ds * prev[s];
-            const double Q = cd * u + cs * prev[s];
-            prev[s] = u;
-            zmp += wmz[qz] * P;
-            zmq += wmz[qz] * Q;
-            zaq += waz[qz] * Q;
+          for (int qy = 0; qy < 3; ++qy) {
+            const double* r = t + (qx * HY + qy) * HZ;
+            mz[qy] = dot3(wmz, r[0], r[1], r[2]);
+            az[qy] = dot3(waz, r[0], r[1], r[2]);
           }
-          ymp += wmy[qy] * zmp;
-          ymq += wmy[qy] * zmq;
-          yaq += way[qy] * zmq + wmy[qy] * zaq;
+          my[qx] = dot3(wmy, mz[0], mz[1], mz[2]);
+          ay[qx] = dot3(way, mz[0], mz[1], mz[2]) + dot3(wmy, az[0], az[1], az[2]);
         }
-        acc += wmx[qx] * ymp + wax[qx] * ymq + wmx[qx] * yaq;
       }
+      mu = dot3(wmx, my[0], my[1], my[2]);
+      au = dot3(wax, my[0], my[1], my[2]) + dot3(wmx, ay[0], ay[1], ay[2]);
+    }
+    const double dd = d_diag[l], cd = c_diag[l];
+    double acc = dd * mu + cd * au;
+    if (l > 0) acc += d_sup[l - 1] * mu_prev + c_sup[l - 1] * au_prev;
+    mu_prev = mu;
+    au_prev = au;
+    if (valid) {
       if (RESIDUAL) {
-        const double f = __ldcs(F + l * nx + p);
+        const double f = sf[cur][tid];
         const double r = f - acc;
         rr += r * r;
         ff += f * f;
@@ -229,7 +325,10 @@ __global__ void __launch_bounds__(256) heat_apply_kernel(
         out[l * nx + p] = acc;
       }
     }
+    cur = cur + 1 == kStages ? 0 : cur + 1;
+    nxt = nxt + 1 == kStages ? 0 : nxt + 1;
   }
+  cp_async_wait<0>();
   if (RESIDUAL) {
     __shared__ double red[8];
     rr = block_sum<256>(rr, red);
@@ -357,6 +456,18 @@ void run_chunk(stkg_heat& h, const double* F, double* U, double* S, int64_t l0, 
   }
 }
 
+// Inverse transforms only, from Y (which must be the buffer the first pass does not
+// write) into U; used by the factored solve.
+void inverse_passes(stkg_heat& h, const double* Y, double* U, double* S, int64_t ntc) {
+  const int d = h.ndim;
+  const double* src = Y;
+  for (int a = 0, k = 1; a < d; ++a, ++k) {
+    double* dst = ((d - k) % 2 == 0) ? U : S;
+    axis_pass(h, a, false, src, dst, ntc);
+    src = dst;
+  }
+}
+
 void check_solvable(const stkg_heat& h) {
   if (h.singular) {
     char buf[160];
@@ -366,9 +477,19 @@ void check_solvable(const stkg_heat& h) {
   }
 }
 
+template <int NDIM>
+int64_t apply_tiles(const stkg_heat& h) {
+  using T = ApplyTile<NDIM>;
+  return ceil_div(h.n[0], T::BX) * ceil_div(h.n[1], T::BY) * ceil_div(h.n[2], T::BZ);
+}
+
+int64_t apply_blocks(const stkg_heat& h) {
+  return h.ndim == 1 ? apply_tiles<1>(h) : (h.ndim == 2 ? apply_tiles<2>(h) : apply_tiles<3>(h));
+}
+
 template <int NDIM, bool RES>
 void launch_apply(stkg_heat& h, const double* U, const double* F, double* out) {
-  const unsigned blocks = static_cast<unsigned>(ceil_div(h.nx, 256));
+  const unsigned blocks = static_cast<unsigned>(apply_tiles<NDIM>(h));
   Tri m[3], a[3];
   for (int i = 0; i < 3; ++i) {
     m[i] = Tri{h.m_diag[i].p, h.m_off[i].p};
@@ -481,7 +602,7 @@ int stkg_heat_create(stkg_heat** out, const stkg_heat_desc* desc, void* cuda_str
       }
     }
     h->carry.alloc(h->nx);
-    h->partials.alloc(2 * ceil_div(h->nx, 256));
+    h->partials.alloc(2 * apply_blocks(*h));
     h->scalars.alloc(4);
     STKG_CUDA_CHECK(cudaMallocHost(&h->pinned, 4 * sizeof(double)));
     h->time_chunk = desc->time_chunk;
@@ -535,7 +656,7 @@ int stkg_heat_destroy(stkg_heat* h) {
 int64_t stkg_heat_workspace_bytes(const stkg_heat* h) {
   if (!h) return 0;
   int64_t b = 0;
-  const DevBuf* bufs[] = {&h->scratch, &h->carry, &h->partials, &h->pf[0], &h->pf[1],
+  const DevBuf* bufs[] = {&h->scratch, &h->lfac, &h->carry, &h->partials, &h->pf[0], &h->pf[1],
                           &h->pu[0],   &h->pu[1], &h->ps};
   for (auto* x : bufs) b += static_cast<int64_t>(x->n) * 8;
   for (int a = 0; a < h->ndim; ++a) b += static_cast<int64_t>(2 * h->X[a].n + h->lam[a].n) * 8;
@@ -549,6 +670,37 @@ int stkg_heat_solve(stkg_heat* h, const double* F, double* U) {
     check_solvable(*h);
     if (h->scratch.n < static_cast<size_t>(h->nx * h->nt)) h->scratch.alloc(h->nx * h->nt);
     run_chunk(*h, F, U, h->scratch.p, 0, h->nt);
+  });
+}
+
+int stkg_heat_solve_factored(stkg_heat* h, int64_t rank, const double* L, const double* R,
+                             double* U) {
+  return guarded([&] {
+    STKG_REQUIRE(h && L && R && U, STKG_ARGUMENT, "stkg_heat_solve_factored: null argument");
+    STKG_REQUIRE(rank >= 1 && rank <= kMaxFactorRank, STKG_ARGUMENT,
+                 "stkg_heat_solve_factored: rank must be in [1, 16]");
+    check_solvable(*h);
+    if (h->scratch.n < static_cast<size_t>(h->nx * h->nt)) h->scratch.alloc(h->nx * h->nt);
+    if (h->lfac.n < static_cast<size_t>(2 * h->nx * rank)) h->lfac.alloc(2 * h->nx * rank);
+    // forward transforms of the rank columns of L (treated as `rank` time slices)
+    double* t0 = h->lfac.p;
+    double* t1 = h->lfac.p + h->nx * rank;
+    const double* src = L;
+    for (int a = h->ndim - 1, k = 1; a >= 0; --a, ++k) {
+      double* dst = ((h->ndim - k) % 2 == 0) ? t0 : t1;
+      axis_pass(*h, a, true, src, dst, rank);
+      src = dst;
+    }
+    // the recurrence writes Y~ where the first inverse pass reads it
+    double* Y = (h->ndim % 2 == 0) ? U : h->scratch.p;
+    {
+      ProfScope ps(*h, 1);
+      heat_scan_factored_kernel<<<static_cast<unsigned>(ceil_div(h->nx, 256)), 256, 0, h->stream>>>(
+          src, R, static_cast<int>(rank), Y, h->nx, h->nt, mode_lambda(*h), h->d_diag.p,
+          h->d_sup.p, h->c_diag.p, h->c_sup.p);
+      STKG_CUDA_CHECK(cudaGetLastError());
+    }
+    inverse_passes(*h, Y, U, h->scratch.p, h->nt);
   });
 }
 
@@ -647,7 +799,7 @@ int stkg_heat_residual(stkg_heat* h, const double* U, const double* F, double* r
     STKG_REQUIRE(h->has_operator, STKG_ARGUMENT,
                  "stkg_heat_residual: plan was created without the spatial factors");
     dispatch_apply<true>(*h, U, F, nullptr);
-    sum_pairs_kernel<<<1, 256, 0, h->stream>>>(h->partials.p, ceil_div(h->nx, 256), h->scalars.p);
+    sum_pairs_kernel<<<1, 256, 0, h->stream>>>(h->partials.p, apply_blocks(*h), h->scalars.p);
     STKG_CUDA_CHECK(cudaGetLastError());
     STKG_CUDA_CHECK(cudaMemcpyAsync(h->pinned, h->scalars.p, 2 * sizeof(double),
                                     cudaMemcpyDeviceToHost, h->stream));

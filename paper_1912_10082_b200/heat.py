@@ -141,6 +141,19 @@ class HeatPlan:
         check(lib.stkg_heat_solve(self._h, C.c_void_p(_dev_ptr(F)), C.c_void_p(_dev_ptr(U))))
         return U
 
+    def solve_factored(self, L, R, out=None):
+        """Solve with a factored load F = L R^T (L: (rank, n_x) C-order == n_x x rank
+        column-major, R: (rank, n_t)); F is never formed."""
+        import torch
+        rank = L.numel() // self.nx
+        if L.numel() != rank * self.nx or R.numel() != rank * self.nt:
+            raise ArgumentError("solve_factored: factor shape mismatch")
+        U = torch.empty((self.nt, self.nx), dtype=torch.float64, device=L.device) if out is None else out
+        self._check_size(U)
+        check(lib.stkg_heat_solve_factored(self._h, rank, C.c_void_p(_dev_ptr(L)),
+                                           C.c_void_p(_dev_ptr(R)), C.c_void_p(_dev_ptr(U))))
+        return U
+
     def apply(self, U, out=None):
         """KronOp::apply of heat_kron_op: M U D + A U C."""
         import torch

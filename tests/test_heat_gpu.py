@@ -194,3 +194,20 @@ def test_host_path_bitwise_equal_device_path(stk, cuda):
     r1 = plan.residual(dev(Ud), dev(F))
     r2 = plan.residual(dev(Ud), dev(F))
     assert r1 == r2
+
+
+@pytest.mark.parametrize("ndim,n,nt,rank", [(1, 255, 256, 1), (2, 63, 40, 4), (3, 15, 12, 8),
+                                            (2, 17, 9, 16)])
+def test_factored_load_equals_dense_load(stk, orc, cuda, ndim, n, nt, rank):
+    """F = L R^T solved from its factors equals the dense-F solve and the oracle."""
+    plan, M, A, D, Cm = p1_setup(stk, ndim, n, nt)
+    rng = np.random.default_rng(rank)
+    L = rng.standard_normal((rank, n ** ndim))  # == n_x x rank column-major
+    R = rng.standard_normal((rank, nt))
+    F = R.T @ L  # (nt, n_x) == L R^T column-major
+    Uf = host(plan.solve_factored(dev(L), dev(R)))
+    Ud = host(plan.solve(dev(F)))
+    assert rel(Uf, Ud) < 1e-13
+    ms, as_, d, c = orc_factors(M, A, D, Cm, ndim)
+    Uref = orc.heat_decoupled([orc.p1_pencil_eig(ms[0], as_[0])] * ndim, d, c, F)
+    assert rel(Uf, Uref) < 1e-10
