@@ -27,6 +27,7 @@ struct GemmProblem {
   int64_t ldb = 0, strideB = 0;
   double* C = nullptr;        // M x N, column-major
   int64_t ldc = 0, strideC = 0;
+  const int* skip = nullptr;  // optional device flag: non-zero => the launch is a no-op
 };
 
 // Epilogues ------------------------------------------------------------------------
@@ -100,6 +101,7 @@ __device__ __forceinline__ void dmma_m16n8k4(double (&c)[4], double a0, double a
 template <class Cfg, class Epi>
 __global__ void __launch_bounds__(Cfg::kThreads, Cfg::kMinBlocks)
     gemm_f64_kernel(const GemmProblem p, const Epi epi) {
+  if (p.skip && *p.skip) return;  // device-side early exit (converged Krylov iteration)
   extern __shared__ __align__(16) double smem[];
   double* sA = smem;                                   // [STAGES][BK][kLdsA]
   double* sB = smem + Cfg::STAGES * Cfg::kStageA;      // [STAGES][BN][kLdsB]

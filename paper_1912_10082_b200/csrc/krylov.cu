@@ -1,5 +1,6 @@
 // Krylov solvers on device vectors: gmres (stk/outer_krylov.hpp:75-164) and PCG.
 #include <algorithm>
+#include <cstring>
 #include <chrono>
 #include <cmath>
 #include <string>
@@ -105,30 +106,6 @@ __global__ void add_kernel(const double* __restrict__ x, double* __restrict__ y,
     y[i] += x[i];
 }
 
-// x += a p; r -= a q; partial ||r||^2
-__global__ void __launch_bounds__(kReduceThreads) cg_update_kernel(
-    double a, const double* __restrict__ p, const double* __restrict__ q, double* __restrict__ x,
-    double* __restrict__ r, int64_t n, double* __restrict__ partials) {
-  __shared__ double red[kReduceThreads / 32];
-  double s = 0.0;
-  for (int64_t i = int64_t(blockIdx.x) * kReduceThreads + threadIdx.x; i < n;
-       i += int64_t(gridDim.x) * kReduceThreads) {
-    x[i] += a * p[i];
-    const double ri = r[i] - a * q[i];
-    r[i] = ri;
-    s += ri * ri;
-  }
-  s = block_sum<kReduceThreads>(s, red);
-  if (threadIdx.x == 0) partials[blockIdx.x] = s;
-}
-
-__global__ void xpby_kernel(const double* __restrict__ z, double b, double* __restrict__ p,
-                            int64_t n) {
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-       i += int64_t(gridDim.x) * blockDim.x)
-    p[i] = z[i] + b * p[i];
-}
-
 void report_history(stkg_report* rep, double v) {
   if (!rep) return;
   if (rep->rel_res_history && rep->history_length < rep->history_capacity)
@@ -189,7 +166,7 @@ void Krylov::ensure(int64_t cols, int64_t hcap) {
   if (partials.n < static_cast<size_t>(h * kReduceBlocks)) partials.alloc(h * kReduceBlocks);
   if (scalars.n < static_cast<size_t>(h)) scalars.alloc(h);
   if (hvec.n < static_cast<size_t>(h)) hvec.alloc(h);
-  pin(8);
+  pin(static_cast<int>(h));  // once: cudaMallocHost synchronises the device
 }
 
 double kdot(Krylov& k, const double* x, const double* y) {
@@ -344,6 +321,125 @@ void gmres_run(Krylov& k, const DevOp& apply, const DevOp* precond, const double
   }
 }
 
+namespace {
+
+// PCG scalars live on the device so that an iteration needs no host round trip; the host
+// only polls `done` every kPcgChunk iterations.
+struct PcgState {
+  double rz, pq, alpha, beta, normb, tol;
+  int done, iters, error, maxit;
+};
+constexpr int kPcgChunk = 8;
+
+__device__ double sum_fixed(const double* partials, int count, double* red) {
+  double s = 0.0;
+  for (int b = threadIdx.x; b < count; b += kReduceThreads) s += partials[b];
+  return block_sum<kReduceThreads>(s, red);
+}
+
+__global__ void __launch_bounds__(kReduceThreads) pcg_init_kernel(const double* partials_rz,
+                                                                  PcgState* st, double normb,
+                                                                  double tol, int maxit) {
+  __shared__ double red[kReduceThreads / 32];
+  const double rz = sum_fixed(partials_rz, kReduceBlocks, red);
+  if (threadIdx.x == 0) {
+    st->rz = rz;
+    st->normb = normb;
+    st->tol = tol;
+    st->maxit = maxit;
+    st->done = 0;
+    st->iters = 0;
+    st->error = 0;
+  }
+}
+
+__global__ void __launch_bounds__(kReduceThreads) pcg_alpha_kernel(const double* partials,
+                                                                   PcgState* st) {
+  __shared__ double red[kReduceThreads / 32];
+  if (st->done) return;
+  const double pq = sum_fixed(partials, kReduceBlocks, red);
+  if (threadIdx.x == 0) {
+    st->pq = pq;
+    if (!(pq > 0.0) || !isfinite(pq)) {
+      st->error = 1;
+      st->done = 1;
+    } else {
+      st->alpha = st->rz / pq;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kReduceThreads) pcg_update_kernel(
+    const PcgState* st, const double* __restrict__ p, const double* __restrict__ q,
+    double* __restrict__ x, double* __restrict__ r, int64_t n, double* __restrict__ partials) {
+  __shared__ double red[kReduceThreads / 32];
+  if (st->done) return;
+  const double a = st->alpha;
+  double s = 0.0;
+  for (int64_t i = int64_t(blockIdx.x) * kReduceThreads + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * kReduceThreads) {
+    x[i] += a * p[i];
+    const double ri = r[i] - a * q[i];
+    r[i] = ri;
+    s += ri * ri;
+  }
+  s = block_sum<kReduceThreads>(s, red);
+  if (threadIdx.x == 0) partials[blockIdx.x] = s;
+}
+
+__global__ void __launch_bounds__(kReduceThreads) pcg_check_kernel(const double* partials,
+                                                                   PcgState* st, double* hist) {
+  __shared__ double red[kReduceThreads / 32];
+  if (st->done) return;
+  const double r2 = sum_fixed(partials, kReduceBlocks, red);
+  if (threadIdx.x == 0) {
+    const double relres = sqrt(r2) / st->normb;
+    hist[st->iters] = relres;
+    st->iters += 1;
+    if (!isfinite(relres)) {
+      st->error = 2;
+      st->done = 1;
+    } else if (relres <= st->tol || st->iters >= st->maxit) {
+      st->done = 1;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kReduceThreads) pcg_dot_kernel(
+    const PcgState* st, const double* __restrict__ x, const double* __restrict__ y, int64_t n,
+    double* __restrict__ partials) {
+  __shared__ double red[kReduceThreads / 32];
+  if (st->done) return;
+  double s = 0.0;
+  for (int64_t i = int64_t(blockIdx.x) * kReduceThreads + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * kReduceThreads)
+    s += x[i] * y[i];
+  s = block_sum<kReduceThreads>(s, red);
+  if (threadIdx.x == 0) partials[blockIdx.x] = s;
+}
+
+__global__ void __launch_bounds__(kReduceThreads) pcg_beta_kernel(const double* partials,
+                                                                  PcgState* st) {
+  __shared__ double red[kReduceThreads / 32];
+  if (st->done) return;
+  const double rz_new = sum_fixed(partials, kReduceBlocks, red);
+  if (threadIdx.x == 0) {
+    st->beta = rz_new / st->rz;
+    st->rz = rz_new;
+  }
+}
+
+__global__ void pcg_xpby_kernel(const PcgState* st, const double* __restrict__ z,
+                                double* __restrict__ p, int64_t n) {
+  if (st->done) return;
+  const double b = st->beta;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    p[i] = z[i] + b * p[i];
+}
+
+}  // namespace
+
 void pcg_run(Krylov& k, const DevOp& apply, const DevOp& precond, const double* b, double* x,
              double tol, int maxit, stkg_report* rep) {
   STKG_REQUIRE(tol > 0.0 && tol < 1.0, STKG_ARGUMENT, "pcg: tol must be in (0,1)");
@@ -365,40 +461,51 @@ void pcg_run(Krylov& k, const DevOp& apply, const DevOp& precond, const double* 
     if (rep) rep->converged = 1;
     return;
   }
+  if (k.state_buf.n < (sizeof(PcgState) + 7) / 8) k.state_buf.alloc((sizeof(PcgState) + 7) / 8);
+  if (k.hist_buf.n < static_cast<size_t>(maxit)) k.hist_buf.alloc(maxit);
+  PcgState* st = reinterpret_cast<PcgState*>(k.state_buf.p);
+  double* hist = k.hist_buf.p;
   double *r = k.r.p, *z = k.z.p, *p = k.p.p, *q = k.q.p;
   STKG_CUDA_CHECK(cudaMemcpyAsync(r, b, sizeof(double) * N, cudaMemcpyDeviceToDevice, s));
   precond(r, z);
   STKG_CUDA_CHECK(cudaMemcpyAsync(p, z, sizeof(double) * N, cudaMemcpyDeviceToDevice, s));
-  double rz = kdot(k, r, z);
-  int it = 0;
-  bool converged = false;
-  while (it < maxit) {
-    apply(p, q);
-    const double pq = kdot(k, p, q);
-    if (!std::isfinite(pq) || pq <= 0.0)
-      throw Error(STKG_NUMERIC, "pcg: non-positive curvature at iteration " + std::to_string(it + 1));
-    const double alpha = rz / pq;
-    cg_update_kernel<<<kReduceBlocks, kReduceThreads, 0, s>>>(alpha, p, q, x, r, N, k.partials.p);
-    sum_partials_kernel<<<1, kReduceThreads, 0, s>>>(k.partials.p, kReduceBlocks, k.scalars.p);
-    STKG_CUDA_CHECK(cudaGetLastError());
-    double r2;
-    fetch(k, 1, &r2);
-    ++it;
-    const double relres = std::sqrt(r2) / norm_b;
-    report_history(rep, relres);
-    if (!std::isfinite(relres))
-      throw Error(STKG_NUMERIC, "pcg: non-finite value at iteration " + std::to_string(it));
-    if (relres <= tol) {
-      converged = true;
-      break;
+  dot_partials_kernel<<<kReduceBlocks, kReduceThreads, 0, s>>>(r, z, N, k.partials.p);
+  pcg_init_kernel<<<1, kReduceThreads, 0, s>>>(k.partials.p, st, norm_b, tol, maxit);
+  STKG_CUDA_CHECK(cudaGetLastError());
+  k.skip = &st->done;  // library operators turn into no-ops once the device test fires
+  PcgState hs{};
+  k.pin(sizeof(PcgState) / 8 + 1);
+  int enqueued = 0;
+  while (true) {
+    for (int c = 0; c < kPcgChunk && enqueued < maxit; ++c, ++enqueued) {
+      apply(p, q);
+      pcg_dot_kernel<<<kReduceBlocks, kReduceThreads, 0, s>>>(st, p, q, N, k.partials.p);
+      pcg_alpha_kernel<<<1, kReduceThreads, 0, s>>>(k.partials.p, st);
+      pcg_update_kernel<<<kReduceBlocks, kReduceThreads, 0, s>>>(st, p, q, x, r, N, k.partials.p);
+      pcg_check_kernel<<<1, kReduceThreads, 0, s>>>(k.partials.p, st, hist);
+      precond(r, z);
+      pcg_dot_kernel<<<kReduceBlocks, kReduceThreads, 0, s>>>(st, r, z, N, k.partials.p);
+      pcg_beta_kernel<<<1, kReduceThreads, 0, s>>>(k.partials.p, st);
+      pcg_xpby_kernel<<<kEwBlocks, 256, 0, s>>>(st, z, p, N);
     }
-    precond(r, z);
-    const double rz_new = kdot(k, r, z);
-    const double beta = rz_new / rz;
-    rz = rz_new;
-    xpby_kernel<<<kEwBlocks, 256, 0, s>>>(z, beta, p, N);
+    STKG_CUDA_CHECK(cudaGetLastError());
+    STKG_CUDA_CHECK(cudaMemcpyAsync(k.pinned, st, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
+    STKG_CUDA_CHECK(cudaStreamSynchronize(s));
+    std::memcpy(&hs, k.pinned, sizeof(PcgState));
+    if (hs.done || enqueued >= maxit) break;
   }
-  apply(x, k.r.p);
+  k.skip = nullptr;
+  if (hs.error == 1)
+    throw Error(STKG_NUMERIC, "pcg: non-positive curvature at iteration " + std::to_string(hs.iters + 1));
+  if (hs.error == 2)
+    throw Error(STKG_NUMERIC, "pcg: non-finite value at iteration " + std::to_string(hs.iters));
+  const int it = hs.iters;
+  std::vector<double> h(static_cast<size_t>(it));
+  if (it > 0)
+    STKG_CUDA_CHECK(cudaMemcpy(h.data(), hist, sizeof(double) * it, cudaMemcpyDeviceToHost));
+  for (int i = 0; i < it; ++i) report_history(rep, h[i]);
+  const bool converged = it > 0 && h[it - 1] <= tol;
+  apply(x, k.r.p);  // true final residual
   sub_from_kernel<<<kEwBlocks, 256, 0, s>>>(b, k.r.p, N);
   const double fr = knorm(k, k.r.p) / norm_b;
   if (rep) {

@@ -21,6 +21,11 @@ struct Krylov {
   DevBuf hvec, partials, scalars;
   double* pinned = nullptr;
   int pinned_cap = 0;
+  // Device flag set when a device-side stopping test fires; operators built on library
+  // kernels may pass it to their launches to turn the remaining queued work into no-ops.
+  const int* skip = nullptr;
+  DevBuf state_buf;  // PCG device scalars
+  DevBuf hist_buf;   // device residual history
   Krylov() = default;
   Krylov(const Krylov&) = delete;
   Krylov& operator=(const Krylov&) = delete;

@@ -39,50 +39,68 @@ struct stkg_wave {
 namespace {
 
 // ------------------------------------------------------------------------------ K5 --
-// Tile of TI (space) x TJ (time) outputs; U tile with a 3-wide halo on both axes is staged
-// in shared memory once; the temporal products V_p = U T_p^T are formed for the TI+6 halo
-// rows, then the spatial bands are applied.  U and out each cross HBM/L2 once.
-constexpr int TI = 64, TJ = 16, KThreads = 256;
+// Tile of TI (space) x TJ (time) outputs.  The U tile with a 3-wide halo on both axes and
+// the band coefficients of the tile's rows/columns are staged in shared memory once; the
+// temporal products V_p = U T_p^T are formed for the TI+6 halo rows, then the spatial
+// bands are applied.  U and out each cross L2/HBM once (16 B/unknown).
+constexpr int TI = 32, TJ = 16, KThreads = 256;
+constexpr int TIH = TI + 2 * kHalf, TJH = TJ + 2 * kHalf;
 
 __global__ void __launch_bounds__(KThreads) wave_apply_kernel(
     const double* __restrict__ U, double* __restrict__ out, int64_t nh, int64_t nt,
     const double* __restrict__ S0, const double* __restrict__ S1, const double* __restrict__ S2,
-    const double* __restrict__ T0, const double* __restrict__ T1, const double* __restrict__ T2) {
-  __shared__ double su[TJ + 2 * kHalf][TI + 2 * kHalf];  // [time][space]
-  __shared__ double sv[kTerms][TJ][TI + 2 * kHalf];
+    const double* __restrict__ T0, const double* __restrict__ T1, const double* __restrict__ T2,
+    const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  __shared__ double su[TJH][TIH];           // [time][space]
+  __shared__ double sv[kTerms][TJ][TIH];    // temporal products
+  __shared__ double st[kTerms][kBand][TJ];  // temporal band coefficients of the tile columns
+  __shared__ double ss[kTerms][kBand][TI];  // spatial band coefficients of the tile rows
   const int64_t i0 = int64_t(blockIdx.x) * TI, j0 = int64_t(blockIdx.y) * TJ;
-  for (int e = threadIdx.x; e < (TJ + 2 * kHalf) * (TI + 2 * kHalf); e += KThreads) {
-    const int jj = e / (TI + 2 * kHalf), ii = e % (TI + 2 * kHalf);
+  for (int e = threadIdx.x; e < TJH * TIH; e += KThreads) {
+    const int jj = e / TIH, ii = e % TIH;
     const int64_t gi = i0 + ii - kHalf, gj = j0 + jj - kHalf;
     su[jj][ii] = (gi >= 0 && gi < nh && gj >= 0 && gj < nt) ? U[gj * nh + gi] : 0.0;
   }
-  __syncthreads();
-  const double* Tp[kTerms] = {T0, T1, T2};
-  for (int e = threadIdx.x; e < TJ * (TI + 2 * kHalf); e += KThreads) {
-    const int jj = e / (TI + 2 * kHalf), ii = e % (TI + 2 * kHalf);
+  for (int e = threadIdx.x; e < kTerms * kBand * TJ; e += KThreads) {
+    const int t = e / (kBand * TJ), b = (e / TJ) % kBand, jj = e % TJ;
     const int64_t gj = j0 + jj;
+    const double* T = t == 0 ? T0 : (t == 1 ? T1 : T2);
+    st[t][b][jj] = gj < nt ? T[b * nt + gj] : 0.0;
+  }
+  for (int e = threadIdx.x; e < kTerms * kBand * TI; e += KThreads) {
+    const int t = e / (kBand * TI), a = (e / TI) % kBand, ii = e % TI;
+    const int64_t gi = i0 + ii;
+    const double* S = t == 0 ? S0 : (t == 1 ? S1 : S2);
+    ss[t][a][ii] = gi < nh ? S[a * nh + gi] : 0.0;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < TJ * TIH; e += KThreads) {
+    const int jj = e / TIH, ii = e % TIH;
+    double u[kBand];
+#pragma unroll
+    for (int b = 0; b < kBand; ++b) u[b] = su[jj + b][ii];
 #pragma unroll
     for (int t = 0; t < kTerms; ++t) {
-      double acc = 0.0;
-      if (gj < nt) {
+      double acc = st[t][0][jj] * u[0];
 #pragma unroll
-        for (int b = 0; b < kBand; ++b) acc += su[jj + b][ii] * __ldg(Tp[t] + b * nt + gj);
-      }
+      for (int b = 1; b < kBand; ++b) acc = fma(st[t][b][jj], u[b], acc);
       sv[t][jj][ii] = acc;
     }
   }
   __syncthreads();
-  const double* Sp[kTerms] = {S0, S1, S2};
   for (int e = threadIdx.x; e < TJ * TI; e += KThreads) {
     const int jj = e / TI, ii = e % TI;
     const int64_t gi = i0 + ii, gj = j0 + jj;
-    if (gi >= nh || gj >= nt) continue;
     double acc = 0.0;
 #pragma unroll
-    for (int t = 0; t < kTerms; ++t)
+    for (int t = 0; t < kTerms; ++t) {
+      double part = ss[t][0][ii] * sv[t][jj][ii];
 #pragma unroll
-      for (int a = 0; a < kBand; ++a) acc += __ldg(Sp[t] + a * nh + gi) * sv[t][jj][ii + a];
-    out[gj * nh + gi] = acc;
+      for (int a = 1; a < kBand; ++a) part = fma(ss[t][a][ii], sv[t][jj][ii + a], part);
+      acc = t == 0 ? part : acc + part;
+    }
+    if (gi < nh && gj < nt) out[gj * nh + gi] = acc;
   }
 }
 
@@ -106,15 +124,18 @@ std::vector<double> band_transpose(const double* band, int64_t n) {
 
 // ------------------------------------------------------------------------ building blocks
 void apply_op(stkg_wave& w, const double* x, double* y) {
+  // (w.krylov.skip: device flag of a converged PCG; the kernel is a no-op once it is set)
   dim3 grid(static_cast<unsigned>(ceil_div(w.nh, TI)), static_cast<unsigned>(ceil_div(w.nt, TJ)));
   wave_apply_kernel<<<grid, KThreads, 0, w.stream>>>(x, y, w.nh, w.nt, w.S[0].p, w.S[1].p,
-                                                    w.S[2].p, w.T[0].p, w.T[1].p, w.T[2].p);
+                                                    w.S[2].p, w.T[0].p, w.T[1].p, w.T[2].p,
+                                                    w.krylov.skip);
   STKG_CUDA_CHECK(cudaGetLastError());
 }
 
 void precond_solve(stkg_wave& w, const double* v, double* out) {
   const int64_t nh = w.nh, nt = w.nt;
   GemmProblem p;
+  p.skip = w.krylov.skip;
   // t1 = Xs^T V   (stk/sylvester.hpp:171, evaluated left to right as Eigen does)
   p.M = nh; p.K = nh; p.N = nt;
   p.A = w.XsT.p; p.lda = nh; p.B = v; p.ldb = nh; p.C = w.t1.p; p.ldc = nh;

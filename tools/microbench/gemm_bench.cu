@@ -15,6 +15,10 @@ using C5 = GemmCfg<64, 64, 16, 32, 32, 4, 3>;
 using C12 = GemmCfg<64, 64, 16, 32, 32, 3, 3>;
 using C13 = GemmCfg<64, 128, 16, 32, 64, 3, 2>;
 using C14 = GemmCfg<64, 64, 32, 32, 32, 2, 3>;
+using C15 = GemmCfg<32, 64, 32, 32, 32, 2, 4>;
+using C16 = GemmCfg<64, 32, 32, 32, 32, 2, 4>;
+using C17 = GemmCfg<32, 32, 32, 32, 32, 2, 8>;
+using C18 = GemmCfg<64, 64, 16, 32, 32, 3, 3>;
 template <class Cfg>
 float run(const GemmProblem& p, int reps) {
   cudaEvent_t a, b;
@@ -89,6 +93,10 @@ int main() {
     report("C12 64x64x16 s3 x3", run<C12>(s.p, reps));
     report("C13 64x128x16 s3 x2", run<C13>(s.p, reps));
     report("C14 64x64x32 s2 x3", run<C14>(s.p, reps));
+    report("C15 32x64x32 s2 x4 2w", run<C15>(s.p, reps));
+    report("C16 64x32x32 s2 x4 2w", run<C16>(s.p, reps));
+    report("C17 32x32x32 s2 x8 1w", run<C17>(s.p, reps));
+    report("C18 64x64x16 s3 x3", run<C18>(s.p, reps));
   }
   cudaError_t e = cudaGetLastError();
   printf("status %s\n", cudaGetErrorString(e));
