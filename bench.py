@@ -10,9 +10,13 @@ solve F -> U (solve_projected_heat_with in tensor form: DMMA transforms + modal 
                barrier + synchronize on both sides, max over ranks).
 * e2e        : unknowns/s through the public host-buffer API (stkg_heat_solve_host) with
                the H2D of F and the D2H of U (pinned host memory) inside the timed region.
-* roofline   : dominant kernel = the DMMA GEMM transforms; achieved = 2 n flops per
-               unknown per transform launch / mean launch time (CUDA events around every
-               launch on the plan stream), peak = measured DMMA FP64 peak.
+* roofline   : dominant kernel = the axis-transform kernel of the headline backend:
+               --transform dst (default): FP64 Stockham-FFT sine transforms, HBM-bound,
+               achieved = 16 B/unknown per axis pass / mean launch time vs measured HBM BW;
+               --transform dense: DMMA GEMMs, achieved = 2n flop/unknown per pass / mean
+               launch time vs the measured DMMA FP64 peak.  Launch times come from CUDA
+               events around every launch on the plan stream.  The other backend is timed
+               too and reported under "alt_path".
 * cpu_baseline / --impl reference : the oracle port of solve_projected_heat_with
                (oracle/oracle.py::heat_decoupled, numpy + multithreaded BLAS) on a bounded
                causal prefix of the same workload, on this host's cores.
@@ -120,13 +124,9 @@ def aggregate_value(unknowns_per_step: int, steps: int, world: int, ms_max: floa
     return world * unknowns_per_step * steps / (ms_max / 1e3)
 
 
-def build_plan(stk, cfg, stream=None, time_chunk=0):
-    g = stk.SpaceGrid1D(0.0, 1.0, cfg.n)
-    M, A = stk.fem1d_matrices(g)
-    D, Cm = stk.heat_time_matrices(stk.TimeGrid(cfg.nt, 1.0))
-    eig = stk.TensorEigPair([stk.p1_eigpair(g)] * cfg.ndim)
-    return stk.HeatPlan(eig, D, Cm, [M] * cfg.ndim, [A] * cfg.ndim, stream=stream,
-                        time_chunk=time_chunk)
+def build_plan(stk, cfg, stream=None, time_chunk=0, transform="dst"):
+    return stk.HeatPlan.p1_uniform(cfg.ndim, cfg.n, cfg.nt, stream=stream, time_chunk=time_chunk,
+                                   transform=transform)
 
 
 def cpu_reference_run(cfg, steps: int, seed: int = 0):
@@ -142,11 +142,11 @@ def cpu_reference_run(cfg, steps: int, seed: int = 0):
     return time.perf_counter() - t0
 
 
-def traffic_from_profiles():
+def traffic_from_profiles(kind: str = "gemm"):
     p = ROOT / "profiles" / "traffic.json"
     if p.exists():
         try:
-            return json.loads(p.read_text()).get("gemm_dram_bytes_per_launch")
+            return json.loads(p.read_text()).get(f"{kind}_dram_bytes_per_launch")
         except Exception:
             return None
     return None
@@ -181,6 +181,66 @@ def run_reference(args):
     return 0
 
 
+def _timed_path(stk, inputs, cfg, transform, args, stream, barrier, F, U, with_clocks):
+    """Warm up and time args.steps solves of one transform backend on the plan stream."""
+    import torch
+    plan = build_plan(stk, cfg, stream=stream.cuda_stream, transform=transform)
+    for _ in range(args.warmup):
+        plan.solve(F, out=U)
+    stream.synchronize()
+    clocks = ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) if with_clocks else None
+    if clocks:
+        clocks.start()
+    barrier()
+    torch.cuda.synchronize()
+    plan.profile_begin()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        plan.solve(F, out=U)
+    e1.record(stream)
+    stream.synchronize()
+    prof = plan.profile_end()
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop() if clocks else None
+    ms = e0.elapsed_time(e1)
+    relres, _ = plan.residual(U, F)
+    t_ms, t_n = prof["transform"]
+    s_ms, s_n = prof["scan"]
+    N = cfg.unknowns
+    if transform == "dense":
+        flops = 2.0 * cfg.n * N  # 2n flop per unknown per axis transform launch
+        achieved = flops / (t_ms / t_n / 1e3) / 1e12
+        roof = {"bound": "tensor", "kernel": "gemm_f64_kernel (DMMA basis transforms)",
+                "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic_from_profiles(),
+                "peak_source": FP64_PEAK_SOURCE,
+                "whole_solve_frac": (2 * cfg.ndim * flops * args.steps / (ms / 1e3) / 1e12)
+                / FP64_PEAK_TFLOPS}
+    else:
+        bytes_launch = 16.0 * N  # read + write each unknown once per axis pass
+        achieved = bytes_launch / (t_ms / t_n / 1e3) / 1e9
+        L = 2 * (cfg.n + 1)
+        fft_flops = 5.0 * L * np.log2(L) / 2.0 / cfg.n  # per element and axis pass
+        roof = {"bound": "hbm", "kernel": "dst_axis_kernel (FP64 Stockham FFT sine transform)",
+                "achieved": achieved, "peak": HBM_GBS, "unit": "GB/s",
+                "frac": achieved / HBM_GBS, "traffic": traffic_from_profiles("dst"),
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+                "flop_per_unknown_per_pass": fft_flops,
+                "whole_solve_frac": ((2 * cfg.ndim + 1) * 16.0 * N * args.steps / (ms / 1e3) / 1e9)
+                / HBM_GBS}
+    roof["share_of_step"] = t_ms / ms
+    roof["scan_share_of_step"] = s_ms / ms
+    out = {"transform": transform, "ms_per_step": ms / args.steps, "ms": ms,
+           "value": N * args.steps / (ms / 1e3), "relres_gpu_k1": relres, "roofline": roof,
+           "launches": int(t_n + s_n),
+           "k3_scan": {"ms_per_launch": s_ms / s_n, "gbs": 16.0 * N / (s_ms / s_n / 1e3) / 1e9,
+                       "frac_hbm": 16.0 * N / (s_ms / s_n / 1e3) / 1e9 / HBM_GBS}}
+    return plan, out, clk
+
+
 def run_ours(args):
     import torch
     rank, world, local = dist_env()
@@ -199,33 +259,13 @@ def run_ours(args):
         if dist is not None:
             dist.barrier()
 
+    main = args.transform
+    alt = "dense" if main == "dst" else "dst"
     with torch.cuda.stream(stream):
-        plan = build_plan(stk, cfg, stream=stream.cuda_stream)
         F = inputs.heat_rhs_device(cfg, seed=rank)
         U = torch.empty_like(F)
         stream.synchronize()
-        for _ in range(args.warmup):
-            plan.solve(F, out=U)
-        stream.synchronize()
-        # ---- device-resident timed region -------------------------------------------
-        clocks = ClockSampler(local)
-        clocks.start()
-        barrier()
-        torch.cuda.synchronize()
-        plan.profile_begin()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(args.steps):
-            plan.solve(F, out=U)
-        e1.record(stream)
-        stream.synchronize()
-        prof = plan.profile_end()
-        torch.cuda.synchronize()
-        barrier()
-        clk = clocks.stop()
-        ms = e0.elapsed_time(e1)
-        relres, _ = plan.residual(U, F)
+        plan, res, clk = _timed_path(stk, inputs, cfg, main, args, stream, barrier, F, U, True)
         # K1 residual kernel (not part of the solve): HBM roofline, 16 B/unknown
         r0 = torch.cuda.Event(enable_timing=True)
         r1 = torch.cuda.Event(enable_timing=True)
@@ -234,7 +274,13 @@ def run_ours(args):
         r1.record(stream)
         stream.synchronize()
         k1_ms = r0.elapsed_time(r1)
-    ms_max = max_over_ranks(ms, dist, "cuda")
+        plan.close()
+        alt_res = None
+        if not args.no_alt:
+            aplan, alt_res, _ = _timed_path(stk, inputs, cfg, alt, args, stream, barrier, F, U,
+                                            False)
+            aplan.close()
+    ms_max = max_over_ranks(res["ms"], dist, "cuda")
     value = aggregate_value(N, args.steps, world, ms_max)
 
     # ---- end to end through the public host-buffer API --------------------------------
@@ -245,7 +291,8 @@ def run_ours(args):
         Fh.copy_(F)
         del U
         torch.cuda.empty_cache()
-        plan_h = build_plan(stk, cfg, stream=stream.cuda_stream, time_chunk=args.time_chunk)
+        plan_h = build_plan(stk, cfg, stream=stream.cuda_stream, time_chunk=args.time_chunk,
+                            transform=main)
         plan_h.solve_host(Fh.numpy(), out=Uh.numpy())  # warm-up (allocates chunk buffers)
         barrier()
         torch.cuda.synchronize()
@@ -260,36 +307,26 @@ def run_ours(args):
                "steps": args.e2e_steps, "api": "stkg_heat_solve_host (pinned host buffers)"}
         plan_h.close()
 
-    # ---- roofline of the dominant kernel -------------------------------------------------
-    t_ms, t_n = prof["transform"]
-    s_ms, s_n = prof["scan"]
-    flops_per_launch = 2.0 * cfg.n * N  # 2n flop per unknown per axis transform pass
-    achieved = flops_per_launch / (t_ms / t_n / 1e3) / 1e12
-    roofline = {"bound": "tensor", "kernel": "gemm_f64_kernel (DMMA transforms)",
-                "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic_from_profiles(),
-                "peak_source": FP64_PEAK_SOURCE,
-                "share_of_step": t_ms / ms, "scan_share_of_step": s_ms / ms,
-                "whole_solve_frac": (2 * cfg.ndim * flops_per_launch * args.steps /
-                                     (ms / 1e3) / 1e12) / FP64_PEAK_TFLOPS}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": cfg.name, "unknowns_per_step": N, "n": cfg.n, "nt": cfg.nt,
+                   "transform": main,
                    "parallelism": "replicas" if world > 1 else "single",
                    "l2_flush": "inputs larger than L2 (F, U 8.6 GB each)",
-                   "relres_gpu_k1": relres},
-        "roofline": roofline,
+                   "relres_gpu_k1": res["relres_gpu_k1"]},
+        "roofline": res["roofline"],
         "e2e": e2e,
-        "gpu_launches": int(t_n + s_n),
+        "gpu_launches": res["launches"],
         "k1_residual": {"ms": k1_ms, "gbs": 16.0 * N / (k1_ms / 1e3) / 1e9,
                         "frac_hbm": 16.0 * N / (k1_ms / 1e3) / 1e9 / HBM_GBS,
                         "bytes_alg": 16 * N},
-        "k3_scan": {"ms_per_launch": s_ms / s_n, "gbs": 16.0 * N / (s_ms / s_n / 1e3) / 1e9,
-                    "frac_hbm": 16.0 * N / (s_ms / s_n / 1e3) / 1e9 / HBM_GBS},
+        "k3_scan": res["k3_scan"],
         "clocks": clk,
     }
+    if alt_res is not None:
+        line["alt_path"] = alt_res
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu_t = cpu_reference_run(cfg, args.ref_sample)
         cpu_v = cfg.nx * args.ref_sample / cpu_t
@@ -300,7 +337,6 @@ def run_ours(args):
                                           f"{cpu_t:.2f} s"}
     if rank == 0:
         print(json.dumps(line), flush=True)
-    plan.close()
     if dist is not None:
         dist.destroy_process_group()
     return 0
@@ -318,6 +354,9 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=CPU_SAMPLE_STEPS)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-alt", action="store_true", help="skip timing the other transform backend")
+    ap.add_argument("--transform", choices=["dst", "dense"], default="dst",
+                    help="headline backend: P1 fast sine transforms (dst) or dense DMMA GEMMs")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)

@@ -108,7 +108,16 @@ typedef struct stkg_heat_desc {
   const double* a_diag[3];  /* host, per-axis tridiagonal A_axis */
   const double* a_off[3];
   int64_t time_chunk;       /* time slices per pipeline chunk for *_host calls (0 = auto) */
+  /* Transform backend.  STKG_TRANSFORM_DENSE: X[a] is applied as a dense DMMA GEMM (any
+   * EigPair).  STKG_TRANSFORM_P1_DST: the axes carry the closed-form uniform-P1 eigenbasis
+   * X = S diag(mu^-1/2) of fem1d_matrices on a grid of spacing p1_h[a],
+   * applied as an O(n log n) FP64 sine transform; needs n[a] + 1 a power of two in
+   * [16, 2048]; X[a] is not read.  lambdas[a] are used by the recurrence in both modes. */
+  int transform;
+  double p1_h[3];
 } stkg_heat_desc;
+
+enum { STKG_TRANSFORM_DENSE = 0, STKG_TRANSFORM_P1_DST = 1 };
 
 int stkg_heat_create(stkg_heat** plan, const stkg_heat_desc* desc, void* cuda_stream);
 int stkg_heat_destroy(stkg_heat* plan);

@@ -32,6 +32,8 @@ class HeatDesc(C.Structure):
         ("a_diag", c_double_p * 3),
         ("a_off", c_double_p * 3),
         ("time_chunk", C.c_int64),
+        ("transform", C.c_int),
+        ("p1_h", C.c_double * 3),
     ]
 
 

@@ -1,0 +1,264 @@
+// Fast sine transform backend for the uniform-P1 eigenbasis.
+//
+// For P1 elements on a uniform grid with n interior nodes (N = n + 1), the generalized
+// eigenbasis of (A_h, M_h) is X = S diag(mu^-1/2) with S[i,k] = sqrt(2/N) sin(pi i k / N)
+// the orthonormal DST-I matrix (S = S^T = S^-1) and mu_k = (h/3)(2 + cos(pi k / N)) the
+// eigenvalues of M_h.  The dense transforms X^T F and X Y of solve_projected_heat_with
+// (stk/sylvester.hpp:126,141) are therefore a DST-I along each axis plus a diagonal
+// scaling; the scaling mu^-1 (both directions) is folded into the modal recurrence.
+//
+// DST-I of two real vectors a, b (length N-1) at once: with c_j = a_j + i b_j (j = 1..N-1,
+// zero elsewhere) and W = FFT_{2N}(c),
+//     DST(a)_k = -(Im W_k - Im W_{2N-k}) / 2,   DST(b)_k = (Re W_k - Re W_{2N-k}) / 2.
+// The length-2N complex FFT runs in shared memory as a Stockham auto-sort FFT with radix-8
+// stages (radix-4/2 last), twiddles from a table of 2N-th roots of unity built on the host
+// with exact integer argument reduction.  Cost: 5 (2N) log2(2N) flop per pair, i.e. about
+// 5 log2(2N) flop per element -- O(log n) instead of the 2n of a dense transform.
+#pragma once
+
+#include "common.cuh"
+#include "gemm_f64.cuh"  // cp_async8 / commit / wait
+
+namespace stkg {
+
+// Complex helpers (double2 = (re, im))
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ double2 mul_neg_i(double2 a) { return make_double2(a.y, -a.x); }  // -i a
+
+// Forward DFT of size 4: Y_q = sum_r c_r exp(-2 pi i r q / 4)
+__device__ __forceinline__ void dft4(double2& c0, double2& c1, double2& c2, double2& c3) {
+  const double2 s02 = cadd(c0, c2), d02 = csub(c0, c2);
+  const double2 s13 = cadd(c1, c3), d13 = mul_neg_i(csub(c1, c3));
+  c0 = cadd(s02, s13);
+  c2 = csub(s02, s13);
+  c1 = cadd(d02, d13);
+  c3 = csub(d02, d13);
+}
+
+// Forward DFT of size 8 (decimation in frequency into two size-4 DFTs); output in
+// natural order in v[0..7].
+__device__ __forceinline__ void dft8(double2 (&v)[8]) {
+  constexpr double r2 = 0.70710678118654752440;  // 1/sqrt(2)
+  double2 a[4], b[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    a[r] = cadd(v[r], v[r + 4]);
+    b[r] = csub(v[r], v[r + 4]);
+  }
+  // b_r *= w^r, w = exp(-2 pi i / 8)
+  b[1] = make_double2((b[1].x + b[1].y) * r2, (b[1].y - b[1].x) * r2);
+  b[2] = mul_neg_i(b[2]);
+  b[3] = make_double2((b[3].y - b[3].x) * r2, -(b[3].x + b[3].y) * r2);
+  dft4(a[0], a[1], a[2], a[3]);
+  dft4(b[0], b[1], b[2], b[3]);
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    v[2 * p] = a[p];
+    v[2 * p + 1] = b[p];
+  }
+}
+
+template <int R>
+__device__ __forceinline__ void dft_radix(double2 (&v)[R]);
+template <>
+__device__ __forceinline__ void dft_radix<8>(double2 (&v)[8]) { dft8(v); }
+template <>
+__device__ __forceinline__ void dft_radix<4>(double2 (&v)[4]) { dft4(v[0], v[1], v[2], v[3]); }
+template <>
+__device__ __forceinline__ void dft_radix<2>(double2 (&v)[2]) {
+  const double2 t = v[0];
+  v[0] = cadd(t, v[1]);
+  v[1] = csub(t, v[1]);
+}
+
+constexpr int ilog2(int x) { return x <= 1 ? 0 : 1 + ilog2(x / 2); }
+
+// Shared-memory index with one pad slot per 8 complex values: the stride-8 (and stride-Ns)
+// Stockham writes then spread over all banks instead of hitting one 128-byte bank group.
+__host__ __device__ constexpr int pidx(int i) { return i + (i >> 3); }
+template <int L>
+constexpr int padded_len() { return L + L / 8; }
+
+// One Stockham stage of radix R over NFFT FFTs of length L stored back to back in buf.
+// Ns = product of the radices of the previous stages.  In place: every thread reads its
+// inputs, the block synchronises, then the outputs are written.
+template <int L, int NFFT, int R, int THREADS>
+__device__ __forceinline__ void stockham_stage(double2* buf, int Ns,
+                                              const double2* __restrict__ tw) {
+  constexpr int kBut = L / R;                 // butterflies per FFT
+  constexpr int total = NFFT * kBut;
+  constexpr int kMaxPer = (total + THREADS - 1) / THREADS;
+  double2 v[kMaxPer][R];
+  int base_out[kMaxPer];
+  int cnt = 0;
+#pragma unroll
+  for (int u = 0; u < kMaxPer; ++u) {
+    const int t = threadIdx.x + u * THREADS;
+    if (t < total) {
+      const int f = t / kBut, j = t % kBut;
+      double2* x = buf + f * padded_len<L>();
+      const int k = j % Ns;
+      const int stride = L / (Ns * R);  // twiddle index step
+      // one table load per butterfly: w = exp(-2 pi i k / (Ns R)); w^r by multiplication
+      // (a few ulps, far below the 1e-10 parity bar) instead of R-1 L1 loads
+      double2 wr = make_double2(1.0, 0.0);
+      const double2 w = k > 0 ? __ldg(tw + k * stride) : make_double2(1.0, 0.0);
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        double2 val = x[pidx(j + r * kBut)];
+        if (r > 0) {
+          wr = r == 1 ? w : cmul(wr, w);
+          if (k > 0) val = cmul(val, wr);
+        }
+        v[u][r] = val;
+      }
+      base_out[u] = f * padded_len<L>() + (j / Ns) * Ns * R + k;  // unpadded within the FFT
+      ++cnt;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < kMaxPer; ++u) {
+    if (u < cnt) {
+      dft_radix<R>(v[u]);
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int fo = base_out[u] / padded_len<L>(), io = base_out[u] % padded_len<L>() + r * Ns;
+        buf[fo * padded_len<L>() + pidx(io)] = v[u][r];
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// Full forward FFT of length L = 2^k: floor(k/3) radix-8 stages, then one radix-4 or -2.
+template <int L, int NFFT, int THREADS>
+__device__ __forceinline__ void fft_inplace(double2* buf, const double2* tw) {
+  constexpr int kStages8 = ilog2(L) / 3;
+  constexpr int kTail = L >> (3 * kStages8);
+  int Ns = 1;
+#pragma unroll
+  for (int st = 0; st < kStages8; ++st) {
+    stockham_stage<L, NFFT, 8, THREADS>(buf, Ns, tw);
+    Ns *= 8;
+  }
+  if constexpr (kTail == 2) stockham_stage<L, NFFT, 2, THREADS>(buf, Ns, tw);
+  if constexpr (kTail == 4) stockham_stage<L, NFFT, 4, THREADS>(buf, Ns, tw);
+}
+
+// Orthonormal DST-I along one axis of data viewed as [outer][n][inner] (element j of
+// vector (o, i) at (o * n + j) * inner + i); vectors = outer * inner.  `scale` multiplies
+// the result (sqrt(2/N)).  dst may alias src (a work item is read completely before any of
+// it is written, and items are disjoint).
+//
+// Persistent CTAs walk over work items of VPI neighbouring vectors (VPI/2 complex FFTs).
+// The raw vectors of item i+1 are prefetched with cp.async into a second staging buffer
+// while item i is packed, transformed and stored, so HBM latency overlaps the FFT.
+template <int L>
+struct DstLaunch {
+  static constexpr int kThreads = 256;
+  static constexpr int kVpiFast = 2;   // contiguous axis: one complex FFT per item
+  static constexpr int kVpiStrided = 2;  // strided axes: 2 neighbours (16-byte rows)
+  static constexpr int kCtasPerSm = 2;
+  template <int VPI>
+  static constexpr size_t smem() {
+    return size_t(VPI / 2) * padded_len<L>() * sizeof(double2) +  // FFT buffers
+           size_t(2) * VPI * (L / 2) * sizeof(double);              // 2 staging buffers
+  }
+};
+
+template <int L, int VPI>
+__global__ void __launch_bounds__(256, 2) dst_axis_kernel(const double* src, double* dst,
+                                                          int64_t n, int64_t inner,
+                                                          int64_t nvec,
+                                                          const double2* __restrict__ tw,
+                                                          double scale) {
+  constexpr int kThreads = 256;
+  constexpr int LP = padded_len<L>();
+  constexpr int NF = VPI / 2;   // complex FFTs per item
+  constexpr int SL = L / 2;     // staging stride per vector (>= n)
+  extern __shared__ __align__(16) double2 cbuf[];
+  double* stage = reinterpret_cast<double*>(cbuf + NF * LP);  // [2][VPI][SL]
+  __shared__ int64_t vbase[2][VPI];
+  const int nn = static_cast<int>(n);
+  const int64_t nitems = (nvec + VPI - 1) / VPI;
+
+  auto item_bases = [&](int buf, int64_t item) {
+    if (threadIdx.x < VPI) {
+      const int64_t gv = item * VPI + threadIdx.x;
+      vbase[buf][threadIdx.x] =
+          (item < nitems && gv < nvec) ? (gv / inner) * n * inner + gv % inner : -1;
+    }
+  };
+  // cp.async the raw vectors of `item` into staging buffer `buf` (vbase[buf] must be set)
+  auto prefetch = [&](int buf, int64_t item) {
+    double* st = stage + buf * VPI * SL;
+    if (inner == 1) {
+#pragma unroll
+      for (int v = 0; v < VPI; ++v) {
+        const int64_t b = vbase[buf][v];
+        for (int e = threadIdx.x; e < nn; e += kThreads)
+          cp_async8(st + v * SL + e, b >= 0 ? src + b + e : src, b >= 0);
+      }
+    } else {
+      for (int e = threadIdx.x; e < VPI * nn; e += kThreads) {
+        const int v = e % VPI, j = e / VPI;
+        const int64_t b = vbase[buf][v];
+        cp_async8(st + v * SL + j, b >= 0 ? src + b + int64_t(j) * inner : src, b >= 0);
+      }
+    }
+  };
+
+  int64_t item = blockIdx.x;
+  item_bases(0, item);
+  __syncthreads();
+  prefetch(0, item);
+  cp_async_commit();
+  const double hs = 0.5 * scale;
+  for (int cur = 0; item < nitems; item += gridDim.x, cur ^= 1) {
+    const int64_t next = item + gridDim.x;
+    __syncthreads();  // previous item fully stored: vbase[cur^1] and cbuf are free
+    item_bases(cur ^ 1, next);
+    __syncthreads();  // vbase[cur^1] visible
+    prefetch(cur ^ 1, next);
+    cp_async_commit();
+    cp_async_wait<1>();  // this item's vectors have landed (own copies)
+    __syncthreads();     // ... everyone's copies
+    // pack: FFT f gets vector 2f as real and 2f+1 as imaginary part at j = 1..n
+    const double* st = stage + cur * VPI * SL;
+    for (int e = threadIdx.x; e < NF * L; e += kThreads) {
+      const int f = e / L, j = e % L;
+      double2 c = make_double2(0.0, 0.0);
+      if (j >= 1 && j <= nn) c = make_double2(st[(2 * f) * SL + j - 1], st[(2 * f + 1) * SL + j - 1]);
+      cbuf[f * LP + pidx(j)] = c;
+    }
+    __syncthreads();
+    fft_inplace<L, NF, kThreads>(cbuf, tw);
+    // post-process and store: output k = e + 1 from W_k and W_{L-k}
+    auto result = [&](int v, int k) -> double {
+      const double2 wk = cbuf[(v >> 1) * LP + pidx(k)], wm = cbuf[(v >> 1) * LP + pidx(L - k)];
+      return (v & 1) ? hs * (wk.x - wm.x) : -hs * (wk.y - wm.y);
+    };
+    if (inner == 1) {
+#pragma unroll
+      for (int v = 0; v < VPI; ++v) {
+        const int64_t b = vbase[cur][v];
+        if (b < 0) continue;
+        for (int e = threadIdx.x; e < nn; e += kThreads) __stcs(dst + b + e, result(v, e + 1));
+      }
+    } else {
+      for (int e = threadIdx.x; e < VPI * nn; e += kThreads) {
+        const int v = e % VPI, j = e / VPI;
+        const int64_t b = vbase[cur][v];
+        if (b >= 0) __stcs(dst + b + int64_t(j) * inner, result(v, j + 1));
+      }
+    }
+  }
+  cp_async_wait<0>();
+}
+
+}  // namespace stkg

@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "dst.cuh"
 #include "gemm_f64.cuh"
 
 using namespace stkg;
@@ -26,6 +27,9 @@ struct stkg_heat {
   int64_t nx = 0;  // spatial unknowns
   cudaStream_t stream = nullptr;
   DevBuf X[3], XT[3], lam[3];
+  int transform = STKG_TRANSFORM_DENSE;
+  DevBuf inv_mu[3];  // P1_DST: 1/mu_k per axis (folded into the recurrence)
+  DevBuf twiddle[3];  // P1_DST: exp(-2 pi i m / 2N) per axis, as double2
   DevBuf d_diag, d_sup, c_diag, c_sup;
   bool has_operator = false;
   DevBuf m_diag[3], m_off[3], a_diag[3], a_off[3];
@@ -70,14 +74,31 @@ struct ModeLambda {
   }
 };
 
+// Optional per-mode output weight w_i = prod_a w_a[i_a] (P1_DST backend: 1/(mu_x mu_y ..)).
+struct ModeWeight {
+  const double* w0;
+  const double* w1;
+  const double* w2;
+  int64_t n1, n2;
+  int ndim;
+  __device__ __forceinline__ double operator()(int64_t i) const {
+    if (!w0) return 1.0;
+    if (ndim == 1) return w0[i];
+    if (ndim == 2) return w0[i / n1] * w1[i % n1];
+    const int64_t iz = i % n2, r = i / n2;
+    return w0[r / n1] * w1[r % n1] * w2[iz];
+  }
+};
+
 __global__ void __launch_bounds__(256) heat_scan_kernel(
-    double* __restrict__ Y, int64_t nx, int64_t ntc, int64_t l0, ModeLambda lam,
+    double* __restrict__ Y, int64_t nx, int64_t ntc, int64_t l0, ModeLambda lam, ModeWeight wgt,
     const double* __restrict__ d_diag, const double* __restrict__ d_sup,
     const double* __restrict__ c_diag, const double* __restrict__ c_sup,
     double* __restrict__ carry) {
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= nx) return;
   const double li = lam(i);
+  const double wi = wgt(i);  // 1 in the dense backend
   double y = l0 > 0 ? carry[i] : 0.0;
   double* col = Y + i;
   constexpr int U = 8;
@@ -93,7 +114,7 @@ __global__ void __launch_bounds__(256) heat_scan_kernel(
       double rhs = g[u];
       if (l > 0) rhs -= (d_sup[l - 1] + li * c_sup[l - 1]) * y;
       y = rhs / piv;
-      __stcs(col + (j + u) * nx, y);
+      __stcs(col + (j + u) * nx, wi * y);
     }
   }
   for (; j < ntc; ++j) {
@@ -102,7 +123,7 @@ __global__ void __launch_bounds__(256) heat_scan_kernel(
     double rhs = col[j * nx];
     if (l > 0) rhs -= (d_sup[l - 1] + li * c_sup[l - 1]) * y;
     y = rhs / piv;
-    col[j * nx] = y;
+    col[j * nx] = wi * y;
   }
   carry[i] = y;
 }
@@ -113,12 +134,13 @@ __global__ void __launch_bounds__(256) heat_scan_kernel(
 constexpr int kMaxFactorRank = 16;
 __global__ void __launch_bounds__(256) heat_scan_factored_kernel(
     const double* __restrict__ Lt, const double* __restrict__ R, int rank, double* __restrict__ Y,
-    int64_t nx, int64_t nt, ModeLambda lam, const double* __restrict__ d_diag,
+    int64_t nx, int64_t nt, ModeLambda lam, ModeWeight wgt, const double* __restrict__ d_diag,
     const double* __restrict__ d_sup, const double* __restrict__ c_diag,
     const double* __restrict__ c_sup) {
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= nx) return;
   const double li = lam(i);
+  const double wi = wgt(i);
   double lt[kMaxFactorRank];
 #pragma unroll
   for (int r = 0; r < kMaxFactorRank; ++r) lt[r] = r < rank ? Lt[int64_t(r) * nx + i] : 0.0;
@@ -131,7 +153,7 @@ __global__ void __launch_bounds__(256) heat_scan_factored_kernel(
     const double piv = d_diag[l] + li * c_diag[l];
     if (l > 0) g -= (d_sup[l - 1] + li * c_sup[l - 1]) * y;
     y = g / piv;
-    __stcs(Y + l * nx + i, y);
+    __stcs(Y + l * nx + i, wi * y);
   }
 }
 
@@ -369,6 +391,57 @@ ModeLambda mode_lambda(const stkg_heat& h) {
                     h.ndim > 2 ? h.lam[2].p : nullptr, h.n[1], h.n[2], h.ndim};
 }
 
+ModeWeight mode_weight(const stkg_heat& h) {
+  if (h.transform != STKG_TRANSFORM_P1_DST) return ModeWeight{nullptr, nullptr, nullptr, 1, 1, 1};
+  return ModeWeight{h.inv_mu[0].p, h.ndim > 1 ? h.inv_mu[1].p : nullptr,
+                    h.ndim > 2 ? h.inv_mu[2].p : nullptr, h.n[1], h.n[2], h.ndim};
+}
+
+template <int L, int VPI>
+void launch_dst_vpi(const stkg_heat& h, int a, const double* src, double* dst, int64_t inner,
+                    int64_t outer) {
+  using C = DstLaunch<L>;
+  constexpr size_t smem = C::template smem<VPI>();
+  static const bool configured = [] {
+    STKG_CUDA_CHECK(cudaFuncSetAttribute(dst_axis_kernel<L, VPI>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem)));
+    return true;
+  }();
+  (void)configured;
+  const int64_t nvec = outer * inner;
+  const int64_t items = ceil_div(nvec, VPI);
+  const int64_t blocks = std::min<int64_t>(items, int64_t(148) * C::kCtasPerSm);
+  const double scale = std::sqrt(2.0 / static_cast<double>(h.n[a] + 1));
+  dst_axis_kernel<L, VPI><<<static_cast<unsigned>(blocks), C::kThreads, smem, h.stream>>>(
+      src, dst, h.n[a], inner, nvec, reinterpret_cast<const double2*>(h.twiddle[a].p), scale);
+  STKG_CUDA_CHECK(cudaGetLastError());
+}
+
+template <int L>
+void launch_dst(const stkg_heat& h, int a, const double* src, double* dst, int64_t inner,
+                int64_t outer) {
+  if (inner == 1)
+    launch_dst_vpi<L, DstLaunch<L>::kVpiFast>(h, a, src, dst, inner, outer);
+  else
+    launch_dst_vpi<L, DstLaunch<L>::kVpiStrided>(h, a, src, dst, inner, outer);
+}
+
+void dst_pass(const stkg_heat& h, int a, const double* src, double* dst, int64_t inner,
+              int64_t outer) {
+  switch (2 * (h.n[a] + 1)) {
+    case 32: return launch_dst<32>(h, a, src, dst, inner, outer);
+    case 64: return launch_dst<64>(h, a, src, dst, inner, outer);
+    case 128: return launch_dst<128>(h, a, src, dst, inner, outer);
+    case 256: return launch_dst<256>(h, a, src, dst, inner, outer);
+    case 512: return launch_dst<512>(h, a, src, dst, inner, outer);
+    case 1024: return launch_dst<1024>(h, a, src, dst, inner, outer);
+    case 2048: return launch_dst<2048>(h, a, src, dst, inner, outer);
+    case 4096: return launch_dst<4096>(h, a, src, dst, inner, outer);
+    default: throw Error(STKG_ARGUMENT, "P1_DST transform: n + 1 must be a power of two in [16, 2048]");
+  }
+}
+
 // One axis transform over a block of ntc time slices.  Axis a with inner extent
 // I = prod_{b>a} n_b: the fastest axis (I == 1) is a left product  Op * data(n_a x rest);
 // every other axis is a batched right product  data_b(I x n_a) * Op'  (SURVEY Appendix A:
@@ -399,6 +472,11 @@ void axis_pass(stkg_heat& h, int a, bool forward, const double* src, double* dst
   for (int b = a + 1; b < h.ndim; ++b) inner *= h.n[b];
   for (int b = 0; b < a; ++b) outer *= h.n[b];
   const int64_t na = h.n[a];
+  if (h.transform == STKG_TRANSFORM_P1_DST) {  // X = S diag(mu^-1/2): S is its own inverse
+    ProfScope ps(h, 0);
+    dst_pass(h, a, src, dst, inner, outer);
+    return;
+  }
   GemmProblem p;
   if (inner == 1) {
     p.M = na;
@@ -445,8 +523,8 @@ void run_chunk(stkg_heat& h, const double* F, double* U, double* S, int64_t l0, 
     const int64_t blocks = ceil_div(h.nx, 256);
     ProfScope ps(h, 1);
     heat_scan_kernel<<<static_cast<unsigned>(blocks), 256, 0, h.stream>>>(
-        Y, h.nx, ntc, l0, mode_lambda(h), h.d_diag.p, h.d_sup.p, h.c_diag.p, h.c_sup.p,
-        h.carry.p);
+        Y, h.nx, ntc, l0, mode_lambda(h), mode_weight(h), h.d_diag.p, h.d_sup.p, h.c_diag.p,
+        h.c_sup.p, h.carry.p);
     STKG_CUDA_CHECK(cudaGetLastError());
   }
   for (int a = 0; a < d; ++a) {  // inverse, slowest axis first
@@ -508,6 +586,20 @@ void dispatch_apply(stkg_heat& h, const double* U, const double* F, double* out)
   else launch_apply<3, RES>(h, U, F, out);
 }
 
+// sin(pi r / N) and cos(pi r / N) for integers r, N with exact range reduction
+double sinpi_ratio_h(int64_t r, int64_t N) {
+  int64_t m = r % (2 * N);
+  if (m < 0) m += 2 * N;
+  double sign = 1.0;
+  if (m >= N) {
+    m -= N;
+    sign = -1.0;
+  }
+  if (2 * m > N) m = N - m;
+  return sign * std::sin(M_PI * static_cast<double>(m) / static_cast<double>(N));
+}
+double cospi_ratio(int64_t r, int64_t N) { return sinpi_ratio_h(2 * r + N, 2 * N); }
+
 std::vector<double> transpose(const double* X, int64_t n) {
   std::vector<double> t(static_cast<size_t>(n * n));
   for (int64_t j = 0; j < n; ++j)
@@ -542,10 +634,20 @@ int stkg_heat_create(stkg_heat** out, const stkg_heat_desc* desc, void* cuda_str
     h->ndim = desc->ndim;
     h->nt = desc->nt;
     h->nx = 1;
+    h->transform = desc->transform;
+    STKG_REQUIRE(h->transform == STKG_TRANSFORM_DENSE || h->transform == STKG_TRANSFORM_P1_DST,
+                 STKG_ARGUMENT, "stkg_heat_create: unknown transform");
+    const bool dst_mode = h->transform == STKG_TRANSFORM_P1_DST;
     for (int a = 0; a < h->ndim; ++a) {
       STKG_REQUIRE(desc->n[a] >= 1, STKG_ARGUMENT, "stkg_heat_create: n must be >= 1");
-      STKG_REQUIRE(desc->X[a] && desc->lambdas[a], STKG_ARGUMENT,
+      STKG_REQUIRE((dst_mode || desc->X[a]) && desc->lambdas[a], STKG_ARGUMENT,
                    "stkg_heat_create: missing EigPair for an axis");
+      if (dst_mode) {
+        const int64_t N = desc->n[a] + 1;
+        STKG_REQUIRE(N >= 16 && N <= 2048 && (N & (N - 1)) == 0, STKG_ARGUMENT,
+                     "P1_DST transform: n + 1 must be a power of two in [16, 2048]");
+        STKG_REQUIRE(desc->p1_h[a] > 0.0, STKG_ARGUMENT, "P1_DST transform: p1_h must be > 0");
+      }
       h->n[a] = desc->n[a];
       h->nx *= desc->n[a];
     }
@@ -555,13 +657,30 @@ int stkg_heat_create(stkg_heat** out, const stkg_heat_desc* desc, void* cuda_str
     cudaStream_t s = h->stream;
     for (int a = 0; a < h->ndim; ++a) {
       const int64_t na = h->n[a];
-      h->X[a].alloc(na * na);
-      h->X[a].upload(desc->X[a], na * na, s);
-      auto t = transpose(desc->X[a], na);
-      h->XT[a].alloc(na * na);
-      h->XT[a].upload(t.data(), na * na, s);
       h->lam[a].alloc(na);
       h->lam[a].upload(desc->lambdas[a], na, s);
+      if (dst_mode) {
+        // 1/mu_k with mu_k = (h/3)(2 + cos(pi k/N)), k = 1..n (the M_h eigenvalues), and the
+        // 2N-th roots of unity, both with exact integer argument reduction.
+        const int64_t N = na + 1, L = 2 * N;
+        std::vector<double> w(na), tw(2 * L);
+        const double hh = desc->p1_h[a];
+        for (int64_t k = 1; k <= na; ++k) w[k - 1] = 1.0 / ((hh / 3.0) * (2.0 + cospi_ratio(k, N)));
+        for (int64_t m = 0; m < L; ++m) {
+          tw[2 * m] = cospi_ratio(2 * m, L);        // cos(2 pi m / L)
+          tw[2 * m + 1] = -sinpi_ratio_h(2 * m, L);  // -sin(2 pi m / L)
+        }
+        h->inv_mu[a].alloc(na);
+        h->inv_mu[a].upload(w.data(), na, s);
+        h->twiddle[a].alloc(2 * L);
+        h->twiddle[a].upload(tw.data(), 2 * L, s);
+      } else {
+        h->X[a].alloc(na * na);
+        h->X[a].upload(desc->X[a], na * na, s);
+        auto t = transpose(desc->X[a], na);
+        h->XT[a].alloc(na * na);
+        h->XT[a].upload(t.data(), na * na, s);
+      }
       STKG_CUDA_CHECK(cudaStreamSynchronize(s));  // host temporaries die here
     }
     const int64_t nt = h->nt;
@@ -659,7 +778,8 @@ int64_t stkg_heat_workspace_bytes(const stkg_heat* h) {
   const DevBuf* bufs[] = {&h->scratch, &h->lfac, &h->carry, &h->partials, &h->pf[0], &h->pf[1],
                           &h->pu[0],   &h->pu[1], &h->ps};
   for (auto* x : bufs) b += static_cast<int64_t>(x->n) * 8;
-  for (int a = 0; a < h->ndim; ++a) b += static_cast<int64_t>(2 * h->X[a].n + h->lam[a].n) * 8;
+  for (int a = 0; a < h->ndim; ++a)
+    b += static_cast<int64_t>(2 * h->X[a].n + h->lam[a].n + h->inv_mu[a].n + h->twiddle[a].n) * 8;
   return b;
 }
 
@@ -696,7 +816,7 @@ int stkg_heat_solve_factored(stkg_heat* h, int64_t rank, const double* L, const 
     {
       ProfScope ps(*h, 1);
       heat_scan_factored_kernel<<<static_cast<unsigned>(ceil_div(h->nx, 256)), 256, 0, h->stream>>>(
-          src, R, static_cast<int>(rank), Y, h->nx, h->nt, mode_lambda(*h), h->d_diag.p,
+          src, R, static_cast<int>(rank), Y, h->nx, h->nt, mode_lambda(*h), mode_weight(*h), h->d_diag.p,
           h->d_sup.p, h->c_diag.p, h->c_sup.p);
       STKG_CUDA_CHECK(cudaGetLastError());
     }

@@ -65,7 +65,11 @@ class HeatPlan:
 
     def __init__(self, eig: TensorEigPair | EigPair, d: Bidiagonal, c: Bidiagonal,
                  m_axes: Sequence[Tridiagonal] | None = None,
-                 a_axes: Sequence[Tridiagonal] | None = None, stream=None, time_chunk: int = 0):
+                 a_axes: Sequence[Tridiagonal] | None = None, stream=None, time_chunk: int = 0,
+                 transform: str = "dense", p1_h: Sequence[float] | None = None):
+        """transform="dense": the per-axis X are applied as DMMA GEMMs (any EigPair).
+        transform="dst": the axes carry the closed-form uniform-P1 eigenbasis of a grid of
+        spacing p1_h[a] (X is not read) and are applied as FP64 fast sine transforms."""
         if isinstance(eig, EigPair):
             eig = TensorEigPair([eig])
         axes = list(eig.axes)
@@ -92,12 +96,22 @@ class HeatPlan:
         desc.d_diag, desc.c_diag = arr(d.diag), arr(c.diag)
         desc.d_sup = arr(d.sup if d.sup.size else np.zeros(1))
         desc.c_sup = arr(c.sup if c.sup.size else np.zeros(1))
+        if transform not in ("dense", "dst"):
+            raise ArgumentError("HeatPlan: transform must be 'dense' or 'dst'")
+        desc.transform = 1 if transform == "dst" else 0
+        if transform == "dst":
+            if p1_h is None or len(p1_h) != ndim:
+                raise ArgumentError("HeatPlan: transform='dst' needs p1_h per axis")
+            for i in range(ndim):
+                desc.p1_h[i] = float(p1_h[i])
+        self.transform = transform
         for i, e in enumerate(axes):
-            X = np.asfortranarray(e.X, dtype=np.float64)
-            if X.shape != (self.n[i], self.n[i]):
-                raise ArgumentError("solve_projected_heat: EigPair X shape mismatch")
-            keep.append(X)
-            desc.X[i] = _np_ptr(X)
+            if transform == "dense":
+                X = np.asfortranarray(e.X, dtype=np.float64)
+                if X.shape != (self.n[i], self.n[i]):
+                    raise ArgumentError("solve_projected_heat: EigPair X shape mismatch")
+                keep.append(X)
+                desc.X[i] = _np_ptr(X)
             desc.lambdas[i] = arr(e.lambdas)
         if m_axes is not None and a_axes is not None:
             for i in range(ndim):
@@ -110,6 +124,21 @@ class HeatPlan:
         h = C.c_void_p()
         check(lib.stkg_heat_create(C.byref(h), C.byref(desc), self._stream))
         self._h = h
+
+    @classmethod
+    def p1_uniform(cls, ndim: int, n: int, nt: int, T: float = 1.0, a: float = 0.0,
+                   b: float = 1.0, transform: str = "dst", with_operator: bool = True,
+                   stream=None, time_chunk: int = 0) -> "HeatPlan":
+        """Heat plan of the tensor P1/Q1 discretisation (fem1d_matrices per axis on (a,b) with
+        n interior nodes, heat_time_matrices with nt steps on (0,T))."""
+        from .assembly import SpaceGrid1D, TimeGrid, fem1d_matrices, heat_time_matrices, p1_eigpair
+        g = SpaceGrid1D(a, b, n)
+        M, A = fem1d_matrices(g)
+        D, Cm = heat_time_matrices(TimeGrid(nt, T))
+        e = p1_eigpair(g)
+        ops = ([M] * ndim, [A] * ndim) if with_operator else (None, None)
+        return cls(TensorEigPair([e] * ndim), D, Cm, ops[0], ops[1], stream=stream,
+                   time_chunk=time_chunk, transform=transform, p1_h=[g.fem_h] * ndim)
 
     def close(self):
         if getattr(self, "_h", None):
