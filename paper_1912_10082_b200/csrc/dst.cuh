@@ -19,6 +19,13 @@
 #include "common.cuh"
 #include "gemm_f64.cuh"  // cp_async8 / commit / wait
 
+#ifndef STKG_DST_THREADS
+#define STKG_DST_THREADS 256
+#endif
+#ifndef STKG_DST_CTAS
+#define STKG_DST_CTAS 2
+#endif
+
 namespace stkg {
 
 // Complex helpers (double2 = (re, im))
@@ -135,6 +142,52 @@ __device__ __forceinline__ void stockham_stage(double2* buf, int Ns,
   __syncthreads();
 }
 
+// First radix-8 Stockham stage (Ns = 1, no twiddles) fused with the packing of two real
+// vectors a, b (length n = L/2 - 1, in shared staging arrays) into c_m = a_{m-1} + i b_{m-1}:
+// inputs m = j + r L/8 with r >= 4 are the zero padding (m >= L/2), so only 4 of the 8
+// butterfly inputs are loaded and the first radix-2 layer of the DFT-8 disappears.
+template <int L, int THREADS>
+__device__ __forceinline__ void stockham_first_stage_packed(double2* buf, const double* sa,
+                                                           const double* sb, int n) {
+  constexpr int kBut = L / 8;
+  constexpr double r2 = 0.70710678118654752440;
+  for (int j = threadIdx.x; j < kBut; j += THREADS) {
+    double2 a[4], b[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int m = j + r * kBut;
+      a[r] = (m >= 1 && m <= n) ? make_double2(sa[m - 1], sb[m - 1]) : make_double2(0.0, 0.0);
+      b[r] = a[r];
+    }
+    b[1] = make_double2((b[1].x + b[1].y) * r2, (b[1].y - b[1].x) * r2);
+    b[2] = mul_neg_i(b[2]);
+    b[3] = make_double2((b[3].y - b[3].x) * r2, -(b[3].x + b[3].y) * r2);
+    dft4(a[0], a[1], a[2], a[3]);
+    dft4(b[0], b[1], b[2], b[3]);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      buf[pidx(j * 8 + 2 * q)] = a[q];
+      buf[pidx(j * 8 + 2 * q + 1)] = b[q];
+    }
+  }
+  __syncthreads();
+}
+
+// Remaining stages of the length-L FFT after the fused first radix-8 stage.
+template <int L, int NFFT, int THREADS>
+__device__ __forceinline__ void fft_after_first_stage(double2* buf, const double2* tw) {
+  constexpr int kStages8 = ilog2(L) / 3;
+  constexpr int kTail = L >> (3 * kStages8);
+  int Ns = 8;
+#pragma unroll
+  for (int st = 1; st < kStages8; ++st) {
+    stockham_stage<L, NFFT, 8, THREADS>(buf, Ns, tw);
+    Ns *= 8;
+  }
+  if constexpr (kTail == 2) stockham_stage<L, NFFT, 2, THREADS>(buf, Ns, tw);
+  if constexpr (kTail == 4) stockham_stage<L, NFFT, 4, THREADS>(buf, Ns, tw);
+}
+
 // Full forward FFT of length L = 2^k: floor(k/3) radix-8 stages, then one radix-4 or -2.
 template <int L, int NFFT, int THREADS>
 __device__ __forceinline__ void fft_inplace(double2* buf, const double2* tw) {
@@ -160,10 +213,10 @@ __device__ __forceinline__ void fft_inplace(double2* buf, const double2* tw) {
 // while item i is packed, transformed and stored, so HBM latency overlaps the FFT.
 template <int L>
 struct DstLaunch {
-  static constexpr int kThreads = 256;
+  static constexpr int kThreads = STKG_DST_THREADS;
   static constexpr int kVpiFast = 2;   // contiguous axis: one complex FFT per item
   static constexpr int kVpiStrided = 2;  // strided axes: 2 neighbours (16-byte rows)
-  static constexpr int kCtasPerSm = 2;
+  static constexpr int kCtasPerSm = STKG_DST_CTAS;
   template <int VPI>
   static constexpr size_t smem() {
     return size_t(VPI / 2) * padded_len<L>() * sizeof(double2) +  // FFT buffers
@@ -172,12 +225,12 @@ struct DstLaunch {
 };
 
 template <int L, int VPI>
-__global__ void __launch_bounds__(256, 2) dst_axis_kernel(const double* src, double* dst,
+__global__ void __launch_bounds__(STKG_DST_THREADS, STKG_DST_CTAS) dst_axis_kernel(const double* src, double* dst,
                                                           int64_t n, int64_t inner,
                                                           int64_t nvec,
                                                           const double2* __restrict__ tw,
                                                           double scale) {
-  constexpr int kThreads = 256;
+  constexpr int kThreads = STKG_DST_THREADS;
   constexpr int LP = padded_len<L>();
   constexpr int NF = VPI / 2;   // complex FFTs per item
   constexpr int SL = L / 2;     // staging stride per vector (>= n)
@@ -228,34 +281,19 @@ __global__ void __launch_bounds__(256, 2) dst_axis_kernel(const double* src, dou
     cp_async_commit();
     cp_async_wait<1>();  // this item's vectors have landed (own copies)
     __syncthreads();     // ... everyone's copies
-    // pack: FFT f gets vector 2f as real and 2f+1 as imaginary part at j = 1..n
+    // packing fused into the first FFT stage (vector 0 -> real, vector 1 -> imaginary)
+    static_assert(VPI == 2, "one complex FFT per work item");
     const double* st = stage + cur * VPI * SL;
-    for (int e = threadIdx.x; e < NF * L; e += kThreads) {
-      const int f = e / L, j = e % L;
-      double2 c = make_double2(0.0, 0.0);
-      if (j >= 1 && j <= nn) c = make_double2(st[(2 * f) * SL + j - 1], st[(2 * f + 1) * SL + j - 1]);
-      cbuf[f * LP + pidx(j)] = c;
-    }
-    __syncthreads();
-    fft_inplace<L, NF, kThreads>(cbuf, tw);
-    // post-process and store: output k = e + 1 from W_k and W_{L-k}
-    auto result = [&](int v, int k) -> double {
-      const double2 wk = cbuf[(v >> 1) * LP + pidx(k)], wm = cbuf[(v >> 1) * LP + pidx(L - k)];
-      return (v & 1) ? hs * (wk.x - wm.x) : -hs * (wk.y - wm.y);
-    };
-    if (inner == 1) {
-#pragma unroll
-      for (int v = 0; v < VPI; ++v) {
-        const int64_t b = vbase[cur][v];
-        if (b < 0) continue;
-        for (int e = threadIdx.x; e < nn; e += kThreads) __stcs(dst + b + e, result(v, e + 1));
-      }
-    } else {
-      for (int e = threadIdx.x; e < VPI * nn; e += kThreads) {
-        const int v = e % VPI, j = e / VPI;
-        const int64_t b = vbase[cur][v];
-        if (b >= 0) __stcs(dst + b + int64_t(j) * inner, result(v, j + 1));
-      }
+    stockham_first_stage_packed<L, kThreads>(cbuf, st, st + SL, nn);
+    fft_after_first_stage<L, NF, kThreads>(cbuf, tw);
+    // post-process and store: both outputs k = e + 1 come from W_k and W_{L-k}
+    const int64_t b0 = vbase[cur][0], b1 = vbase[cur][1];
+    const int64_t step = inner;  // element stride (1 for the contiguous axis)
+    for (int e = threadIdx.x; e < nn; e += kThreads) {
+      const int k = e + 1;
+      const double2 wk = cbuf[pidx(k)], wm = cbuf[pidx(L - k)];
+      if (b0 >= 0) __stcs(dst + b0 + int64_t(e) * step, -hs * (wk.y - wm.y));
+      if (b1 >= 0) __stcs(dst + b1 + int64_t(e) * step, hs * (wk.x - wm.x));
     }
   }
   cp_async_wait<0>();
