@@ -188,6 +188,72 @@ __device__ __forceinline__ void fft_after_first_stage(double2* buf, const double
   if constexpr (kTail == 4) stockham_stage<L, NFFT, 4, THREADS>(buf, Ns, tw);
 }
 
+// Radix of the last stage of the length-L plan (8, 4 or 2).
+template <int L>
+constexpr int last_radix() {
+  return (L >> (3 * (ilog2(L) / 3))) == 1 ? 8 : (L >> (3 * (ilog2(L) / 3)));
+}
+
+// All stages after the fused first one except the last (used when the last stage is fused
+// with the DST post-processing).
+template <int L, int THREADS>
+__device__ __forceinline__ int fft_middle_stages(double2* buf, const double2* tw) {
+  constexpr int kStages8 = ilog2(L) / 3;
+  constexpr int kLast8 = last_radix<L>() == 8 ? 1 : 0;  // last stage is one of the radix-8s
+  int Ns = 8;
+#pragma unroll
+  for (int st = 1; st < kStages8 - kLast8; ++st) {
+    stockham_stage<L, 1, 8, THREADS>(buf, Ns, tw);
+    Ns *= 8;
+  }
+  return Ns;
+}
+
+// Last Stockham stage of radix 4 (Ns = L/4 butterflies, THREADS = L/8: two per thread)
+// fused with the DST-I post-processing.  Thread t takes butterflies j1 = t and
+// j2 = Ns - t (t = 0: j2 = Ns/2); the output pairs (W_k, W_{L-k}) then live in its own
+// registers: k = j1 + r Ns pairs with L - k = j2 + (3 - r) Ns.  Writes ya_k, yb_k
+// (k = 1..n) through `emit(k, ya, yb)`.
+template <int L, int THREADS, class Emit>
+__device__ __forceinline__ void last_radix4_stage_with_post(const double2* buf,
+                                                            const double2* __restrict__ tw,
+                                                            double hs, int n, Emit emit) {
+  constexpr int Ns = L / 4;
+  static_assert(THREADS * 2 == Ns, "two radix-4 butterflies per thread");
+  const int t = threadIdx.x;
+  const int jj[2] = {t, t == 0 ? Ns / 2 : Ns - t};
+  double2 W[2][4];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int j = jj[u], k = j;  // j % Ns == j
+    const double2 w = k > 0 ? __ldg(tw + k) : make_double2(1.0, 0.0);  // stride L/(Ns R) = 1
+    double2 wr = w;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      double2 val = buf[pidx(j + r * Ns)];
+      if (r > 0) {
+        if (r > 1) wr = cmul(wr, w);
+        if (k > 0) val = cmul(val, wr);
+      }
+      W[u][r] = val;
+    }
+    dft4(W[u][0], W[u][1], W[u][2], W[u][3]);  // outputs j + r Ns, r = 0..3
+  }
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int k = jj[u] + r * Ns;
+      if (k < 1 || k > n) continue;
+      // partner W_{L-k}: (t >= 1) other butterfly, index 3 - r; (t == 0) same butterfly
+      double2 pm;
+      if (t > 0) pm = W[1 - u][3 - r];
+      else pm = u == 0 ? W[0][(4 - r) & 3] : W[1][3 - r];
+      emit(k, -hs * (W[u][r].y - pm.y), hs * (W[u][r].x - pm.x));
+    }
+  }
+}
+
 // Full forward FFT of length L = 2^k: floor(k/3) radix-8 stages, then one radix-4 or -2.
 template <int L, int NFFT, int THREADS>
 __device__ __forceinline__ void fft_inplace(double2* buf, const double2* tw) {
@@ -208,95 +274,92 @@ __device__ __forceinline__ void fft_inplace(double2* buf, const double2* tw) {
 // the result (sqrt(2/N)).  dst may alias src (a work item is read completely before any of
 // it is written, and items are disjoint).
 //
-// Persistent CTAs walk over work items of VPI neighbouring vectors (VPI/2 complex FFTs).
-// The raw vectors of item i+1 are prefetched with cp.async into a second staging buffer
-// while item i is packed, transformed and stored, so HBM latency overlaps the FFT.
+// Persistent CTAs walk over work items of two neighbouring vectors (one complex FFT).  The
+// first FFT stage needs, per thread, the 4 nonzero inputs m = j + r L/8 (r < 4) of both
+// vectors: those 8 doubles of the NEXT item are loaded into registers while the current
+// item is transformed, so HBM latency hides behind the FFT without staging buffers.
 template <int L>
 struct DstLaunch {
-  static constexpr int kThreads = STKG_DST_THREADS;
-  static constexpr int kVpiFast = 2;   // contiguous axis: one complex FFT per item
-  static constexpr int kVpiStrided = 2;  // strided axes: 2 neighbours (16-byte rows)
-  static constexpr int kCtasPerSm = STKG_DST_CTAS;
-  template <int VPI>
-  static constexpr size_t smem() {
-    return size_t(VPI / 2) * padded_len<L>() * sizeof(double2) +  // FFT buffers
-           size_t(2) * VPI * (L / 2) * sizeof(double);              // 2 staging buffers
-  }
+  static constexpr int kThreads = L / 8;  // one radix-8 butterfly per thread per stage
+  static constexpr int kCtasPerSm = 2048 / kThreads < 8 ? 2048 / kThreads : 8;
+  static constexpr size_t kSmem = size_t(padded_len<L>()) * sizeof(double2);
 };
 
-template <int L, int VPI>
-__global__ void __launch_bounds__(STKG_DST_THREADS, STKG_DST_CTAS) dst_axis_kernel(const double* src, double* dst,
-                                                          int64_t n, int64_t inner,
-                                                          int64_t nvec,
-                                                          const double2* __restrict__ tw,
-                                                          double scale) {
-  constexpr int kThreads = STKG_DST_THREADS;
-  constexpr int LP = padded_len<L>();
-  constexpr int NF = VPI / 2;   // complex FFTs per item
-  constexpr int SL = L / 2;     // staging stride per vector (>= n)
+template <int L>
+__global__ void __launch_bounds__(L / 8, (L >= 2048 ? 2 : 3)) dst_axis_kernel(const double* __restrict__ src,
+                                                         double* dst, int64_t n, int64_t inner,
+                                                         int64_t nvec,
+                                                         const double2* __restrict__ tw,
+                                                         double scale) {
+  constexpr int kThreads = L / 8;
+  constexpr double r2 = 0.70710678118654752440;
   extern __shared__ __align__(16) double2 cbuf[];
-  double* stage = reinterpret_cast<double*>(cbuf + NF * LP);  // [2][VPI][SL]
-  __shared__ int64_t vbase[2][VPI];
   const int nn = static_cast<int>(n);
-  const int64_t nitems = (nvec + VPI - 1) / VPI;
+  const int64_t nitems = (nvec + 1) / 2;
+  const int j = threadIdx.x;
 
-  auto item_bases = [&](int buf, int64_t item) {
-    if (threadIdx.x < VPI) {
-      const int64_t gv = item * VPI + threadIdx.x;
-      vbase[buf][threadIdx.x] =
-          (item < nitems && gv < nvec) ? (gv / inner) * n * inner + gv % inner : -1;
+  // first-stage inputs of an item: a[r] = vector 0, b[r] = vector 1 at m = j + r L/8
+  auto fetch = [&](int64_t item, double (&a)[4], double (&b)[4], int64_t& b0, int64_t& b1) {
+    b0 = b1 = -1;
+    if (item < nitems) {
+      const int64_t g0 = 2 * item, g1 = g0 + 1;
+      b0 = (g0 / inner) * n * inner + g0 % inner;
+      if (g1 < nvec) b1 = (g1 / inner) * n * inner + g1 % inner;
     }
-  };
-  // cp.async the raw vectors of `item` into staging buffer `buf` (vbase[buf] must be set)
-  auto prefetch = [&](int buf, int64_t item) {
-    double* st = stage + buf * VPI * SL;
-    if (inner == 1) {
 #pragma unroll
-      for (int v = 0; v < VPI; ++v) {
-        const int64_t b = vbase[buf][v];
-        for (int e = threadIdx.x; e < nn; e += kThreads)
-          cp_async8(st + v * SL + e, b >= 0 ? src + b + e : src, b >= 0);
-      }
-    } else {
-      for (int e = threadIdx.x; e < VPI * nn; e += kThreads) {
-        const int v = e % VPI, j = e / VPI;
-        const int64_t b = vbase[buf][v];
-        cp_async8(st + v * SL + j, b >= 0 ? src + b + int64_t(j) * inner : src, b >= 0);
-      }
+    for (int r = 0; r < 4; ++r) {
+      const int m = j + r * kThreads;  // < L/2 = n + 1
+      const bool in = m >= 1;
+      const int64_t off = int64_t(m - 1) * inner;
+      a[r] = (in && b0 >= 0) ? __ldcs(src + b0 + off) : 0.0;
+      b[r] = (in && b1 >= 0) ? __ldcs(src + b1 + off) : 0.0;
     }
   };
 
+  double na[4], nb[4];
+  int64_t nb0, nb1;
   int64_t item = blockIdx.x;
-  item_bases(0, item);
-  __syncthreads();
-  prefetch(0, item);
-  cp_async_commit();
+  fetch(item, na, nb, nb0, nb1);
   const double hs = 0.5 * scale;
-  for (int cur = 0; item < nitems; item += gridDim.x, cur ^= 1) {
-    const int64_t next = item + gridDim.x;
-    __syncthreads();  // previous item fully stored: vbase[cur^1] and cbuf are free
-    item_bases(cur ^ 1, next);
-    __syncthreads();  // vbase[cur^1] visible
-    prefetch(cur ^ 1, next);
-    cp_async_commit();
-    cp_async_wait<1>();  // this item's vectors have landed (own copies)
-    __syncthreads();     // ... everyone's copies
-    // packing fused into the first FFT stage (vector 0 -> real, vector 1 -> imaginary)
-    static_assert(VPI == 2, "one complex FFT per work item");
-    const double* st = stage + cur * VPI * SL;
-    stockham_first_stage_packed<L, kThreads>(cbuf, st, st + SL, nn);
-    fft_after_first_stage<L, NF, kThreads>(cbuf, tw);
-    // post-process and store: both outputs k = e + 1 come from W_k and W_{L-k}
-    const int64_t b0 = vbase[cur][0], b1 = vbase[cur][1];
-    const int64_t step = inner;  // element stride (1 for the contiguous axis)
-    for (int e = threadIdx.x; e < nn; e += kThreads) {
-      const int k = e + 1;
-      const double2 wk = cbuf[pidx(k)], wm = cbuf[pidx(L - k)];
-      if (b0 >= 0) __stcs(dst + b0 + int64_t(e) * step, -hs * (wk.y - wm.y));
-      if (b1 >= 0) __stcs(dst + b1 + int64_t(e) * step, hs * (wk.x - wm.x));
+  for (; item < nitems; item += gridDim.x) {
+    double2 v[4], w[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) v[r] = make_double2(na[r], nb[r]);
+    const int64_t b0 = nb0, b1 = nb1;
+    fetch(item + gridDim.x, na, nb, nb0, nb1);  // next item's loads in flight
+    // stage 1 (Ns = 1): DFT-8 of (v0..v3, 0, 0, 0, 0)
+#pragma unroll
+    for (int r = 0; r < 4; ++r) w[r] = v[r];
+    w[1] = make_double2((w[1].x + w[1].y) * r2, (w[1].y - w[1].x) * r2);
+    w[2] = mul_neg_i(w[2]);
+    w[3] = make_double2((w[3].y - w[3].x) * r2, -(w[3].x + w[3].y) * r2);
+    dft4(v[0], v[1], v[2], v[3]);
+    dft4(w[0], w[1], w[2], w[3]);
+    __syncthreads();  // previous item's post-processing reads of cbuf are done
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      cbuf[pidx(j * 8 + 2 * q)] = v[q];
+      cbuf[pidx(j * 8 + 2 * q + 1)] = w[q];
+    }
+    __syncthreads();
+    if constexpr (last_radix<L>() == 4) {
+      // middle stages, then the last radix-4 stage fused with the post-processing
+      fft_middle_stages<L, kThreads>(cbuf, tw);
+      last_radix4_stage_with_post<L, kThreads>(cbuf, tw, hs, nn, [&](int k, double ya, double yb) {
+        if (b0 >= 0) __stcs(dst + b0 + int64_t(k - 1) * inner, ya);
+        if (b1 >= 0) __stcs(dst + b1 + int64_t(k - 1) * inner, yb);
+      });
+    } else {
+      fft_after_first_stage<L, 1, kThreads>(cbuf, tw);
+      // post-process and store: both outputs k = e + 1 come from W_k and W_{L-k}
+      for (int e = j; e < nn; e += kThreads) {
+        const int k = e + 1;
+        const double2 wk = cbuf[pidx(k)], wm = cbuf[pidx(L - k)];
+        if (b0 >= 0) __stcs(dst + b0 + int64_t(e) * inner, -hs * (wk.y - wm.y));
+        if (b1 >= 0) __stcs(dst + b1 + int64_t(e) * inner, hs * (wk.x - wm.x));
+      }
     }
   }
-  cp_async_wait<0>();
 }
 
 }  // namespace stkg

@@ -397,34 +397,27 @@ ModeWeight mode_weight(const stkg_heat& h) {
                     h.ndim > 2 ? h.inv_mu[2].p : nullptr, h.n[1], h.n[2], h.ndim};
 }
 
-template <int L, int VPI>
-void launch_dst_vpi(const stkg_heat& h, int a, const double* src, double* dst, int64_t inner,
-                    int64_t outer) {
-  using C = DstLaunch<L>;
-  constexpr size_t smem = C::template smem<VPI>();
-  static const bool configured = [] {
-    STKG_CUDA_CHECK(cudaFuncSetAttribute(dst_axis_kernel<L, VPI>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem)));
-    return true;
-  }();
-  (void)configured;
-  const int64_t nvec = outer * inner;
-  const int64_t items = ceil_div(nvec, VPI);
-  const int64_t blocks = std::min<int64_t>(items, int64_t(148) * C::kCtasPerSm);
-  const double scale = std::sqrt(2.0 / static_cast<double>(h.n[a] + 1));
-  dst_axis_kernel<L, VPI><<<static_cast<unsigned>(blocks), C::kThreads, smem, h.stream>>>(
-      src, dst, h.n[a], inner, nvec, reinterpret_cast<const double2*>(h.twiddle[a].p), scale);
-  STKG_CUDA_CHECK(cudaGetLastError());
-}
-
 template <int L>
 void launch_dst(const stkg_heat& h, int a, const double* src, double* dst, int64_t inner,
                 int64_t outer) {
-  if (inner == 1)
-    launch_dst_vpi<L, DstLaunch<L>::kVpiFast>(h, a, src, dst, inner, outer);
-  else
-    launch_dst_vpi<L, DstLaunch<L>::kVpiStrided>(h, a, src, dst, inner, outer);
+  using C = DstLaunch<L>;
+  static const bool configured = [] {
+    STKG_CUDA_CHECK(cudaFuncSetAttribute(dst_axis_kernel<L>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(C::kSmem)));
+    return true;
+  }();
+  (void)configured;
+  int per_sm = 0;
+  STKG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dst_axis_kernel<L>,
+                                                                C::kThreads, C::kSmem));
+  const int64_t nvec = outer * inner;
+  const int64_t items = ceil_div(nvec, 2);
+  const int64_t blocks = std::min<int64_t>(items, int64_t(148) * std::max(per_sm, 1));
+  const double scale = std::sqrt(2.0 / static_cast<double>(h.n[a] + 1));
+  dst_axis_kernel<L><<<static_cast<unsigned>(blocks), C::kThreads, C::kSmem, h.stream>>>(
+      src, dst, h.n[a], inner, nvec, reinterpret_cast<const double2*>(h.twiddle[a].p), scale);
+  STKG_CUDA_CHECK(cudaGetLastError());
 }
 
 void dst_pass(const stkg_heat& h, int a, const double* src, double* dst, int64_t inner,
