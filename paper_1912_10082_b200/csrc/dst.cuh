@@ -91,122 +91,88 @@ template <int L>
 constexpr int padded_len() { return L + L / 8; }
 
 // One Stockham stage of radix R over NFFT FFTs of length L stored back to back in buf.
-// Ns = product of the radices of the previous stages.  In place: every thread reads its
-// inputs, the block synchronises, then the outputs are written.
-template <int L, int NFFT, int R, int THREADS>
-__device__ __forceinline__ void stockham_stage(double2* buf, int Ns,
-                                              const double2* __restrict__ tw) {
+// NS = product of the radices of the previous stages, a compile-time constant so that the
+// padded shared-memory index arithmetic folds into constant offsets.  In place: every
+// thread reads its inputs, the block synchronises, then the outputs are written.
+template <int L, int NFFT, int R, int THREADS, int NS>
+__device__ __forceinline__ void stockham_stage(double2* buf, const double2* __restrict__ tw) {
   constexpr int kBut = L / R;                 // butterflies per FFT
   constexpr int total = NFFT * kBut;
   constexpr int kMaxPer = (total + THREADS - 1) / THREADS;
+  constexpr int stride = L / (NS * R);        // twiddle index step
   double2 v[kMaxPer][R];
-  int base_out[kMaxPer];
-  int cnt = 0;
 #pragma unroll
   for (int u = 0; u < kMaxPer; ++u) {
     const int t = threadIdx.x + u * THREADS;
-    if (t < total) {
+    if (total % THREADS == 0 || t < total) {
       const int f = t / kBut, j = t % kBut;
-      double2* x = buf + f * padded_len<L>();
-      const int k = j % Ns;
-      const int stride = L / (Ns * R);  // twiddle index step
-      // one table load per butterfly: w = exp(-2 pi i k / (Ns R)); w^r by multiplication
+      const double2* x = buf + f * padded_len<L>();
+      const int k = j % NS;
+      // one table load per butterfly: w = exp(-2 pi i k / (NS R)); w^r by multiplication
       // (a few ulps, far below the 1e-10 parity bar) instead of R-1 L1 loads
       double2 wr = make_double2(1.0, 0.0);
-      const double2 w = k > 0 ? __ldg(tw + k * stride) : make_double2(1.0, 0.0);
+      const double2 w = (NS > 1 && k > 0) ? __ldg(tw + k * stride) : make_double2(1.0, 0.0);
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         double2 val = x[pidx(j + r * kBut)];
-        if (r > 0) {
+        if (NS > 1 && r > 0) {
           wr = r == 1 ? w : cmul(wr, w);
           if (k > 0) val = cmul(val, wr);
         }
         v[u][r] = val;
       }
-      base_out[u] = f * padded_len<L>() + (j / Ns) * Ns * R + k;  // unpadded within the FFT
-      ++cnt;
     }
   }
   __syncthreads();
 #pragma unroll
   for (int u = 0; u < kMaxPer; ++u) {
-    if (u < cnt) {
+    const int t = threadIdx.x + u * THREADS;
+    if (total % THREADS == 0 || t < total) {
+      const int f = t / kBut, j = t % kBut;
       dft_radix<R>(v[u]);
+      double2* y = buf + f * padded_len<L>();
+      const int base = (j / NS) * NS * R + j % NS;
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const int fo = base_out[u] / padded_len<L>(), io = base_out[u] % padded_len<L>() + r * Ns;
-        buf[fo * padded_len<L>() + pidx(io)] = v[u][r];
-      }
+      for (int r = 0; r < R; ++r) y[pidx(base + r * NS)] = v[u][r];
     }
   }
   __syncthreads();
 }
 
-// First radix-8 Stockham stage (Ns = 1, no twiddles) fused with the packing of two real
-// vectors a, b (length n = L/2 - 1, in shared staging arrays) into c_m = a_{m-1} + i b_{m-1}:
-// inputs m = j + r L/8 with r >= 4 are the zero padding (m >= L/2), so only 4 of the 8
-// butterfly inputs are loaded and the first radix-2 layer of the DFT-8 disappears.
-template <int L, int THREADS>
-__device__ __forceinline__ void stockham_first_stage_packed(double2* buf, const double* sa,
-                                                           const double* sb, int n) {
-  constexpr int kBut = L / 8;
-  constexpr double r2 = 0.70710678118654752440;
-  for (int j = threadIdx.x; j < kBut; j += THREADS) {
-    double2 a[4], b[4];
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const int m = j + r * kBut;
-      a[r] = (m >= 1 && m <= n) ? make_double2(sa[m - 1], sb[m - 1]) : make_double2(0.0, 0.0);
-      b[r] = a[r];
-    }
-    b[1] = make_double2((b[1].x + b[1].y) * r2, (b[1].y - b[1].x) * r2);
-    b[2] = mul_neg_i(b[2]);
-    b[3] = make_double2((b[3].y - b[3].x) * r2, -(b[3].x + b[3].y) * r2);
-    dft4(a[0], a[1], a[2], a[3]);
-    dft4(b[0], b[1], b[2], b[3]);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      buf[pidx(j * 8 + 2 * q)] = a[q];
-      buf[pidx(j * 8 + 2 * q + 1)] = b[q];
-    }
-  }
-  __syncthreads();
-}
-
-// Remaining stages of the length-L FFT after the fused first radix-8 stage.
-template <int L, int NFFT, int THREADS>
-__device__ __forceinline__ void fft_after_first_stage(double2* buf, const double2* tw) {
-  constexpr int kStages8 = ilog2(L) / 3;
-  constexpr int kTail = L >> (3 * kStages8);
-  int Ns = 8;
-#pragma unroll
-  for (int st = 1; st < kStages8; ++st) {
-    stockham_stage<L, NFFT, 8, THREADS>(buf, Ns, tw);
-    Ns *= 8;
-  }
-  if constexpr (kTail == 2) stockham_stage<L, NFFT, 2, THREADS>(buf, Ns, tw);
-  if constexpr (kTail == 4) stockham_stage<L, NFFT, 4, THREADS>(buf, Ns, tw);
-}
-
-// Radix of the last stage of the length-L plan (8, 4 or 2).
+// Radix of the last stage of the length-L plan: floor(log8 L) radix-8 stages, then a
+// radix-4 or -2 stage when log2 L is not a multiple of 3.
 template <int L>
 constexpr int last_radix() {
   return (L >> (3 * (ilog2(L) / 3))) == 1 ? 8 : (L >> (3 * (ilog2(L) / 3)));
 }
 
-// All stages after the fused first one except the last (used when the last stage is fused
-// with the DST post-processing).
-template <int L, int THREADS>
-__device__ __forceinline__ int fft_middle_stages(double2* buf, const double2* tw) {
-  constexpr int kStages8 = ilog2(L) / 3;
-  constexpr int kLast8 = last_radix<L>() == 8 ? 1 : 0;  // last stage is one of the radix-8s
-  int Ns = 8;
-#pragma unroll
-  for (int st = 1; st < kStages8 - kLast8; ++st) {
-    stockham_stage<L, 1, 8, THREADS>(buf, Ns, tw);
-    Ns *= 8;
+// COUNT radix-8 stages starting at NS (compile-time recursion).
+template <int L, int NFFT, int THREADS, int NS, int COUNT>
+__device__ __forceinline__ void radix8_stages(double2* buf, const double2* tw) {
+  if constexpr (COUNT > 0) {
+    stockham_stage<L, NFFT, 8, THREADS, NS>(buf, tw);
+    radix8_stages<L, NFFT, THREADS, NS * 8, COUNT - 1>(buf, tw);
   }
-  return Ns;
+}
+
+// The stages after the fused first radix-8 stage, excluding the last one (which is fused
+// with the DST post-processing when it has radix 4).
+template <int L, int THREADS>
+__device__ __forceinline__ void fft_middle_stages(double2* buf, const double2* tw) {
+  constexpr int kStages8 = ilog2(L) / 3;
+  constexpr int kLast8 = last_radix<L>() == 8 ? 1 : 0;
+  radix8_stages<L, 1, THREADS, 8, kStages8 - 1 - kLast8>(buf, tw);
+}
+
+// All stages after the fused first radix-8 stage.
+template <int L, int NFFT, int THREADS>
+__device__ __forceinline__ void fft_after_first_stage(double2* buf, const double2* tw) {
+  constexpr int kStages8 = ilog2(L) / 3;
+  constexpr int kTail = L >> (3 * kStages8);
+  constexpr int kNsTail = 1 << (3 * kStages8);
+  radix8_stages<L, NFFT, THREADS, 8, kStages8 - 1>(buf, tw);
+  if constexpr (kTail == 2) stockham_stage<L, NFFT, 2, THREADS, kNsTail>(buf, tw);
+  if constexpr (kTail == 4) stockham_stage<L, NFFT, 4, THREADS, kNsTail>(buf, tw);
 }
 
 // Last Stockham stage of radix 4 (Ns = L/4 butterflies, THREADS = L/8: two per thread)
@@ -252,21 +218,6 @@ __device__ __forceinline__ void last_radix4_stage_with_post(const double2* buf,
       emit(k, -hs * (W[u][r].y - pm.y), hs * (W[u][r].x - pm.x));
     }
   }
-}
-
-// Full forward FFT of length L = 2^k: floor(k/3) radix-8 stages, then one radix-4 or -2.
-template <int L, int NFFT, int THREADS>
-__device__ __forceinline__ void fft_inplace(double2* buf, const double2* tw) {
-  constexpr int kStages8 = ilog2(L) / 3;
-  constexpr int kTail = L >> (3 * kStages8);
-  int Ns = 1;
-#pragma unroll
-  for (int st = 0; st < kStages8; ++st) {
-    stockham_stage<L, NFFT, 8, THREADS>(buf, Ns, tw);
-    Ns *= 8;
-  }
-  if constexpr (kTail == 2) stockham_stage<L, NFFT, 2, THREADS>(buf, Ns, tw);
-  if constexpr (kTail == 4) stockham_stage<L, NFFT, 4, THREADS>(buf, Ns, tw);
 }
 
 // Orthonormal DST-I along one axis of data viewed as [outer][n][inner] (element j of
@@ -360,6 +311,113 @@ __global__ void __launch_bounds__(L / 8, (L >= 2048 ? 2 : 3)) dst_axis_kernel(co
       }
     }
   }
+}
+
+// Strided axis (inner > 1): element j of vector (o, i) at (o * n + j) * inner + i.  A work
+// item is a tile of G = 8 neighbouring vectors, so every row of the tile is 64 contiguous
+// bytes (full DRAM bursts instead of 16-byte pieces).  Tiles are staged by cp.async into
+// a double-buffered [G][n] shared-memory buffer (the next tile loads while this one is
+// transformed), the G/2 complex FFTs read their inputs from and write their outputs back
+// into the tile rows, and the tile leaves with coalesced 64-byte row stores.
+template <int L>
+struct DstStridedLaunch {
+  static constexpr int kG = 8;
+  static constexpr int kThreads = L / 8;
+  static constexpr int kRow = L / 2;  // staging row pitch (>= n)
+  // One staging buffer and 2 CTAs per SM: while one CTA waits for its tile the other one
+  // transforms (a second buffer per CTA would halve the CTAs per SM).
+  static constexpr int kBufs = 1;
+  static constexpr size_t kSmem =
+      size_t(padded_len<L>()) * sizeof(double2) + size_t(kBufs) * kG * kRow * sizeof(double);
+};
+
+template <int L>
+__global__ void __launch_bounds__(L / 8, 2) dst_strided_kernel(
+    const double* __restrict__ src, double* __restrict__ dst, int64_t n, int64_t inner,
+    int64_t nvec, const double2* __restrict__ tw, double scale) {
+  using C = DstStridedLaunch<L>;
+  constexpr int G = C::kG, kThreads = C::kThreads, RP = C::kRow;
+  constexpr double r2 = 0.70710678118654752440;
+  extern __shared__ __align__(16) double2 cbuf[];
+  double* stage = reinterpret_cast<double*>(cbuf + padded_len<L>());  // [2][G][RP]
+  __shared__ int64_t vbase[2][G];
+  const int nn = static_cast<int>(n);
+  const int64_t ntiles = (nvec + G - 1) / G;
+  const int j = threadIdx.x;
+
+  auto tile_bases = [&](int buf, int64_t tile) {
+    for (int v = threadIdx.x; v < G; v += kThreads) {  // kThreads may be < G (small L)
+      const int64_t g = tile * G + v;
+      vbase[buf][v] = (tile < ntiles && g < nvec) ? (g / inner) * n * inner + g % inner : -1;
+    }
+  };
+  auto load_tile = [&](int buf) {  // rows of G consecutive doubles -> stage[buf][v][j]
+    double* st = stage + buf * G * RP;
+    for (int e = threadIdx.x; e < G * nn; e += kThreads) {
+      const int v = e % G, jj = e / G;
+      const int64_t b = vbase[buf][v];
+      cp_async8(st + v * RP + jj, b >= 0 ? src + b + int64_t(jj) * inner : src, b >= 0);
+    }
+  };
+
+  const double hs = 0.5 * scale;
+  const int cur = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    __syncthreads();  // previous tile stored: vbase / stage are free
+    tile_bases(0, tile);
+    __syncthreads();
+    load_tile(0);
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();  // this tile has landed
+    double* st = stage + cur * G * RP;
+#pragma unroll 1
+    for (int f = 0; f < G / 2; ++f) {
+      double* ra = st + (2 * f) * RP;
+      double* rb = st + (2 * f + 1) * RP;
+      double2 v[4], w[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int m = j + r * kThreads;  // < L/2 = n + 1
+        v[r] = (m >= 1) ? make_double2(ra[m - 1], rb[m - 1]) : make_double2(0.0, 0.0);
+        w[r] = v[r];
+      }
+      w[1] = make_double2((w[1].x + w[1].y) * r2, (w[1].y - w[1].x) * r2);
+      w[2] = mul_neg_i(w[2]);
+      w[3] = make_double2((w[3].y - w[3].x) * r2, -(w[3].x + w[3].y) * r2);
+      dft4(v[0], v[1], v[2], v[3]);
+      dft4(w[0], w[1], w[2], w[3]);
+      __syncthreads();  // previous FFT's reads of cbuf are done
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        cbuf[pidx(j * 8 + 2 * q)] = v[q];
+        cbuf[pidx(j * 8 + 2 * q + 1)] = w[q];
+      }
+      __syncthreads();  // (also: every thread has read rows 2f, 2f+1)
+      auto emit = [&](int k, double ya, double yb) {
+        ra[k - 1] = ya;
+        rb[k - 1] = yb;
+      };
+      if constexpr (last_radix<L>() == 4) {
+        fft_middle_stages<L, kThreads>(cbuf, tw);
+        last_radix4_stage_with_post<L, kThreads>(cbuf, tw, hs, nn, emit);
+      } else {
+        fft_after_first_stage<L, 1, kThreads>(cbuf, tw);
+        for (int e = j; e < nn; e += kThreads) {
+          const int k = e + 1;
+          const double2 wk = cbuf[pidx(k)], wm = cbuf[pidx(L - k)];
+          emit(k, -hs * (wk.y - wm.y), hs * (wk.x - wm.x));
+        }
+      }
+    }
+    __syncthreads();  // all G rows of results are in the stage buffer
+    for (int e = threadIdx.x; e < G * nn; e += kThreads) {
+      const int v = e % G, kk = e / G;
+      const int64_t b = vbase[cur][v];
+      if (b >= 0) __stcs(dst + b + int64_t(kk) * inner, st[v * RP + kk]);
+    }
+  }
+  cp_async_wait<0>();
 }
 
 }  // namespace stkg

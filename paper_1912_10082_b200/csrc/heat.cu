@@ -398,8 +398,32 @@ ModeWeight mode_weight(const stkg_heat& h) {
 }
 
 template <int L>
+void launch_dst_strided(const stkg_heat& h, int a, const double* src, double* dst,
+                        int64_t inner, int64_t outer) {
+  using C = DstStridedLaunch<L>;
+  static const bool configured = [] {
+    STKG_CUDA_CHECK(cudaFuncSetAttribute(dst_strided_kernel<L>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(C::kSmem)));
+    return true;
+  }();
+  (void)configured;
+  int per_sm = 0;
+  STKG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dst_strided_kernel<L>,
+                                                                C::kThreads, C::kSmem));
+  const int64_t nvec = outer * inner;
+  const int64_t tiles = ceil_div(nvec, C::kG);
+  const int64_t blocks = std::min<int64_t>(tiles, int64_t(148) * std::max(per_sm, 1));
+  const double scale = std::sqrt(2.0 / static_cast<double>(h.n[a] + 1));
+  dst_strided_kernel<L><<<static_cast<unsigned>(blocks), C::kThreads, C::kSmem, h.stream>>>(
+      src, dst, h.n[a], inner, nvec, reinterpret_cast<const double2*>(h.twiddle[a].p), scale);
+  STKG_CUDA_CHECK(cudaGetLastError());
+}
+
+template <int L>
 void launch_dst(const stkg_heat& h, int a, const double* src, double* dst, int64_t inner,
                 int64_t outer) {
+  if (inner > 1) return launch_dst_strided<L>(h, a, src, dst, inner, outer);
   using C = DstLaunch<L>;
   static const bool configured = [] {
     STKG_CUDA_CHECK(cudaFuncSetAttribute(dst_axis_kernel<L>,
