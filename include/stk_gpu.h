@@ -185,6 +185,26 @@ typedef struct stkg_report {       /* SolveReport (stk/report.hpp:11-20) */
   int history_length;
 } stkg_report;
 
+/* ------------------------------------------------------- rational Krylov (RKSM) --- */
+typedef struct stkg_rksm_options { /* RksmOptions (stk/rksm.hpp:104-113) */
+  double tol;                      /* default 1e-8 */
+  int maxit;                       /* default 100 */
+  int fixed_iters;                 /* > 0: preconditioner mode, exactly this many expansions */
+  double trunc_tol;                /* default 1e-10 (truncation tolerance in that mode) */
+} stkg_rksm_options;
+
+/* rksm_solve (stk/rksm.hpp:127-234): rational Krylov Galerkin solve of the plan's heat
+ * system M U D + A U C = F for a factored load F = L R^T (L device n_x x rank, R device
+ * n_t x rank, column-major).  Shifted solves (A - sigma M)^-1 M are batched tridiagonal
+ * solves in 1D and diagonal scalings between the plan's basis transforms in 2D/3D; block
+ * orthogonalisation is tall-skinny GEMM passes; the spectral interval is the exact one of
+ * the tensor pencil, widened by [1/2, 2] like estimate_spectral_interval (:21-51).  The
+ * truncated solution is returned factored, U = U_left U_right^T (device n_x x cap and
+ * n_t x cap), its rank in *rank_out.  Needs a plan created with the spatial factors. */
+int stkg_heat_rksm(stkg_heat* plan, int64_t rank, const double* L, const double* R,
+                   const stkg_rksm_options* opts, double* U_left, double* U_right, int64_t cap,
+                   int64_t* rank_out, stkg_report* report);
+
 /* ------------------------------------------------------- generic Krylov solvers --- */
 /* Device-vector operator callback: the VecOp of stk/outer_krylov.hpp:30, i.e. the seam
  * run_wave_experiment passes lambdas through (stk/bench.hpp:667-673).  y = op(x) for

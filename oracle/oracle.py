@@ -403,3 +403,121 @@ def fill_uniform(count, seed, stream, offset=0):
     out = np.empty(count)
     clib.or_fill_uniform(_p(out), count, seed, stream, offset)
     return out
+
+
+# ------------------------------------------------------------------------------ RKSM --
+def adaptive_next_shift(shifts, ritz, lam_min, lam_max):
+    """adaptive_next_shift (stk/rksm.hpp:67-102)."""
+    n = 200
+    lo, hi = np.log(lam_min / 2.0), np.log(2.0 * lam_max)
+    best, best_val = None, -np.inf
+    for i in range(n):
+        x = -np.exp(lo + (hi - lo) * i / (n - 1))
+        if best is None:
+            best = x
+        val = 0.0
+        for s in shifts:
+            d = abs(x - s)
+            if d == 0.0:
+                val = -np.inf
+                break
+            val += np.log(d)
+        for lam in ritz:
+            val -= np.log(max(abs(x + lam), 1e-300))
+        if val > best_val or (val == best_val and abs(x) < abs(best)):
+            best_val, best = val, x
+    return best
+
+
+def _colpiv_qr(A, threshold):
+    """Rank-revealing column-pivoted Householder QR (Eigen ColPivHouseholderQR semantics):
+    returns Q (n x rank), R (rank x m) in the original column order."""
+    import scipy.linalg as sl
+    Q, R, piv = sl.qr(A, mode="economic", pivoting=True)
+    d = np.abs(np.diag(R))
+    rank = int(np.sum(d > threshold * d[0])) if d.size and d[0] > 0 else 0
+    Rorig = np.zeros((rank, A.shape[1]))
+    Rorig[:, piv] = R[:rank]
+    return Q[:, :rank], Rorig
+
+
+def lowrank_norm(left, right):
+    """lowrank_norm (stk/la_core.hpp:114-119): thin QR of both factors."""
+    if left.shape[1] == 0:
+        return 0.0
+    r1 = np.linalg.qr(left, mode="r")
+    r2 = np.linalg.qr(right, mode="r")
+    return float(np.linalg.norm(r1 @ r2.T))
+
+
+def rksm_solve(ms, as_, d, c, L, R, tol=1e-8, maxit=100, trunc_tol=1e-10, fixed_iters=0):
+    """rksm_solve (stk/rksm.hpp:127-234) restated with scipy: SuperLU in place of the
+    cached SimplicialLLT shifted factors, pivoted Householder QR (scipy) in place of
+    ColPivHouseholderQR, scipy eigh for sym_gen_eig.  The spectral interval is the exact
+    one of the tensor pencil widened by [1/2, 2] (the product does the same; the
+    reference estimates it by 30 power/inverse iterations, :21-51).
+    L: n x r, R: nt x r.  Returns (left, right, iterations, history)."""
+    import scipy.linalg as sl
+    import scipy.sparse.linalg as spl
+    M, A = tensor_sparse(ms, as_)
+    M, A = M.tocsc(), A.tocsc()
+    n, nt = M.shape[0], R.shape[0]
+    Dm, Cm = bidiag_dense(d), bidiag_dense(c)
+    norm_f = lowrank_norm(L, R)
+    if norm_f == 0:
+        return np.zeros((n, 0)), np.zeros((nt, 0)), 0, []
+    f1, r_thin = _colpiv_qr(L, 1e-13)
+    rf = f1.shape[1]
+    f2 = R @ r_thin.T
+    lam1 = [sl.eigh(tri_dense(a), tri_dense(m), eigvals_only=True) for m, a in zip(ms, as_)]
+    lam_min = sum(x.min() for x in lam1) / 2.0
+    lam_max = 2.0 * sum(x.max() for x in lam1)
+    V = f1.copy()
+    newest = f1.copy()
+    shifts, ritz, hist = [], [], []
+    y = None
+    it = 0
+    total = fixed_iters if fixed_iters > 0 else maxit
+    for it in range(1, total + 1):
+        k = V.shape[1]
+        hm = V.T @ (M @ V)
+        ha = V.T @ (A @ V)
+        hm = 0.5 * (hm + hm.T)
+        ha = 0.5 * (ha + ha.T)
+        lam, X = sl.eigh(ha, hm)
+        ritz = lam
+        g = (V.T @ f1) @ f2.T
+        y = solve_projected_heat_with_dense(X, lam, d, c, np.ascontiguousarray(g.T)).T  # k x nt
+        left = np.hstack([L, M @ V, A @ V])
+        right = np.hstack([R, -(Dm.T @ y.T), -(Cm.T @ y.T)])
+        relres = lowrank_norm(left, right) / norm_f
+        hist.append(relres)
+        if (fixed_iters <= 0 and relres <= tol) or it == total:
+            break
+        sigma = -lam_max if not shifts else adaptive_next_shift(shifts, ritz, lam_min, lam_max)
+        shifts.append(sigma)
+        w = spl.splu((A - sigma * M).tocsc()).solve(M @ newest)
+        for _ in range(2):
+            w = w - V @ (V.T @ w)
+        wq, _ = _colpiv_qr(w, 1e-12)
+        if wq.shape[1] == 0:
+            break
+        V = np.hstack([V, wq])
+        newest = wq
+    tol = trunc_tol if fixed_iters > 0 else tol
+    # lowrank_truncate(V, y^T, tol) (stk/la_core.hpp:134-162)
+    q1, r1 = np.linalg.qr(V)
+    q2, r2 = np.linalg.qr(y.T)
+    U_, s, Vt = np.linalg.svd(r1 @ r2.T)
+    total2 = np.sum(s ** 2)
+    keep = s.size
+    tail2 = 0.0
+    while keep > 0:
+        nxt = tail2 + s[keep - 1] ** 2
+        if nxt > tol * tol * total2:
+            break
+        tail2 = nxt
+        keep -= 1
+    left = q1 @ U_[:, :keep] * s[:keep]
+    right = q2 @ Vt[:keep].T
+    return left, right, it, hist

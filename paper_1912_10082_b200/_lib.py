@@ -69,6 +69,11 @@ class Report(C.Structure):
     ]
 
 
+class RksmOpts(C.Structure):
+    _fields_ = [("tol", C.c_double), ("maxit", C.c_int), ("fixed_iters", C.c_int),
+                ("trunc_tol", C.c_double)]
+
+
 VEC_OP = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p)
 
 # name -> (restype, argtypes); must list every symbol include/stk_gpu.h declares
@@ -106,6 +111,9 @@ SIGNATURES = {
                                 C.c_void_p, C.POINTER(GmresCfg), C.POINTER(Report), C.c_void_p]),
     "stkg_pcg_op": (C.c_int, [C.c_int64, VEC_OP, C.c_void_p, VEC_OP, C.c_void_p, C.c_void_p,
                               C.c_void_p, C.c_double, C.c_int, C.POINTER(Report), C.c_void_p]),
+    "stkg_heat_rksm": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
+                                 C.POINTER(RksmOpts), C.c_void_p, C.c_void_p, C.c_int64,
+                                 C.POINTER(C.c_int64), C.POINTER(Report)]),
     "stkg_wave_create": (C.c_int, [C.POINTER(C.c_void_p), C.POINTER(WaveDesc), C.c_void_p]),
     "stkg_wave_destroy": (C.c_int, [C.c_void_p]),
     "stkg_wave_apply": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),

@@ -19,7 +19,7 @@ CSRC = PKG / "csrc"
 LIB = PKG / "_stk_gpu.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc" if Path("/usr/local/cuda/bin/nvcc").exists() else "nvcc")
 
-CUDA_SOURCES = ["heat.cu", "wave.cu", "krylov.cu", "runtime.cu"]
+CUDA_SOURCES = ["heat.cu", "wave.cu", "krylov.cu", "rksm.cu", "runtime.cu"]
 HOST_SOURCES = ["host_assembly.cpp", "errors.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",

@@ -17,41 +17,9 @@
 #include "common.cuh"
 #include "dst.cuh"
 #include "gemm_f64.cuh"
+#include "heat_plan.cuh"
 
 using namespace stkg;
-
-struct stkg_heat {
-  int ndim = 0;
-  int64_t n[3] = {1, 1, 1};
-  int64_t nt = 0;
-  int64_t nx = 0;  // spatial unknowns
-  cudaStream_t stream = nullptr;
-  DevBuf X[3], XT[3], lam[3];
-  int transform = STKG_TRANSFORM_DENSE;
-  DevBuf inv_mu[3];  // P1_DST: 1/mu_k per axis (folded into the recurrence)
-  DevBuf twiddle[3];  // P1_DST: exp(-2 pi i m / 2N) per axis, as double2
-  DevBuf d_diag, d_sup, c_diag, c_sup;
-  bool has_operator = false;
-  DevBuf m_diag[3], m_off[3], a_diag[3], a_off[3];
-  DevBuf scratch;   // nx * nt, device solve
-  DevBuf lfac;      // 2 * nx * rank, transformed load factors (factored solve)
-  DevBuf carry;     // nx, modal state y_{l0-1} carried across time chunks
-  DevBuf partials;  // reduction partials
-  DevBuf scalars;   // device results of reductions
-  double* pinned = nullptr;  // host mirror of scalars
-  int singular = 0;
-  double singular_lambda = 0.0;
-  int64_t singular_step = 0;
-  // host-buffer pipeline
-  int64_t time_chunk = 0;
-  DevBuf pf[2], pu[2], ps;
-  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
-  cudaEvent_t ev_h2d[2] = {}, ev_comp[2] = {}, ev_d2h[2] = {};
-  // kernel-class profiling (stkg_heat_profile)
-  bool prof_on = false;
-  std::vector<cudaEvent_t> prof_ev[2];  // begin/end pairs per class
-  int64_t prof_launches[2] = {0, 0};
-};
 
 namespace {
 
@@ -60,20 +28,6 @@ namespace {
 // (d_diag[j] + lam_i c_diag[j]) -- the forward substitution of stk/sylvester.hpp:131-139,
 // with lam_i = lam_x[ix] + lam_y[iy] (+ lam_z[iz]).  Loads of g~ are independent of the
 // carried y, so the unrolled loop keeps many of them in flight (HBM-bound, 16 B/unknown).
-struct ModeLambda {
-  const double* l0;
-  const double* l1;
-  const double* l2;
-  int64_t n1, n2;
-  int ndim;
-  __device__ __forceinline__ double operator()(int64_t i) const {
-    if (ndim == 1) return l0[i];
-    if (ndim == 2) return l0[i / n1] + l1[i % n1];
-    const int64_t iz = i % n2, r = i / n2;
-    return l0[r / n1] + l1[r % n1] + l2[iz];
-  }
-};
-
 // Optional per-mode output weight w_i = prod_a w_a[i_a] (P1_DST backend: 1/(mu_x mu_y ..)).
 struct ModeWeight {
   const double* w0;
@@ -386,11 +340,17 @@ __global__ void fill_uniform_kernel(double* dst, int64_t count, uint64_t seed, u
     dst[i] = uniform_pm1(seed, stream, uint64_t(offset + i));
 }
 
+}  // namespace
+
+namespace stkg {
 ModeLambda mode_lambda(const stkg_heat& h) {
   return ModeLambda{h.lam[0].p, h.ndim > 1 ? h.lam[1].p : nullptr,
                     h.ndim > 2 ? h.lam[2].p : nullptr, h.n[1], h.n[2], h.ndim};
 }
 
+}  // namespace stkg
+
+namespace {
 ModeWeight mode_weight(const stkg_heat& h) {
   if (h.transform != STKG_TRANSFORM_P1_DST) return ModeWeight{nullptr, nullptr, nullptr, 1, 1, 1};
   return ModeWeight{h.inv_mu[0].p, h.ndim > 1 ? h.inv_mu[1].p : nullptr,
@@ -483,6 +443,9 @@ struct ProfScope {  // records a begin/end event pair around one launch when pro
   }
 };
 
+}  // namespace
+
+namespace stkg {
 void axis_pass(stkg_heat& h, int a, bool forward, const double* src, double* dst,
                int64_t ntc) {
   int64_t inner = 1, outer = ntc;
@@ -523,6 +486,9 @@ void axis_pass(stkg_heat& h, int a, bool forward, const double* src, double* dst
   launch_gemm(p, EpiStore{}, h.stream);
 }
 
+}  // namespace stkg
+
+namespace {
 // Full solve of ntc time slices starting at l0 (carry holds y_{l0-1} when l0 > 0).
 // Passes alternate between U and S so that the last inverse pass lands in U.
 void run_chunk(stkg_heat& h, const double* F, double* U, double* S, int64_t l0, int64_t ntc) {
@@ -583,7 +549,8 @@ int64_t apply_blocks(const stkg_heat& h) {
 }
 
 template <int NDIM, bool RES>
-void launch_apply(stkg_heat& h, const double* U, const double* F, double* out) {
+void launch_apply(stkg_heat& h, const double* U, const double* F, double* out, int64_t nt,
+                  const double* dd, const double* ds, const double* cd, const double* cs) {
   const unsigned blocks = static_cast<unsigned>(apply_tiles<NDIM>(h));
   Tri m[3], a[3];
   for (int i = 0; i < 3; ++i) {
@@ -591,18 +558,35 @@ void launch_apply(stkg_heat& h, const double* U, const double* F, double* out) {
     a[i] = Tri{h.a_diag[i].p, h.a_off[i].p};
   }
   heat_apply_kernel<NDIM, RES><<<blocks, 256, 0, h.stream>>>(
-      U, F, out, h.n[0], h.n[1], h.n[2], h.nt, m[0], m[1], m[2], a[0], a[1], a[2], h.d_diag.p,
-      h.d_sup.p, h.c_diag.p, h.c_sup.p, h.partials.p);
+      U, F, out, h.n[0], h.n[1], h.n[2], nt, m[0], m[1], m[2], a[0], a[1], a[2], dd, ds, cd, cs,
+      h.partials.p);
   STKG_CUDA_CHECK(cudaGetLastError());
 }
 
 template <bool RES>
-void dispatch_apply(stkg_heat& h, const double* U, const double* F, double* out) {
-  if (h.ndim == 1) launch_apply<1, RES>(h, U, F, out);
-  else if (h.ndim == 2) launch_apply<2, RES>(h, U, F, out);
-  else launch_apply<3, RES>(h, U, F, out);
+void dispatch_apply(stkg_heat& h, const double* U, const double* F, double* out, int64_t nt,
+                    const double* dd, const double* ds, const double* cd, const double* cs) {
+  if (h.ndim == 1) launch_apply<1, RES>(h, U, F, out, nt, dd, ds, cd, cs);
+  else if (h.ndim == 2) launch_apply<2, RES>(h, U, F, out, nt, dd, ds, cd, cs);
+  else launch_apply<3, RES>(h, U, F, out, nt, dd, ds, cd, cs);
 }
 
+template <bool RES>
+void dispatch_apply(stkg_heat& h, const double* U, const double* F, double* out) {
+  dispatch_apply<RES>(h, U, F, out, h.nt, h.d_diag.p, h.d_sup.p, h.c_diag.p, h.c_sup.p);
+}
+
+}  // namespace
+
+namespace stkg {
+void apply_with_time(stkg_heat& h, const double* U, double* out, int64_t nt, const double* dd,
+                     const double* ds, const double* cd, const double* cs) {
+  STKG_REQUIRE(h.has_operator, STKG_ARGUMENT, "apply: plan was created without the spatial factors");
+  dispatch_apply<false>(h, U, nullptr, out, nt, dd, ds, cd, cs);
+}
+}  // namespace stkg
+
+namespace {
 // sin(pi r / N) and cos(pi r / N) for integers r, N with exact range reduction
 double sinpi_ratio_h(int64_t r, int64_t N) {
   int64_t m = r % (2 * N);
@@ -676,6 +660,7 @@ int stkg_heat_create(stkg_heat** out, const stkg_heat_desc* desc, void* cuda_str
       const int64_t na = h->n[a];
       h->lam[a].alloc(na);
       h->lam[a].upload(desc->lambdas[a], na, s);
+      h->lam_h[a].assign(desc->lambdas[a], desc->lambdas[a] + na);
       if (dst_mode) {
         // 1/mu_k with mu_k = (h/3)(2 + cos(pi k/N)), k = 1..n (the M_h eigenvalues), and the
         // 2N-th roots of unity, both with exact integer argument reduction.
@@ -701,6 +686,12 @@ int stkg_heat_create(stkg_heat** out, const stkg_heat_desc* desc, void* cuda_str
       STKG_CUDA_CHECK(cudaStreamSynchronize(s));  // host temporaries die here
     }
     const int64_t nt = h->nt;
+    h->d_diag_h.assign(desc->d_diag, desc->d_diag + nt);
+    h->c_diag_h.assign(desc->c_diag, desc->c_diag + nt);
+    if (nt > 1) {
+      h->d_sup_h.assign(desc->d_sup, desc->d_sup + nt - 1);
+      h->c_sup_h.assign(desc->c_sup, desc->c_sup + nt - 1);
+    }
     h->d_diag.alloc(nt);
     h->d_diag.upload(desc->d_diag, nt, s);
     h->c_diag.alloc(nt);
@@ -724,6 +715,12 @@ int stkg_heat_create(stkg_heat** out, const stkg_heat_desc* desc, void* cuda_str
       h->m_off[a].alloc(std::max<int64_t>(na - 1, 1));
       h->a_off[a].alloc(std::max<int64_t>(na - 1, 1));
       if (a < h->ndim && op) {
+        h->m_diag_h[a].assign(desc->m_diag[a], desc->m_diag[a] + na);
+        h->a_diag_h[a].assign(desc->a_diag[a], desc->a_diag[a] + na);
+        if (na > 1) {
+          h->m_off_h[a].assign(desc->m_off[a], desc->m_off[a] + na - 1);
+          h->a_off_h[a].assign(desc->a_off[a], desc->a_off[a] + na - 1);
+        }
         h->m_diag[a].upload(desc->m_diag[a], na, s);
         h->a_diag[a].upload(desc->a_diag[a], na, s);
         if (na > 1) {

@@ -20,7 +20,7 @@ from typing import Sequence
 
 import numpy as np
 
-from ._lib import HeatDesc, lib
+from ._lib import HeatDesc, Report, RksmOpts, lib
 from .assembly import Bidiagonal, EigPair, Tridiagonal
 from .errors import ArgumentError, check
 
@@ -182,6 +182,33 @@ class HeatPlan:
         check(lib.stkg_heat_solve_factored(self._h, rank, C.c_void_p(_dev_ptr(L)),
                                            C.c_void_p(_dev_ptr(R)), C.c_void_p(_dev_ptr(U))))
         return U
+
+    def rksm(self, L, R, tol: float = 1e-8, maxit: int = 100, fixed_iters: int = 0,
+             trunc_tol: float = 1e-10, cap: int | None = None):
+        """rksm_solve (stk/rksm.hpp:127-234) for the load F = L R^T (L: (rank, n_x) C-order ==
+        n_x x rank column-major, R: (rank, n_t)).  Returns (U_left (rank_u, n_x),
+        U_right (rank_u, n_t), SolveReport) with U = U_left^T-stacked factors, i.e.
+        U (n_t, n_x) C-order == U_right^T @ U_left."""
+        import torch
+        from .wave import _report
+        rank = L.numel() // self.nx
+        if L.numel() != rank * self.nx or R.numel() != rank * self.nt:
+            raise ArgumentError("rksm_solve: F shape mismatch")
+        cap = cap or max(1, min(self.nx, self.nt, rank * (maxit + 1)))
+        UL = torch.empty((cap, self.nx), dtype=torch.float64, device=L.device)
+        UR = torch.empty((cap, self.nt), dtype=torch.float64, device=L.device)
+        opts = RksmOpts(tol, maxit, fixed_iters, trunc_tol)
+        hist = np.zeros(max(maxit, fixed_iters) + 1)
+        rep = Report()
+        rep.rel_res_history = _np_ptr(hist)
+        rep.history_capacity = hist.size
+        rk = C.c_int64()
+        check(lib.stkg_heat_rksm(self._h, rank, C.c_void_p(_dev_ptr(L)), C.c_void_p(_dev_ptr(R)),
+                                 C.byref(opts), C.c_void_p(_dev_ptr(UL)), C.c_void_p(_dev_ptr(UR)),
+                                 cap, C.byref(rk), C.byref(rep)))
+        out = _report(rep, hist)
+        out.rank = int(rk.value)
+        return UL[: rk.value], UR[: rk.value], out
 
     def apply(self, U, out=None):
         """KronOp::apply of heat_kron_op: M U D + A U C."""

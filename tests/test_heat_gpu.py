@@ -265,3 +265,105 @@ def test_dst_host_and_factored_paths(stk, cuda):
     assert rel(ps.solve_host(F), Ud) < 1e-14
     assert np.array_equal(host(ps.solve(dev(F))), Ud)  # deterministic
     assert rel(host(ps.solve_factored(dev(L), dev(R))), Ud) < 1e-13
+
+
+# ------------------------------------------------------------------------------ RKSM --
+def _smooth_load(n, ndim, nt, T=1.0):
+    """heat-ex1-shaped separable load (stk/bench.hpp:302-306): 10 sin(t) t x cos(pi x/2)^ndim,
+    lumped onto the P1 basis (midpoint in time)."""
+    h = 1.0 / (n + 1)
+    f = np.cos(np.pi / 2 * np.arange(1, n + 1) * h) * h
+    L = f
+    for _ in range(ndim - 1):
+        L = np.kron(L, f)
+    tt = (np.arange(nt) + 0.5) * T / nt
+    return L[None, :], (10 * np.sin(tt) * tt * T / nt)[None, :]
+
+
+def _rksm_oracle(orc, ndim, n, nt, L, R, **kw):
+    m, a = orc.fem1d_matrices(0.0, 1.0, n)
+    d, c = orc.heat_time_matrices(nt)
+    left, right, its, hist = orc.rksm_solve([m] * ndim, [a] * ndim, d, c, L.T, R.T, **kw)
+    return (left @ right.T).T, its, hist
+
+
+def _rksm_gpu(stk, ndim, n, nt, L, R, transform="dense", **kw):
+    plan = stk.HeatPlan.p1_uniform(ndim, n, nt, transform=transform)
+    UL, UR, rep = plan.rksm(dev(L), dev(R), **kw)
+    return plan, host(UR).T @ host(UL), rep
+
+
+@pytest.mark.parametrize("n,nt,rank,src", [(10, 6, 1, "rand"), (63, 40, 3, "rand"),
+                                           (255, 256, 1, "cfg1"), (255, 256, 1, "smooth")])
+def test_rksm_1d_converges_vs_oracle_and_direct(stk, orc, cuda, n, nt, rank, src):
+    """rksm_solve (stk/rksm.hpp:127-234), 1D (shifted solves = batched Thomas): converges to
+    1e-8; the truncated solution matches the direct solve to 1e-6 (SPEC.md:411 example,
+    cfg1's shape) and the oracle's iterate and iteration count."""
+    from paper_1912_10082_b200 import inputs
+    if src == "cfg1":
+        left, right = inputs.heat_factors(inputs.CONFIGS["cfg1"])
+        L, R = left.T.copy(), right.T.copy()
+    elif src == "smooth":
+        L, R = _smooth_load(n, 1, nt)
+    else:
+        rng = np.random.default_rng(n)
+        L, R = rng.standard_normal((rank, n)), rng.standard_normal((rank, nt))
+    plan, U, rep = _rksm_gpu(stk, 1, n, nt, L, R, tol=1e-8, maxit=100)
+    assert rep.converged and rep.final_relres <= 1e-8
+    assert len(rep.rel_res_history) == rep.iterations
+    Ud = host(plan.solve_factored(dev(L), dev(R)))
+    assert rel(U, Ud) <= 1e-6
+    rr, _ = plan.residual(dev(U), dev(R.T @ L))
+    assert rr <= 1e-5  # truncation at tol perturbs U by 1e-8 ||U||; B amplifies it
+    Uo, its, hist = _rksm_oracle(orc, 1, n, nt, L, R, tol=1e-8, maxit=100)
+    assert abs(its - rep.iterations) <= 1
+    assert rel(U, Uo) <= 1e-6
+
+
+@pytest.mark.parametrize("transform", ["dense", "dst"])
+def test_rksm_2d_history_vs_oracle(stk, orc, cuda, transform):
+    """2D, fixed_iters (preconditioner mode, stk/rksm.hpp:172,226): per-iteration relative
+    residuals and the truncated iterate follow the oracle.  (With real negative poles the
+    reference's adaptive rule stalls near 1e-4 on 2D heat loads -- see DESIGN.md -- so
+    2D parity is on the history, not on convergence.)"""
+    n, nt = 31, 20
+    L, R = _smooth_load(n, 2, nt)
+    rng = np.random.default_rng(5)
+    L = np.vstack([L, rng.standard_normal((1, n * n))])
+    R = np.vstack([R, rng.standard_normal((1, nt))])
+    _, U, rep = _rksm_gpu(stk, 2, n, nt, L, R, transform=transform, fixed_iters=8)
+    Uo, its, hist = _rksm_oracle(orc, 2, n, nt, L, R, fixed_iters=8)
+    assert rep.iterations == its == 8 and rep.converged
+    np.testing.assert_allclose(rep.rel_res_history, hist, rtol=1e-6)
+    assert rel(U, Uo) <= 1e-8
+
+
+def test_rksm_maxit_and_zero_load(stk, orc, cuda):
+    """maxit reached above tol -> non-convergence result with the full history
+    (stk/rksm.hpp:201-204); F = 0 -> rank 0, 0 iterations (:137-141)."""
+    n, nt = 31, 24
+    L, R = _smooth_load(n, 2, nt)
+    _, U, rep = _rksm_gpu(stk, 2, n, nt, L, R, tol=1e-12, maxit=12)
+    assert not rep.converged and rep.iterations == 12 and len(rep.rel_res_history) == 12
+    Uo, its, hist = _rksm_oracle(orc, 2, n, nt, L, R, tol=1e-12, maxit=12)
+    np.testing.assert_allclose(rep.rel_res_history, hist, rtol=1e-6)
+    assert rel(U, Uo) <= 1e-8
+    _, U0, rep0 = _rksm_gpu(stk, 2, n, nt, np.zeros((1, n * n)), np.ones((1, nt)))
+    assert rep0.iterations == 0 and rep0.rank == 0 and rep0.converged and not U0.any()
+
+
+def test_rksm_cfg2_shape(stk, cuda):
+    """BASELINE cfg2 shape (2D 255^2 x 512, rank-4 N(0,1) load): both transform backends give
+    the same history; the true residual of the returned factors equals the reported one."""
+    from paper_1912_10082_b200 import inputs
+    cfg = inputs.CONFIGS["cfg2"]
+    left, right = inputs.heat_factors(cfg)
+    L, R = left.T.copy(), right.T.copy()
+    out = {}
+    for transform in ("dst", "dense"):
+        plan, U, rep = _rksm_gpu(stk, 2, cfg.n, cfg.nt, L, R, transform=transform, maxit=15)
+        rr, _ = plan.residual(dev(U), dev(R.T @ L))
+        assert abs(rr - rep.final_relres) <= 1e-6 * max(rr, 1e-12) + 1e-9
+        out[transform] = rep.rel_res_history
+        print(transform, "its", rep.iterations, "relres", rep.final_relres, "s", rep.wall_time_s)
+    np.testing.assert_allclose(out["dst"], out["dense"], rtol=1e-6)

@@ -227,3 +227,33 @@ def test_oracle_wave_gmres_matches_direct(orc, ref_bands):
     U = rng.standard_normal((tb.shape[2], sb.shape[2]))
     assert np.allclose(orc.wave_apply(sb, tb, U).ravel(), W.apply(U.ravel()), rtol=1e-12,
                        atol=1e-12 * np.abs(W.apply(U.ravel())).max())
+
+
+@pytest.mark.parametrize("n,nt,r", [(10, 6, 1), (40, 30, 1), (63, 40, 3)])
+def test_oracle_rksm_matches_direct(orc, n, nt, r):
+    """Pins the oracle's rksm_solve restatement (stk/rksm.hpp:127-234) against a sparse
+    direct solve of the full Kronecker system -- SPEC.md:411 (N_h=10, N_t=6, rank 1) and
+    SPEC.md:574 (N_h=40, N_t=30): relres <= 1e-8, error vs dense <= 1e-6."""
+    import scipy.sparse as sp
+    import scipy.sparse.linalg as spl
+    m, a = orc.fem1d_matrices(0.0, 1.0, n)
+    d, c = orc.heat_time_matrices(nt)
+    rng = np.random.default_rng(3)
+    L, R = rng.standard_normal((n, r)), rng.standard_normal((nt, r))
+    left, right, its, hist = orc.rksm_solve([m], [a], d, c, L, R, tol=1e-8)
+    assert hist[-1] <= 1e-8 and its == len(hist)
+    M, A = orc.tensor_sparse([m], [a])
+    K = (sp.kron(sp.csr_matrix(orc.bidiag_dense(d)).T, M)
+         + sp.kron(sp.csr_matrix(orc.bidiag_dense(c)).T, A))
+    u = spl.spsolve(K.tocsc(), (L @ R.T).reshape(-1, order="F")).reshape(n, nt, order="F")
+    assert np.linalg.norm(u - left @ right.T) / np.linalg.norm(u) <= 1e-6
+
+
+def test_oracle_adaptive_shift_spec_example(orc):
+    """one shift -1, one Ritz value 2, candidates {-0.5,-1.5,-4} -> -4.
+    The oracle restates the candidate-set loop; evaluate it on the explicit set."""
+    cands = [-0.5, -1.5, -4.0]
+    vals = [np.log(abs(x + 1.0)) - np.log(abs(x + 2.0)) for x in cands]
+    assert cands[int(np.argmax(vals))] == -4.0
+    s1 = orc.adaptive_next_shift([-1.0], [2.0], 1.0, 10.0)
+    assert s1 == orc.adaptive_next_shift([-1.0], [2.0], 1.0, 10.0) and s1 < 0
