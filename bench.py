@@ -241,6 +241,48 @@ def _timed_path(stk, inputs, cfg, transform, args, stream, barrier, F, U, with_c
     return plan, out, clk
 
 
+def rksm_leg(stk, inputs, with_cpu=True, name="cfg1"):
+    """the paper's rational Krylov solver (rksm_solve, stk/rksm.hpp:127-234)
+    on the BASELINE rank-1 config, next to the direct decoupled solve of the same factored
+    load.  Wall-clock around the synchronous C-ABI call (it interleaves host decisions)."""
+    import torch
+    cfg = inputs.CONFIGS[name]
+    left, right = inputs.heat_factors(cfg)
+    L = torch.tensor(left.T.copy(), device="cuda")
+    R = torch.tensor(right.T.copy(), device="cuda")
+    plan = stk.HeatPlan.p1_uniform(cfg.ndim, cfg.n, cfg.nt, transform="dst")
+    plan.rksm(L, R, maxit=4)  # warm-up: scratch buffers, pinned staging
+    reps = 5
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        _, _, rep = plan.rksm(L, R, tol=1e-8, maxit=100)
+    torch.cuda.synchronize()
+    t = (time.perf_counter() - t0) / reps
+    plan.solve_factored(L, R)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        plan.solve_factored(L, R)
+    torch.cuda.synchronize()
+    td = (time.perf_counter() - t0) / reps
+    out = {"workload": cfg.name, "tol": 1e-8, "iterations": rep.iterations,
+           "final_relres": rep.final_relres, "converged": rep.converged, "rank": rep.rank,
+           "mu_mem": rep.mu_mem, "ms": 1e3 * t, "unknowns_per_s": cfg.unknowns / t,
+           "direct_ms": 1e3 * td, "direct_unknowns_per_s": cfg.unknowns / td}
+    if with_cpu:
+        sys.path.insert(0, str(ROOT))
+        from oracle import oracle as orc
+        m, a = orc.fem1d_matrices(0.0, 1.0, cfg.n)
+        d, c = orc.heat_time_matrices(cfg.nt)
+        t0 = time.perf_counter()
+        _, _, its, _ = orc.rksm_solve([m], [a], d, c, left, right, tol=1e-8, maxit=100)
+        out["cpu_oracle"] = {"s": time.perf_counter() - t0, "iterations": its, "cores": 1,
+                             "kind": "port (numpy/scipy SuperLU restatement)"}
+    plan.close()
+    return out
+
+
 def run_ours(args):
     import torch
     rank, world, local = dist_env()
@@ -327,6 +369,8 @@ def run_ours(args):
     }
     if alt_res is not None:
         line["alt_path"] = alt_res
+    if rank == 0 and not args.no_rksm:
+        line["rksm"] = rksm_leg(stk, inputs, with_cpu=(world == 1 and not args.no_cpu))
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu_t = cpu_reference_run(cfg, args.ref_sample)
         cpu_v = cfg.nx * args.ref_sample / cpu_t
@@ -354,6 +398,7 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=CPU_SAMPLE_STEPS)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-rksm", action="store_true", help="skip the RKSM (cfg1) side leg")
     ap.add_argument("--no-alt", action="store_true", help="skip timing the other transform backend")
     ap.add_argument("--transform", choices=["dst", "dense"], default="dst",
                     help="headline backend: P1 fast sine transforms (dst) or dense DMMA GEMMs")

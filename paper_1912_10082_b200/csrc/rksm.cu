@@ -80,13 +80,16 @@ __global__ void __launch_bounds__(256) ts_gram_kernel(const double* __restrict__
   }
 }
 
+// Row r = j * kk + c of the partials -> out[j * ld + c] (a kk x bb block of a column-major
+// matrix with leading dimension ld).
 __global__ void __launch_bounds__(256) reduce_rows_kernel(const double* __restrict__ partials,
-                                                          int count, double* __restrict__ out) {
+                                                          int count, int kk, int64_t ld,
+                                                          double* __restrict__ out) {
   __shared__ double red[8];
   double s = 0.0;
   for (int b = threadIdx.x; b < count; b += 256) s += partials[int64_t(blockIdx.x) * count + b];
   s = block_sum<256>(s, red);
-  if (threadIdx.x == 0) out[blockIdx.x] = s;
+  if (threadIdx.x == 0) out[int64_t(blockIdx.x / kk) * ld + blockIdx.x % kk] = s;
 }
 
 // W (n x b) -= V (n x k) H (k x b, column-major, staged in shared memory)
@@ -184,10 +187,33 @@ class Rksm {
     STKG_CUDA_CHECK(cudaStreamSynchronize(s_));
   }
 
+  ~Rksm() {
+    if (hpin_) cudaFreeHost(hpin_);
+  }
+
   // ------------------------------------------------------------- device helpers ----
-  // H (k x b, column-major, host) = V(:, 0:k)^T W(:, 0:b)
-  hla::Mat gram(const double* V, int64_t k, const double* W, int64_t b) {
-    hla::Mat H(static_cast<size_t>(k * b));
+  // Growable per-purpose device scratch (no cudaMalloc inside the iteration once warm).
+  double* scratch(int slot, size_t count) {
+    DevBuf& b = slots_[slot];
+    if (b.n < count) {
+      STKG_CUDA_CHECK(cudaStreamSynchronize(s_));
+      b.alloc(std::max(count, 2 * b.n));
+    }
+    return b.p;
+  }
+  double* pinned(size_t count) {
+    if (hpin_n_ < count) {
+      STKG_CUDA_CHECK(cudaStreamSynchronize(s_));
+      if (hpin_) cudaFreeHost(hpin_);
+      hpin_n_ = std::max(count, 2 * hpin_n_);
+      STKG_CUDA_CHECK(cudaMallocHost(&hpin_, sizeof(double) * hpin_n_));
+    }
+    return hpin_;
+  }
+
+  // Hd (k x b, column-major, device, ld k) = V(:, 0:k)^T W(:, 0:b); asynchronous,
+  // deterministic (fixed-grid partials summed in index order).
+  void gram_dev(const double* V, int64_t k, const double* W, int64_t b, double* Hd) {
     for (int64_t j0 = 0; j0 < b; j0 += kTsRhs) {
       const int bb = static_cast<int>(std::min<int64_t>(kTsRhs, b - j0));
       for (int64_t c0 = 0; c0 < k; c0 += 1024) {
@@ -195,59 +221,75 @@ class Rksm {
         dim3 grid(kReduceBlocks, static_cast<unsigned>(ceil_div(kk, kTsCols)));
         ts_gram_kernel<kTsRhs><<<grid, 256, 0, s_>>>(V + c0 * n_, n_, kk, W + j0 * n_, bb,
                                                      partials_.p);
-        reduce_rows_kernel<<<kk * bb, 256, 0, s_>>>(partials_.p, kReduceBlocks, hdev_.p);
+        reduce_rows_kernel<<<kk * bb, 256, 0, s_>>>(partials_.p, kReduceBlocks, kk, k,
+                                                    Hd + j0 * k + c0);
         STKG_CUDA_CHECK(cudaGetLastError());
-        std::vector<double> tmp(static_cast<size_t>(kk) * bb);
-        STKG_CUDA_CHECK(cudaMemcpyAsync(tmp.data(), hdev_.p, sizeof(double) * tmp.size(),
-                                        cudaMemcpyDeviceToHost, s_));
-        STKG_CUDA_CHECK(cudaStreamSynchronize(s_));
-        for (int j = 0; j < bb; ++j)
-          for (int c = 0; c < kk; ++c) H[(j0 + j) * k + c0 + c] = tmp[static_cast<size_t>(j) * kk + c];
       }
     }
+  }
+
+  // H (k x b, column-major, host) = V(:, 0:k)^T W(:, 0:b): one device->host read.
+  hla::Mat gram(const double* V, int64_t k, const double* W, int64_t b) {
+    hla::Mat H(static_cast<size_t>(k * b));
+    if (k == 0 || b == 0) return H;
+    double* hd = scratch(kSlotGram, H.size());
+    gram_dev(V, k, W, b, hd);
+    double* hp = pinned(H.size());
+    STKG_CUDA_CHECK(cudaMemcpyAsync(hp, hd, sizeof(double) * H.size(), cudaMemcpyDeviceToHost, s_));
+    STKG_CUDA_CHECK(cudaStreamSynchronize(s_));
+    std::copy(hp, hp + H.size(), H.begin());
     return H;
+  }
+
+  // W(:, 0:b) -= V(:, 0:k) Hd (k x b, device, ld k); asynchronous.
+  void update_dev(double* W, int64_t b, const double* V, int64_t k, const double* Hd) {
+    if (k == 0 || b == 0) return;
+    static const bool configured = [] {
+      STKG_CUDA_CHECK(cudaFuncSetAttribute(ts_update_kernel<kTsRhs>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      return true;
+    }();
+    (void)configured;
+    const size_t smem = sizeof(double) * static_cast<size_t>(k) * kTsRhs;
+    STKG_REQUIRE(smem <= 200 * 1024, STKG_ARGUMENT, "rksm: Krylov basis too large");
+    for (int64_t j0 = 0; j0 < b; j0 += kTsRhs) {
+      const int bb = static_cast<int>(std::min<int64_t>(kTsRhs, b - j0));
+      ts_update_kernel<kTsRhs><<<kEw, 256, smem, s_>>>(W + j0 * n_, n_, bb, V, static_cast<int>(k),
+                                                       Hd + j0 * k);
+      STKG_CUDA_CHECK(cudaGetLastError());
+    }
   }
 
   // W(:, 0:b) -= V(:, 0:k) H (k x b host)
   void update(double* W, int64_t b, const double* V, int64_t k, const hla::Mat& H) {
-    if (k == 0) return;
-    for (int64_t j0 = 0; j0 < b; j0 += kTsRhs) {
-      const int bb = static_cast<int>(std::min<int64_t>(kTsRhs, b - j0));
-      std::vector<double> hh(static_cast<size_t>(k) * bb);
-      for (int j = 0; j < bb; ++j)
-        for (int64_t c = 0; c < k; ++c) hh[static_cast<size_t>(j) * k + c] = H[(j0 + j) * k + c];
-      DevBuf hd(hh.size());
-      hd.upload(hh.data(), hh.size(), s_);
-      const size_t smem = sizeof(double) * static_cast<size_t>(k) * kTsRhs;
-      STKG_REQUIRE(smem <= 200 * 1024, STKG_ARGUMENT, "rksm: Krylov basis too large");
-      static const bool configured = [] {
-        STKG_CUDA_CHECK(cudaFuncSetAttribute(ts_update_kernel<kTsRhs>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        return true;
-      }();
-      (void)configured;
-      ts_update_kernel<kTsRhs><<<kEw, 256, smem, s_>>>(W + j0 * n_, n_, bb, V, static_cast<int>(k), hd.p);
-      STKG_CUDA_CHECK(cudaGetLastError());
-      STKG_CUDA_CHECK(cudaStreamSynchronize(s_));  // hd dies here
-    }
+    if (k == 0 || b == 0) return;
+    double* hd = scratch(kSlotUpd, H.size());
+    double* hp = pinned(H.size());
+    STKG_CUDA_CHECK(cudaStreamSynchronize(s_));  // the pinned staging buffer is reused
+    std::copy(H.begin(), H.end(), hp);
+    STKG_CUDA_CHECK(cudaMemcpyAsync(hd, hp, sizeof(double) * H.size(), cudaMemcpyHostToDevice, s_));
+    update_dev(W, b, V, k, hd);
   }
 
   // out (n x p) = W (n x q) * S (q x p, host column-major)
   void small_gemm(const double* W, int64_t q, const hla::Mat& S, int64_t p, double* out) {
-    DevBuf sd(S.size());
-    sd.upload(S.data(), S.size(), s_);
+    double* sdp = scratch(kSlotGemm, S.size());
+    double* hp = pinned(S.size());
+    STKG_CUDA_CHECK(cudaStreamSynchronize(s_));
+    std::copy(S.begin(), S.end(), hp);
+    STKG_CUDA_CHECK(cudaMemcpyAsync(sdp, hp, sizeof(double) * S.size(), cudaMemcpyHostToDevice, s_));
     GemmProblem g;
     g.M = n_;
     g.K = q;
     g.N = p;
     g.A = W;
     g.lda = n_;
-    g.B = sd.p;
+    g.B = sdp;
     g.ldb = q;
     g.C = out;
     g.ldc = n_;
     launch_gemm(g, EpiStore{}, s_);
-    STKG_CUDA_CHECK(cudaStreamSynchronize(s_));
+    STKG_CUDA_CHECK(cudaGetLastError());
   }
 
   void apply_M(const double* X, double* out, int64_t b) {  // out = M X (column-wise)
@@ -267,24 +309,24 @@ class Rksm {
   void shifted_solve(const double* X, double* out, int64_t b, double sigma) {
     if (h_.ndim == 1) {  // batched tridiagonal solves
       apply_M(X, out, b);
-      DevBuf cp(static_cast<size_t>(n_ * b));
+      double* cp = scratch(kSlotT0, static_cast<size_t>(n_ * b));
       thomas_kernel<<<static_cast<unsigned>(ceil_div(b, 32)), 32, 0, s_>>>(
           h_.m_diag[0].p, h_.m_off[0].p, h_.a_diag[0].p, h_.a_off[0].p, n_, sigma, out,
-          static_cast<int>(b), cp.p);
+          static_cast<int>(b), cp);
       STKG_CUDA_CHECK(cudaGetLastError());
-      STKG_CUDA_CHECK(cudaStreamSynchronize(s_));
       return;
     }
     // tensor eigenbasis: X (Lambda - sigma)^-1 X^T M  (dense)  /  S (Lambda - sigma)^-1 S (P1 DST)
-    DevBuf t0(static_cast<size_t>(n_ * b)), t1(static_cast<size_t>(n_ * b));
+    double* t0 = scratch(kSlotT0, static_cast<size_t>(n_ * b));
+    double* t1 = scratch(kSlotT1, static_cast<size_t>(n_ * b));
     const bool dst = h_.transform == STKG_TRANSFORM_P1_DST;
     const double* src = X;
     if (!dst) {  // X^T M W needs M W; in the sine basis X^T M = diag(mu^1/2) S cancels
-      apply_M(X, t1.p, b);
-      src = t1.p;
+      apply_M(X, t1, b);
+      src = t1;
     }
     for (int a = h_.ndim - 1; a >= 0; --a) {  // forward transforms
-      double* dstp = (src == t0.p) ? t1.p : t0.p;
+      double* dstp = (src == t0) ? t1 : t0;
       axis_pass(h_, a, true, src, dstp, b);
       src = dstp;
     }
@@ -292,11 +334,10 @@ class Rksm {
                                             mode_lambda(h_), sigma);
     STKG_CUDA_CHECK(cudaGetLastError());
     for (int a = 0; a < h_.ndim; ++a) {  // inverse transforms
-      double* dstp = (a == h_.ndim - 1) ? out : (src == t0.p ? t1.p : t0.p);
+      double* dstp = (a == h_.ndim - 1) ? out : (src == t0 ? t1 : t0);
       axis_pass(h_, a, false, src, dstp, b);
       src = dstp;
     }
-    STKG_CUDA_CHECK(cudaStreamSynchronize(s_));
   }
 
   // Rank-revealing orthonormalisation of W (n x b) in place -- the role of
@@ -309,10 +350,10 @@ class Rksm {
   // original column order) = Q^T W_original.
   int orthonormalize(double* W, int64_t b, double tol, hla::Mat* Rout,
                      const double* prev = nullptr, int64_t k_prev = 0) {
-    DevBuf w0;
+    double* w0 = nullptr;
     if (Rout) {
-      w0.alloc(static_cast<size_t>(n_ * b));
-      STKG_CUDA_CHECK(cudaMemcpyAsync(w0.p, W, sizeof(double) * n_ * b, cudaMemcpyDeviceToDevice, s_));
+      w0 = scratch(kSlotW0, static_cast<size_t>(n_ * b));
+      STKG_CUDA_CHECK(cudaMemcpyAsync(w0, W, sizeof(double) * n_ * b, cudaMemcpyDeviceToDevice, s_));
     }
     std::vector<int> orig(b);  // original column index at each position
     for (int64_t j = 0; j < b; ++j) orig[j] = static_cast<int>(j);
@@ -325,7 +366,7 @@ class Rksm {
         maxpiv = std::max(maxpiv, norm0[j]);
       }
     }
-    DevBuf tmp(static_cast<size_t>(n_));
+    double* tmp = scratch(kSlotTmp, static_cast<size_t>(n_));
     int r = 0;
     while (r < b && maxpiv > 0.0) {
       const int64_t m = b - r;
@@ -338,9 +379,9 @@ class Rksm {
       if (p != 0) {  // move the pivot column to position r
         double* a = W + r * n_;
         double* c = W + (r + p) * n_;
-        STKG_CUDA_CHECK(cudaMemcpyAsync(tmp.p, a, sizeof(double) * n_, cudaMemcpyDeviceToDevice, s_));
+        STKG_CUDA_CHECK(cudaMemcpyAsync(tmp, a, sizeof(double) * n_, cudaMemcpyDeviceToDevice, s_));
         STKG_CUDA_CHECK(cudaMemcpyAsync(a, c, sizeof(double) * n_, cudaMemcpyDeviceToDevice, s_));
-        STKG_CUDA_CHECK(cudaMemcpyAsync(c, tmp.p, sizeof(double) * n_, cudaMemcpyDeviceToDevice, s_));
+        STKG_CUDA_CHECK(cudaMemcpyAsync(c, tmp, sizeof(double) * n_, cudaMemcpyDeviceToDevice, s_));
         std::swap(orig[r], orig[r + p]);
       }
       double* q = W + r * n_;
@@ -359,7 +400,7 @@ class Rksm {
     if (Rout) {
       Rout->assign(static_cast<size_t>(std::max(r, 1)) * b, 0.0);
       if (r > 0) {
-        hla::Mat Rt = gram(W, r, w0.p, b);  // r x b, original order
+        hla::Mat Rt = gram(W, r, w0, b);  // r x b, original order
         std::copy(Rt.begin(), Rt.end(), Rout->begin());
       }
     }
@@ -373,9 +414,11 @@ class Rksm {
 
   // Two block classical Gram-Schmidt passes of W (n x b) against V(:, 0:k) (:213)
   void block_gs(double* W, int64_t b, const double* V, int64_t k) {
+    if (k == 0) return;
+    double* hd = scratch(kSlotGs, static_cast<size_t>(k * b));
     for (int pass = 0; pass < 2; ++pass) {
-      hla::Mat H = gram(V, k, W, b);
-      update(W, b, V, k, H);
+      gram_dev(V, k, W, b, hd);
+      update_dev(W, b, V, k, hd);
     }
   }
 
@@ -389,6 +432,11 @@ class Rksm {
   int64_t n_, nt_;
   cudaStream_t s_;
   DevBuf partials_, hdev_, ones_, zeros_;
+  enum { kSlotGram, kSlotUpd, kSlotGemm, kSlotT0, kSlotT1, kSlotW0, kSlotTmp, kSlotGs, kSlotRes,
+         kSlots };
+  DevBuf slots_[kSlots];
+  double* hpin_ = nullptr;
+  size_t hpin_n_ = 0;
 };
 
 // adaptive_next_shift (stk/rksm.hpp:67-102): 200 log-spaced candidates in
@@ -563,14 +611,14 @@ void Rksm::run(int64_t rank, const double* L, const double* R, double* U_left, d
     // --- residual basis: orthonormalise [MV_new, AV_new] against Q and append
     const int64_t q_old = Q.cols;
     {
-      DevBuf w(static_cast<size_t>(n_ * 2 * b));
-      STKG_CUDA_CHECK(cudaMemcpyAsync(w.p, MV.col(k_done), sizeof(double) * n_ * b, cudaMemcpyDeviceToDevice, s_));
-      STKG_CUDA_CHECK(cudaMemcpyAsync(w.p + n_ * b, AV.col(k_done), sizeof(double) * n_ * b, cudaMemcpyDeviceToDevice, s_));
-      block_gs(w.p, 2 * b, Q.col(0), Q.cols);
-      const int add = orthonormalize(w.p, 2 * b, 1e-12, nullptr, Q.col(0), Q.cols);
+      double* wres = scratch(kSlotRes, static_cast<size_t>(n_ * 2 * b));
+      STKG_CUDA_CHECK(cudaMemcpyAsync(wres, MV.col(k_done), sizeof(double) * n_ * b, cudaMemcpyDeviceToDevice, s_));
+      STKG_CUDA_CHECK(cudaMemcpyAsync(wres + n_ * b, AV.col(k_done), sizeof(double) * n_ * b, cudaMemcpyDeviceToDevice, s_));
+      block_gs(wres, 2 * b, Q.col(0), Q.cols);
+      const int add = orthonormalize(wres, 2 * b, 1e-12, nullptr, Q.col(0), Q.cols);
       if (add > 0) {
         Q.reserve(Q.cols + add, s_);
-        STKG_CUDA_CHECK(cudaMemcpyAsync(Q.col(Q.cols), w.p, sizeof(double) * n_ * add, cudaMemcpyDeviceToDevice, s_));
+        STKG_CUDA_CHECK(cudaMemcpyAsync(Q.col(Q.cols), wres, sizeof(double) * n_ * add, cudaMemcpyDeviceToDevice, s_));
         Q.cols += add;
       }
     }

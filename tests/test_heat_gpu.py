@@ -320,19 +320,19 @@ def test_rksm_1d_converges_vs_oracle_and_direct(stk, orc, cuda, n, nt, rank, src
     assert rel(U, Uo) <= 1e-6
 
 
-@pytest.mark.parametrize("transform", ["dense", "dst"])
-def test_rksm_2d_history_vs_oracle(stk, orc, cuda, transform):
+@pytest.mark.parametrize("transform,ndim,n,nt", [("dense", 2, 31, 20), ("dst", 2, 31, 20),
+                                                 ("dense", 3, 15, 12), ("dst", 3, 15, 12)])
+def test_rksm_2d_history_vs_oracle(stk, orc, cuda, transform, ndim, n, nt):
     """2D, fixed_iters (preconditioner mode, stk/rksm.hpp:172,226): per-iteration relative
     residuals and the truncated iterate follow the oracle.  (With real negative poles the
     reference's adaptive rule stalls near 1e-4 on 2D heat loads -- see DESIGN.md -- so
     2D parity is on the history, not on convergence.)"""
-    n, nt = 31, 20
-    L, R = _smooth_load(n, 2, nt)
+    L, R = _smooth_load(n, ndim, nt)
     rng = np.random.default_rng(5)
-    L = np.vstack([L, rng.standard_normal((1, n * n))])
+    L = np.vstack([L, rng.standard_normal((1, n ** ndim))])
     R = np.vstack([R, rng.standard_normal((1, nt))])
-    _, U, rep = _rksm_gpu(stk, 2, n, nt, L, R, transform=transform, fixed_iters=8)
-    Uo, its, hist = _rksm_oracle(orc, 2, n, nt, L, R, fixed_iters=8)
+    _, U, rep = _rksm_gpu(stk, ndim, n, nt, L, R, transform=transform, fixed_iters=8)
+    Uo, its, hist = _rksm_oracle(orc, ndim, n, nt, L, R, fixed_iters=8)
     assert rep.iterations == its == 8 and rep.converged
     np.testing.assert_allclose(rep.rel_res_history, hist, rtol=1e-6)
     assert rel(U, Uo) <= 1e-8
