@@ -20,6 +20,7 @@
 #include <stdexcept>
 #include <string>
 #include <utility>
+#include <ostream>
 #include <vector>
 
 #include "stk_gpu.h"
@@ -229,6 +230,11 @@ class HeatPlan {
     return U;
   }
   void apply(const double* U_dev, double* out_dev) { check(stkg_heat_apply(h_, U_dev, out_dev)); }
+  // F = L R^T given as device factors (L: N_h x r, R: N_t x r, column-major): U (N_h x N_t).
+  void solve_factored(int64_t rank, const double* L_dev, const double* R_dev, double* U_dev) {
+    check(stkg_heat_solve_factored(h_, rank, L_dev, R_dev, U_dev));
+  }
+  stkg_heat* handle() { return h_; }
   double residual(const double* U_dev, const double* F_dev, double* fnorm = nullptr) {
     double rel = 0.0, fn = 0.0;
     check(stkg_heat_residual(h_, U_dev, F_dev, &rel, &fn));
@@ -267,6 +273,13 @@ struct SolveReport {  // stk/report.hpp:11-20
   bool stagnated = false;
 };
 
+// write_history_csv (stk/report.hpp:22-26)
+inline void write_history_csv(std::ostream& os, const SolveReport& report) {
+  os << "iter,relres\n";
+  for (size_t i = 0; i < report.rel_res_history.size(); ++i)
+    os << i + 1 << "," << report.rel_res_history[i] << "\n";
+}
+
 namespace detail {
 inline SolveReport to_report(const stkg_report& r, std::vector<double>& hist) {
   SolveReport out;
@@ -281,6 +294,43 @@ inline SolveReport to_report(const stkg_report& r, std::vector<double>& hist) {
   return out;
 }
 }  // namespace detail
+
+// rksm_solve (stk/rksm.hpp:104-234) on a HeatPlan built with the spatial factors.
+struct RksmOptions {
+  double tol = 1e-8;
+  int maxit = 100;
+  int fixed_iters = 0;  // > 0: preconditioner mode (exactly that many expansions)
+  double trunc_tol = 1e-10;
+};
+
+// Device low-rank factors U = left * right^T (left: N_h x rank, right: N_t x rank).
+struct LowRankDev {
+  DeviceBuffer left, right;
+  int64_t rank = 0;
+};
+
+inline LowRankDev rksm_solve(HeatPlan& plan, int64_t rank, const double* L_dev,
+                             const double* R_dev, const RksmOptions& opts = {},
+                             SolveReport* report = nullptr) {
+  const int64_t cap = std::max<int64_t>(
+      1, std::min<int64_t>(std::min(plan.space_dim(), plan.time_dim()),
+                           rank * (std::max(opts.maxit, opts.fixed_iters) + 1)));
+  LowRankDev out;
+  out.left = DeviceBuffer(static_cast<size_t>(cap * plan.space_dim()));
+  out.right = DeviceBuffer(static_cast<size_t>(cap * plan.time_dim()));
+  stkg_rksm_options o{opts.tol, opts.maxit, opts.fixed_iters, opts.trunc_tol};
+  std::vector<double> hist(static_cast<size_t>(std::max(opts.maxit, opts.fixed_iters) + 1));
+  stkg_report rep{};
+  rep.rel_res_history = hist.data();
+  rep.history_capacity = static_cast<int>(hist.size());
+  check(stkg_heat_rksm(plan.handle(), rank, L_dev, R_dev, &o, out.left.data(), out.right.data(),
+                       cap, &out.rank, &rep));
+  if (report) {
+    *report = detail::to_report(rep, hist);
+    report->rank = static_cast<int>(out.rank);
+  }
+  return out;
+}
 
 class WavePlan {
  public:

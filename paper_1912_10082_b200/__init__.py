@@ -14,5 +14,7 @@ from .errors import (ArgumentError, CudaError, DefinitenessError, NumericError,
                      SingularityError, SolvabilityError, StkError)
 from .heat import HeatKronOp, HeatPlan, TensorEigPair, heat_kron_op, solve_projected_heat_with
 from .wave import (GmresConfig, SolveReport, TwoTermPrecond, WaveOperator, WavePlan, gmres)
+from . import formats  # noqa: E402
+from .formats import ResultRow, read_matrix_market, write_history_csv, write_matrix_market
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -4,6 +4,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <random>
+#include <sstream>
 #include <string>
 #include <vector>
 
@@ -64,6 +65,33 @@ int main() {
     EXPECT(rr < 1e-12 && fn > 0);
     auto Uh = plan.solve_host(F);
     EXPECT(rel(Uh, dU.download()) == 0.0);
+  }
+  // rksm_solve: 1D, N_h=10, N_t=6, rank-1 F -> relres <= 1e-8, U matches the
+  // direct solve to 1e-6
+  {
+    const int n = 10, nt = 6;
+    auto [M, A] = fem1d_matrices(0.0, 1.0, n);
+    auto [Dt, Ct] = heat_time_matrices(nt, 1.0);
+    std::vector<Tridiagonal> ms{M}, as{A};
+    HeatPlan plan({p1_eigpair(0.0, 1.0, n)}, Dt, Ct, &ms, &as);
+    std::vector<double> l(n), r(nt);
+    for (int i = 0; i < n; ++i) l[i] = std::sin(0.3 * i + 0.1);
+    for (int j = 0; j < nt; ++j) r[j] = 1.0 + 0.5 * j;
+    DeviceBuffer dl(l), dr(r), dU(static_cast<size_t>(n) * nt);
+    SolveReport rep;
+    LowRankDev u = rksm_solve(plan, 1, dl.data(), dr.data(), RksmOptions{}, &rep);
+    EXPECT(rep.converged && rep.final_relres <= 1e-8 && u.rank >= 1);
+    EXPECT(static_cast<int>(rep.rel_res_history.size()) == rep.iterations);
+    std::ostringstream hist;
+    write_history_csv(hist, rep);
+    EXPECT(hist.str().rfind("iter,relres\n1,", 0) == 0);
+    plan.solve_factored(1, dl.data(), dr.data(), dU.data());
+    std::vector<double> ud = dU.download(), L = u.left.download(), R = u.right.download();
+    std::vector<double> ur(ud.size(), 0.0);  // U (N_h x N_t) = left right^T
+    for (int64_t c = 0; c < u.rank; ++c)
+      for (int j = 0; j < nt; ++j)
+        for (int i = 0; i < n; ++i) ur[static_cast<size_t>(j) * n + i] += L[c * n + i] * R[c * nt + j];
+    EXPECT(rel(ur, ud) <= 1e-6);
   }
   // SingularityError (stk/sylvester.hpp:133-135)
   {
