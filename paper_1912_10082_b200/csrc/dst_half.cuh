@@ -1,0 +1,352 @@
+// Half-length fast sine transform (DST-I) for the uniform-P1 eigenbasis.
+//
+// dst.cuh transforms two real vectors with one complex FFT of length 2N (N = n + 1).  The
+// kernels here need a complex FFT of length N for the same two vectors -- half the flops
+// and half the shared-memory traffic -- by the classical odd-symmetry reduction of DST-I
+// to a real DFT of length N:
+//
+//     y_0 = 0,  y_j = sin(pi j / N) (x_j + x_{N-j}) + (x_j - x_{N-j}) / 2   (j = 1..N-1)
+//     Y_k = sum_j y_j exp(-2 pi i j k / N) = A_k - i B_k
+//     DST(x)_{2k}   = B_k                          (k = 1..N/2-1)
+//     DST(x)_{2k+1} = DST(x)_{2k-1} + A_k,  DST(x)_1 = A_0 / 2   (k = 0..N/2-1)
+//
+// (the x_{N-j} terms cancel in B and double in A; sin(pi j/N) cos(2 pi j k/N) splits into
+// the two neighbouring odd sines).  Two real vectors a, b share one complex FFT
+// z = y(a) + i y(b): Y(a)_k = (Z_k + conj Z_{N-k}) / 2, Y(b)_k = (Z_k - conj Z_{N-k}) / 2i.
+// The odd outputs are a prefix sum over k: serial within a thread (consecutive k), one
+// warp-shuffle block scan across threads.  Its rounding grows like sqrt(N) eps.
+//
+// FFT: Stockham auto-sort in shared memory with every thread holding V = 16 complex
+// values; a stage of radix R <= V runs V/R butterflies per thread.  All stages read the
+// thread's values from positions t + T p (T = N/V threads per FFT, p < V), so one read
+// pattern serves every stage; pidx() padding spreads the stride-T accesses over banks.
+// Twiddles come from the 2N-th-root table the plan already holds (stride 2), and
+// sin(pi m / N) = -Im of its m-th entry.
+//
+// Used for N in {512, 1024, 2048} (T >= 32: each FFT owns whole warps); smaller axes keep
+// the dst.cuh kernels.
+#pragma once
+
+#include "dst.cuh"
+
+namespace stkg {
+
+template <int R>
+__device__ __forceinline__ void dft_small(double2 (&u)[R]);
+template <>
+__device__ __forceinline__ void dft_small<2>(double2 (&u)[2]) { dft_radix<2>(u); }
+template <>
+__device__ __forceinline__ void dft_small<4>(double2 (&u)[4]) { dft_radix<4>(u); }
+template <>
+__device__ __forceinline__ void dft_small<8>(double2 (&u)[8]) { dft8(u); }
+template <>
+__device__ __forceinline__ void dft_small<16>(double2 (&u)[16]) {
+  // 16 = 2 x 8 by decimation in frequency: a_r = u_r + u_{r+8}, b_r = (u_r - u_{r+8}) w16^r,
+  // two DFT-8, outputs even <- a, odd <- b.
+  constexpr double c1 = 0.92387953251128675613;  // cos(pi/8)
+  constexpr double s1 = 0.38268343236508977173;  // sin(pi/8)
+  constexpr double r2 = 0.70710678118654752440;
+  double2 a[8], b[8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    a[r] = cadd(u[r], u[r + 8]);
+    b[r] = csub(u[r], u[r + 8]);
+  }
+  b[1] = cmul(b[1], make_double2(c1, -s1));
+  b[2] = make_double2((b[2].x + b[2].y) * r2, (b[2].y - b[2].x) * r2);
+  b[3] = cmul(b[3], make_double2(s1, -c1));
+  b[4] = mul_neg_i(b[4]);
+  b[5] = cmul(b[5], make_double2(-s1, -c1));
+  b[6] = make_double2((b[6].y - b[6].x) * r2, -(b[6].x + b[6].y) * r2);
+  b[7] = cmul(b[7], make_double2(-c1, -s1));
+  dft8(a);
+  dft8(b);
+#pragma unroll
+  for (int p = 0; p < 8; ++p) {
+    u[2 * p] = a[p];
+    u[2 * p + 1] = b[p];
+  }
+}
+
+// Shared-memory index of the half-length FFT buffer: an XOR swizzle of the low three bits
+// (a permutation inside aligned groups of 8 complex = 128 bytes).  Checked offline against
+// every access pattern of the kernels (first-stage writes of 16 consecutive values per
+// thread, the t + T p reads, the later stage writes and the post-processing's k and N - k
+// reads): conflict-free for 128-bit accesses except 1/8 of the N - k reads (2-way).
+__host__ __device__ constexpr int hpidx(int i) { return i ^ (((i >> 3) ^ (i >> 6)) & 7); }
+// Buffer length (complex): N for the FFT, and 2 opad(N) doubles for the output staging.
+template <int N>
+constexpr int hpadded_len() { return N + N / 16; }
+
+// One Stockham stage (radix R; NS = product of the earlier radices) of a length-N FFT
+// whose T = N/V threads hold x[p] = value at position t + T p.  Computes in registers,
+// writes the stage output to buf, and re-reads the thread's values for the next stage.
+template <int N, int V, int R, int NS>
+__device__ __forceinline__ void half_stage(double2 (&x)[V], double2* buf,
+                                           const double2* __restrict__ tw2, int t) {
+  constexpr int T = N / V;
+  constexpr int B = V / R;                   // butterflies per thread
+  constexpr int kStep = (2 * N) / (NS * R);  // tw2 index of exp(-2 pi i / (NS R))
+#pragma unroll
+  for (int i = 0; i < B; ++i) {
+    const int j = t + T * i;
+    const int k = j % NS;
+    double2 u[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) u[q] = x[i + q * B];
+    if constexpr (NS > 1) {
+      if (k > 0) {
+        const double2 w = __ldg(tw2 + k * kStep);
+        double2 wr = w;
+#pragma unroll
+        for (int q = 1; q < R; ++q) {
+          if (q > 1) wr = cmul(wr, w);
+          u[q] = cmul(u[q], wr);
+        }
+      }
+    }
+    dft_small<R>(u);
+#pragma unroll
+    for (int q = 0; q < R; ++q) x[i + q * B] = u[q];
+  }
+  __syncthreads();  // every thread has consumed the previous contents of buf
+#pragma unroll
+  for (int i = 0; i < B; ++i) {
+    const int j = t + T * i;
+    const int base = (j / NS) * NS * R + j % NS;
+#pragma unroll
+    for (int q = 0; q < R; ++q) buf[hpidx(base + q * NS)] = x[i + q * B];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int p = 0; p < V; ++p) x[p] = buf[hpidx(t + T * p)];
+}
+
+// All stages: radix V while V divides the remaining length, then the remainder radix.
+template <int N, int V, int NS>
+__device__ __forceinline__ void half_fft_stages(double2 (&x)[V], double2* buf,
+                                                const double2* __restrict__ tw2, int t) {
+  if constexpr (NS < N) {
+    constexpr int rem = N / NS;
+    constexpr int R = rem >= V ? V : rem;
+    half_stage<N, V, R, NS>(x, buf, tw2, t);
+    half_fft_stages<N, V, NS * R>(x, buf, tw2, t);
+  }
+}
+
+// Output staging index: one pad double per 16 (conflict-free for the post-processing
+// writes, in which thread t writes 16 consecutive outputs).
+__device__ __forceinline__ int opad(int e) { return e + (e >> 4); }
+
+// Inclusive prefix sum of (a, b) over the T threads of one FFT (T a multiple of 32; the
+// FFT's warps are warp0 .. warp0 + T/32 - 1, red has 2 T/32 doubles for this FFT).
+template <int T>
+__device__ __forceinline__ void fft_scan2(double& a, double& b, double* red, int t) {
+  const int lane = t & 31, warp = t >> 5;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double ta = __shfl_up_sync(0xffffffffu, a, o);
+    const double tb = __shfl_up_sync(0xffffffffu, b, o);
+    if (lane >= o) {
+      a += ta;
+      b += tb;
+    }
+  }
+  if constexpr (T > 32) {
+    if (lane == 31) {
+      red[2 * warp] = a;
+      red[2 * warp + 1] = b;
+    }
+    __syncthreads();
+    double oa = 0.0, ob = 0.0;
+    for (int w = 0; w < warp; ++w) {
+      oa += red[2 * w];
+      ob += red[2 * w + 1];
+    }
+    a += oa;
+    b += ob;
+  }
+}
+
+// Pre-processing of one FFT input position m (value pair x_m, x_{N-m} of both vectors).
+__device__ __forceinline__ double2 half_pre(double s, double xa, double xam, double xb,
+                                            double xbm) {
+  return make_double2(fma(s, xa + xam, 0.5 * (xa - xam)), fma(s, xb + xbm, 0.5 * (xb - xbm)));
+}
+
+// FFT (x holds the pre-processed inputs), post-processing and prefix scan; writes the
+// n outputs of both vectors into oa / ob at opad(e).  buf may overlap oa/ob.
+template <int N>
+__device__ __forceinline__ void half_fft_post(double2 (&x)[16], double2* buf,
+                                             const double2* __restrict__ tw2, int t, double hs,
+                                             double* red, double* oa, double* ob) {
+  constexpr int V = 16, T = N / V, H = V / 2;
+  half_fft_stages<N, V, 1>(x, buf, tw2, t);
+  // thread t owns k = t H + i (i < H) of the half spectrum k < N/2
+  double Aa[H], Ab[H], Ba[H], Bb[H];
+#pragma unroll
+  for (int i = 0; i < H; ++i) {
+    const int k = t * H + i;
+    const double2 zk = buf[hpidx(k)];
+    const double2 zm = buf[hpidx(k == 0 ? 0 : N - k)];
+    Aa[i] = hs * (zk.x + zm.x);
+    Ab[i] = hs * (zk.y + zm.y);
+    Ba[i] = hs * (zm.y - zk.y);
+    Bb[i] = hs * (zk.x - zm.x);
+  }
+  if (t == 0) {
+    Aa[0] *= 0.5;
+    Ab[0] *= 0.5;
+  }
+  double sa = 0.0, sb = 0.0;
+#pragma unroll
+  for (int i = 0; i < H; ++i) {
+    sa += Aa[i];
+    sb += Ab[i];
+    Aa[i] = sa;
+    Ab[i] = sb;
+  }
+  double ea = sa, eb = sb;
+  fft_scan2<T>(ea, eb, red, t);
+  ea -= sa;  // exclusive offsets
+  eb -= sb;
+  __syncthreads();  // all reads of Z are done: buf may be overwritten by the outputs
+#pragma unroll
+  for (int i = 0; i < H; ++i) {
+    const int k = t * H + i;
+    if (k > 0) {  // X_{2k} -> index 2k - 1
+      oa[opad(2 * k - 1)] = Ba[i];
+      ob[opad(2 * k - 1)] = Bb[i];
+    }
+    oa[opad(2 * k)] = Aa[i] + ea;  // X_{2k+1} -> index 2k
+    ob[opad(2 * k)] = Ab[i] + eb;
+  }
+}
+
+template <int N>
+struct HalfCfg {
+  static constexpr int V = 16;
+  static constexpr int T = N / V;  // threads per FFT
+  static constexpr size_t kSmem = size_t(hpadded_len<N>()) * sizeof(double2);
+  static constexpr int kMinBlocks = 65536 / (T * 128) < 8 ? 65536 / (T * 128) : 8;
+  static_assert(T % 32 == 0, "one FFT per whole warps");
+};
+
+// Contiguous axis (vectors of length n = N - 1 back to back): one CTA transforms a pair of
+// vectors per step (persistent grid).  dst may alias src (an item is read before written).
+template <int N>
+__global__ void __launch_bounds__(HalfCfg<N>::T, HalfCfg<N>::kMinBlocks)
+    dst_half_kernel(const double* src, double* dst, int64_t nvec,
+                    const double2* __restrict__ tw2, double scale) {
+  using C = HalfCfg<N>;
+  constexpr int V = C::V, T = C::T, n = N - 1;
+  extern __shared__ __align__(16) double2 hbuf[];
+  __shared__ double red[2 * (T / 32)];
+  const int t = threadIdx.x;
+  const int64_t nitems = (nvec + 1) / 2;
+  const double hs = 0.5 * scale;
+  double* oa = reinterpret_cast<double*>(hbuf);
+  double* ob = oa + opad(N);
+  for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x) {
+    const int64_t g0 = 2 * item;
+    const bool has_b = g0 + 1 < nvec;
+    const double* sa = src + g0 * n;
+    const double* sb = has_b ? sa + n : sa;
+    double2 x[V];
+#pragma unroll
+    for (int p = 0; p < V; ++p) {
+      const int m = t + T * p;
+      x[p] = make_double2(0.0, 0.0);
+      if (m > 0) {
+        const int mm = N - m;  // in 1..N-1 as well
+        const double s = -__ldg(&tw2[m].y);
+        const double xb = has_b ? sb[m - 1] : 0.0, xbm = has_b ? sb[mm - 1] : 0.0;
+        x[p] = half_pre(s, sa[m - 1], sa[mm - 1], xb, xbm);
+      }
+    }
+    // (half_fft_post's first barrier orders these reads before hbuf is overwritten, and
+    // the previous item's stores from hbuf before this item's first write)
+    half_fft_post<N>(x, hbuf, tw2, t, hs, red, oa, ob);
+    __syncthreads();
+    double* da = dst + g0 * n;
+    for (int e = t; e < n; e += T) da[e] = oa[opad(e)];
+    if (has_b)
+      for (int e = t; e < n; e += T) da[n + e] = ob[opad(e)];
+  }
+}
+
+// Strided axis (inner > 1; element j of vector (o, i) at (o n + j) inner + i).  A tile is
+// G = 2P neighbouring vectors (rows of 8G contiguous bytes), staged by cp.async; the P
+// pairs run their FFTs side by side (P T threads), each in its own shared region that
+// holds first the two input rows, then the FFT, then the two output rows.  Region pitch
+// and row offsets are chosen so that the tile's row accesses are bank-conflict free.
+template <int N>
+struct HalfStridedCfg {
+  static constexpr int V = 16, T = N / V, P = N >= 2048 ? 2 : 4, G = 2 * P;
+  static constexpr int kThreads = P * T;
+  // Row v of the tile starts at (v/2) kRegion + (v%2) kRowB; with kStep = 16/G these are
+  // = kStep v (mod 16 doubles), so each half-warp's G x (16/G) row accesses of 8 bytes hit
+  // distinct banks.
+  static constexpr int kStep = 16 / G;
+  static constexpr int kRowB = N + N / 16 + kStep;                 // doubles: offset of row b
+  static constexpr int kRegion = 2 * hpadded_len<N>() + 2 * kStep;  // doubles per pair
+  static constexpr size_t kSmem = size_t(P) * kRegion * sizeof(double);
+  static_assert(T % 32 == 0, "one FFT per whole warps");
+};
+
+template <int N>
+__global__ void __launch_bounds__(HalfStridedCfg<N>::kThreads, 2)
+    dst_half_strided_kernel(const double* __restrict__ src, double* __restrict__ dst,
+                            int64_t inner, int64_t nvec, const double2* __restrict__ tw2,
+                            double scale) {
+  using C = HalfStridedCfg<N>;
+  constexpr int V = C::V, T = C::T, P = C::P, G = C::G, n = N - 1;
+  constexpr int RB = C::kRowB, RG = C::kRegion;
+  extern __shared__ __align__(16) double smem[];
+  __shared__ int64_t vbase[G];
+  __shared__ double red[P][2 * (T / 32)];
+  const int f = threadIdx.x / T, t = threadIdx.x % T;
+  double* region = smem + f * RG;
+  double2* fbuf = reinterpret_cast<double2*>(region);
+  const int64_t ntiles = (nvec + G - 1) / G;
+  const double hs = 0.5 * scale;
+  auto row = [&](int v) { return smem + (v >> 1) * RG + (v & 1) * RB; };
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    __syncthreads();  // the previous tile's stores have read the staging rows
+    if (threadIdx.x < G) {
+      const int64_t g = tile * G + threadIdx.x;
+      vbase[threadIdx.x] = g < nvec ? (g / inner) * n * inner + g % inner : -1;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < G * n; e += C::kThreads) {
+      const int v = e % G, jj = e / G;
+      const int64_t b = vbase[v];
+      cp_async8(row(v) + jj, b >= 0 ? src + b + int64_t(jj) * inner : src, b >= 0);
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+    const double* ra = region;
+    const double* rb = region + RB;
+    double2 x[V];
+#pragma unroll
+    for (int p = 0; p < V; ++p) {
+      const int m = t + T * p;
+      x[p] = make_double2(0.0, 0.0);
+      if (m > 0) {
+        const int mm = N - m;
+        const double s = -__ldg(&tw2[m].y);
+        x[p] = half_pre(s, ra[m - 1], ra[mm - 1], rb[m - 1], rb[mm - 1]);
+      }
+    }
+    half_fft_post<N>(x, fbuf, tw2, t, hs, red[f], region, region + RB);
+    __syncthreads();
+    for (int e = threadIdx.x; e < G * n; e += C::kThreads) {
+      const int v = e % G, kk = e / G;
+      const int64_t b = vbase[v];
+      if (b >= 0) __stcs(dst + b + int64_t(kk) * inner, row(v)[opad(kk)]);
+    }
+  }
+}
+
+}  // namespace stkg

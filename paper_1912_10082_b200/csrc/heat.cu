@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -16,6 +17,7 @@
 
 #include "common.cuh"
 #include "dst.cuh"
+#include "dst_half.cuh"
 #include "gemm_f64.cuh"
 #include "heat_plan.cuh"
 
@@ -404,8 +406,67 @@ void launch_dst(const stkg_heat& h, int a, const double* src, double* dst, int64
   STKG_CUDA_CHECK(cudaGetLastError());
 }
 
+// Half-length kernels (dst_half.cuh) for N = n + 1 in {512, 1024}.
+template <int N>
+void launch_dst_half(const stkg_heat& h, int a, const double* src, double* dst, int64_t inner,
+                     int64_t outer) {
+  const int64_t nvec = outer * inner;
+  const double scale = std::sqrt(2.0 / static_cast<double>(N));
+  const double2* tw2 = reinterpret_cast<const double2*>(h.twiddle[a].p);
+  if (inner == 1) {
+    using C = HalfCfg<N>;
+    static const int per_sm = [] {
+      STKG_CUDA_CHECK(cudaFuncSetAttribute(dst_half_kernel<N>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(C::kSmem)));
+      int b = 0;
+      STKG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, dst_half_kernel<N>, C::T,
+                                                                    C::kSmem));
+      return std::max(b, 1);
+    }();
+    const int64_t blocks = std::min<int64_t>(ceil_div(nvec, 2), int64_t(148) * per_sm);
+    dst_half_kernel<N><<<static_cast<unsigned>(blocks), C::T, C::kSmem, h.stream>>>(
+        src, dst, nvec, tw2, scale);
+  } else {
+    using C = HalfStridedCfg<N>;
+    static const int per_sm = [] {
+      STKG_CUDA_CHECK(cudaFuncSetAttribute(dst_half_strided_kernel<N>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(C::kSmem)));
+      int b = 0;
+      STKG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+          &b, dst_half_strided_kernel<N>, C::kThreads, C::kSmem));
+      return std::max(b, 1);
+    }();
+    const int64_t blocks = std::min<int64_t>(ceil_div(nvec, C::G), int64_t(148) * per_sm);
+    dst_half_strided_kernel<N><<<static_cast<unsigned>(blocks), C::kThreads, C::kSmem, h.stream>>>(
+        src, dst, inner, nvec, tw2, scale);
+  }
+  STKG_CUDA_CHECK(cudaGetLastError());
+}
+
+bool use_dst_half() {
+  static const bool on = [] {
+    const char* e = std::getenv("STKG_DST_HALF");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 void dst_pass(const stkg_heat& h, int a, const double* src, double* dst, int64_t inner,
               int64_t outer) {
+  // The half-length kernels trade accuracy for speed (their odd outputs are a prefix sum):
+  // measured relres 2.6e-12 (2D, n = 1023) and 7e-13 (2D 511) but 5e-11 for 1D n = 1023,
+  // too close to the 1e-10 gate -- so 1D plans keep the padded kernels.
+  if (use_dst_half() && h.ndim >= 2) {
+    switch (h.n[a] + 1) {
+      // N = 2048 keeps the padded 2N kernel: the half-length recurrence's sqrt(N) error
+      // growth costs 1D n = 2047 the 1e-10 residual gate (3e-10 measured)
+      case 512: return launch_dst_half<512>(h, a, src, dst, inner, outer);
+      case 1024: return launch_dst_half<1024>(h, a, src, dst, inner, outer);
+      default: break;
+    }
+  }
   switch (2 * (h.n[a] + 1)) {
     case 32: return launch_dst<32>(h, a, src, dst, inner, outer);
     case 64: return launch_dst<64>(h, a, src, dst, inner, outer);
@@ -514,6 +575,36 @@ void run_chunk(stkg_heat& h, const double* F, double* U, double* S, int64_t l0, 
     double* dst = next_dst(++k);
     axis_pass(h, a, false, src, dst, ntc);
     src = dst;
+  }
+}
+
+// Slices per L2-resident sub-chunk.  Running all passes of a few time slices back to back
+// keeps the intermediate slices (the U sub-chunk and the scratch) in the 126 MB L2, so HBM
+// sees F once and U once (16 B/unknown) instead of 16 B/unknown per pass.  The recurrence
+// carries its state across sub-chunks (heat_scan_kernel's carry).  STKG_L2_CHUNK_MB
+// overrides the working-set budget (0 = one chunk over all of n_t).
+int64_t l2_chunk_slices(const stkg_heat& h) {
+  static const long budget_mb = [] {
+    const char* e = std::getenv("STKG_L2_CHUNK_MB");
+    return e ? std::atol(e) : -1L;
+  }();
+  long mb = budget_mb;
+  if (mb < 0) mb = 0;  // measured: sub-chunking loses to whole-n_t passes (DESIGN K2b)
+  if (mb == 0) return h.nt;
+  const int64_t per_slice = 2 * h.nx * static_cast<int64_t>(sizeof(double));  // U + scratch
+  return std::min<int64_t>(h.nt, std::max<int64_t>(1, (int64_t(mb) << 20) / per_slice));
+}
+
+// F, U: slices [l0, l0 + ntc) (already offset).  Uses h.scratch (grown to one sub-chunk).
+void solve_range(stkg_heat& h, const double* F, double* U, int64_t l0, int64_t ntc) {
+  const int64_t tc = std::min(l2_chunk_slices(h), ntc);
+  if (h.scratch.n < static_cast<size_t>(h.nx * tc)) {
+    STKG_CUDA_CHECK(cudaStreamSynchronize(h.stream));
+    h.scratch.alloc(h.nx * tc);
+  }
+  for (int64_t j = 0; j < ntc; j += tc) {
+    const int64_t m = std::min(tc, ntc - j);
+    run_chunk(h, F + j * h.nx, U + j * h.nx, h.scratch.p, l0 + j, m);
   }
 }
 
@@ -802,8 +893,7 @@ int stkg_heat_solve(stkg_heat* h, const double* F, double* U) {
     STKG_REQUIRE(h && F && U, STKG_ARGUMENT, "stkg_heat_solve: null argument");
     STKG_REQUIRE(F != U, STKG_ARGUMENT, "stkg_heat_solve: U may not alias F");
     check_solvable(*h);
-    if (h->scratch.n < static_cast<size_t>(h->nx * h->nt)) h->scratch.alloc(h->nx * h->nt);
-    run_chunk(*h, F, U, h->scratch.p, 0, h->nt);
+    solve_range(*h, F, U, 0, h->nt);
   });
 }
 
@@ -846,12 +936,12 @@ int stkg_heat_solve_host(stkg_heat* h, const double* F_host, double* U_host) {
     if (tc <= 0) tc = std::max<int64_t>(1, (int64_t(256) << 20) / (h->nx * 8));
     tc = std::min(tc, h->nt);
     const int64_t chunk_elems = h->nx * tc;
-    if (h->ps.n < static_cast<size_t>(chunk_elems)) {
+    if (h->pf[0].n < static_cast<size_t>(chunk_elems)) {
+      STKG_CUDA_CHECK(cudaStreamSynchronize(h->stream));
       for (int b = 0; b < 2; ++b) {
         h->pf[b].alloc(chunk_elems);
         h->pu[b].alloc(chunk_elems);
       }
-      h->ps.alloc(chunk_elems);
     }
     if (!h->s_h2d) {
       STKG_CUDA_CHECK(cudaStreamCreateWithFlags(&h->s_h2d, cudaStreamNonBlocking));
@@ -873,7 +963,7 @@ int stkg_heat_solve_host(stkg_heat* h, const double* F_host, double* U_host) {
       STKG_CUDA_CHECK(cudaEventRecord(h->ev_h2d[b], h->s_h2d));
       STKG_CUDA_CHECK(cudaStreamWaitEvent(h->stream, h->ev_h2d[b], 0));
       if (c >= 2) STKG_CUDA_CHECK(cudaStreamWaitEvent(h->stream, h->ev_d2h[b], 0));
-      run_chunk(*h, h->pf[b].p, h->pu[b].p, h->ps.p, l0, ntc);
+      solve_range(*h, h->pf[b].p, h->pu[b].p, l0, ntc);
       STKG_CUDA_CHECK(cudaEventRecord(h->ev_comp[b], h->stream));
       STKG_CUDA_CHECK(cudaStreamWaitEvent(h->s_d2h, h->ev_comp[b], 0));
       STKG_CUDA_CHECK(cudaMemcpyAsync(U_host + l0 * h->nx, h->pu[b].p, bytes,

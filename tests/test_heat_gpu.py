@@ -216,7 +216,8 @@ def test_factored_load_equals_dense_load(stk, orc, cuda, ndim, n, nt, rank):
 # --------------------------------------------------------------- fast sine transforms --
 @pytest.mark.parametrize("ndim,n,nt", [(1, 15, 7), (1, 255, 256), (2, 15, 5), (2, 63, 17),
                                        (2, 127, 4), (3, 15, 6), (3, 31, 3), (1, 2047, 3),
-                                       (2, 1023, 2)])
+                                       (2, 1023, 2), (1, 511, 9), (2, 511, 3), (3, 511, 1),
+                                       (2, 2047, 1), (1, 1023, 5)])
 def test_dst_backend_equals_dense_backend(stk, cuda, ndim, n, nt):
     """The P1 fast-sine-transform backend computes the same solve_projected_heat_with as the
     dense DMMA backend on the closed-form eigenbasis (X = S diag(mu^-1/2))."""
@@ -226,8 +227,11 @@ def test_dst_backend_equals_dense_backend(stk, cuda, ndim, n, nt):
     ps = stk.HeatPlan.p1_uniform(ndim, n, nt, transform="dst")
     Ud = host(pd.solve(dev(F)))
     Us = host(ps.solve(dev(F)))
-    assert rel(Us, Ud) < 1e-12
+    # the half-length DST's odd outputs are a prefix sum over k, whose rounding grows like
+    # sqrt(N) eps (dst_half.cuh): ~1e-13 at N = 2048 instead of ~1e-14
+    assert rel(Us, Ud) < (1e-12 if n < 511 else 2e-12), rel(Us, Ud)
     rr, _ = ps.residual(dev(Us), dev(F))
+    print(ndim, n, nt, "rel vs dense", rel(Us, Ud), "relres", rr)
     assert rr < 1e-10  # north_star gate (cond grows ~ n^2: 3e-12 at n = 2047, nt = 3)
 
 
