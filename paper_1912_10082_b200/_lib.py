@@ -7,6 +7,7 @@ is built in-tree with nvcc; if that fails, importing this module raises.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 from . import build as _build
@@ -126,9 +127,13 @@ SIGNATURES = {
 
 
 def _load():
-    if _build.needs_build():
-        _build.build()
-    lib = C.CDLL(str(_LIB_PATH))
+    override = os.environ.get("STKG_LIB_PATH")  # A/B runs of an alternative in-tree build
+    if override:
+        lib = C.CDLL(override)
+    else:
+        if _build.needs_build():
+            _build.build()
+        lib = C.CDLL(str(_LIB_PATH))
     for name, (res, args) in SIGNATURES.items():
         fn = getattr(lib, name)  # AttributeError => the ABI is incomplete: fail loudly
         fn.restype = res
