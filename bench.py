@@ -222,11 +222,18 @@ def _timed_path(stk, inputs, cfg, transform, args, stream, barrier, F, U, with_c
     else:
         bytes_launch = 16.0 * N  # read + write each unknown once per axis pass
         achieved = bytes_launch / (t_ms / t_n / 1e3) / 1e9
-        L = 2 * (cfg.n + 1)
+        # which sine-transform kernels the plan runs (heat.cu::dst_pass)
+        half = (cfg.ndim >= 2 and cfg.n + 1 in (512, 1024)
+                and os.environ.get("STKG_DST_HALF", "1") != "0")
+        L = (cfg.n + 1) if half else 2 * (cfg.n + 1)  # complex FFT length per vector pair
         fft_flops = 5.0 * L * np.log2(L) / 2.0 / cfg.n  # per element and axis pass
-        roof = {"bound": "hbm", "kernel": "dst_axis_kernel (FP64 Stockham FFT sine transform)",
+        kname = ("dst_half_kernel / dst_half_strided_kernel (FP64 half-length DST-I: "
+                 "N-point Stockham FFT per vector pair)") if half else \
+            "dst_axis_kernel / dst_strided_kernel (FP64 padded 2N-point FFT DST-I)"
+        roof = {"bound": "hbm", "kernel": kname,
                 "achieved": achieved, "peak": HBM_GBS, "unit": "GB/s",
-                "frac": achieved / HBM_GBS, "traffic": traffic_from_profiles("dst"),
+                "frac": achieved / HBM_GBS,
+                "traffic": traffic_from_profiles("dst_half" if half else "dst"),
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs",
                 "flop_per_unknown_per_pass": fft_flops,
                 "whole_solve_frac": ((2 * cfg.ndim + 1) * 16.0 * N * args.steps / (ms / 1e3) / 1e9)
