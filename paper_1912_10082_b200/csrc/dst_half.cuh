@@ -68,6 +68,17 @@ __device__ __forceinline__ void dft_small<16>(double2 (&u)[16]) {
   }
 }
 
+// Barrier over the threads of one FFT: a warp barrier when the FFT is exactly one warp
+// (its shared region is private to that warp), else a CTA barrier.
+template <int T>
+__device__ __forceinline__ void fft_sync() {
+  if constexpr (T == 32) {
+    __syncwarp();
+  } else {
+    __syncthreads();
+  }
+}
+
 // Shared-memory index of the half-length FFT buffer: an XOR swizzle of the low three bits
 // (a permutation inside aligned groups of 8 complex = 128 bytes).  Checked offline against
 // every access pattern of the kernels (first-stage writes of 16 consecutive values per
@@ -109,7 +120,7 @@ __device__ __forceinline__ void half_stage(double2 (&x)[V], double2* buf,
 #pragma unroll
     for (int q = 0; q < R; ++q) x[i + q * B] = u[q];
   }
-  __syncthreads();  // every thread has consumed the previous contents of buf
+  fft_sync<T>();  // every thread has consumed the previous contents of buf
 #pragma unroll
   for (int i = 0; i < B; ++i) {
     const int j = t + T * i;
@@ -117,7 +128,7 @@ __device__ __forceinline__ void half_stage(double2 (&x)[V], double2* buf,
 #pragma unroll
     for (int q = 0; q < R; ++q) buf[hpidx(base + q * NS)] = x[i + q * B];
   }
-  __syncthreads();
+  fft_sync<T>();
 #pragma unroll
   for (int p = 0; p < V; ++p) x[p] = buf[hpidx(t + T * p)];
 }
@@ -134,9 +145,10 @@ __device__ __forceinline__ void half_fft_stages(double2 (&x)[V], double2* buf,
   }
 }
 
-// Output staging index: one pad double per 16 (conflict-free for the post-processing
-// writes, in which thread t writes 16 consecutive outputs).
-__device__ __forceinline__ int opad(int e) { return e + (e >> 4); }
+// Output staging index: one pad double per V (conflict-free for the post-processing
+// writes, in which thread t writes V consecutive outputs).
+template <int V>
+__device__ __forceinline__ int opad(int e) { return e + e / V; }
 
 // Inclusive prefix sum of (a, b) over the T threads of one FFT (T a multiple of 32; the
 // FFT's warps are warp0 .. warp0 + T/32 - 1, red has 2 T/32 doubles for this FFT).
@@ -176,11 +188,11 @@ __device__ __forceinline__ double2 half_pre(double s, double xa, double xam, dou
 
 // FFT (x holds the pre-processed inputs), post-processing and prefix scan; writes the
 // n outputs of both vectors into oa / ob at opad(e).  buf may overlap oa/ob.
-template <int N>
-__device__ __forceinline__ void half_fft_post(double2 (&x)[16], double2* buf,
+template <int N, int V>
+__device__ __forceinline__ void half_fft_post(double2 (&x)[V], double2* buf,
                                              const double2* __restrict__ tw2, int t, double hs,
                                              double* red, double* oa, double* ob) {
-  constexpr int V = 16, T = N / V, H = V / 2;
+  constexpr int T = N / V, H = V / 2;
   half_fft_stages<N, V, 1>(x, buf, tw2, t);
   // thread t owns k = t H + i (i < H) of the half spectrum k < N/2
   double Aa[H], Ab[H], Ba[H], Bb[H];
@@ -210,25 +222,32 @@ __device__ __forceinline__ void half_fft_post(double2 (&x)[16], double2* buf,
   fft_scan2<T>(ea, eb, red, t);
   ea -= sa;  // exclusive offsets
   eb -= sb;
-  __syncthreads();  // all reads of Z are done: buf may be overwritten by the outputs
+  fft_sync<T>();  // all reads of Z are done: buf may be overwritten by the outputs
 #pragma unroll
   for (int i = 0; i < H; ++i) {
     const int k = t * H + i;
     if (k > 0) {  // X_{2k} -> index 2k - 1
-      oa[opad(2 * k - 1)] = Ba[i];
-      ob[opad(2 * k - 1)] = Bb[i];
+      oa[opad<V>(2 * k - 1)] = Ba[i];
+      ob[opad<V>(2 * k - 1)] = Bb[i];
     }
-    oa[opad(2 * k)] = Aa[i] + ea;  // X_{2k+1} -> index 2k
-    ob[opad(2 * k)] = Ab[i] + eb;
+    oa[opad<V>(2 * k)] = Aa[i] + ea;  // X_{2k+1} -> index 2k
+    ob[opad<V>(2 * k)] = Ab[i] + eb;
   }
 }
 
+// Values per thread.  16 everywhere: radix 16, 16, 4 for N = 1024 (two warps per FFT) and
+// radix 16, 16, 2 for N = 512 (one warp per FFT, warp-level barriers).  A radix-32 variant
+// for N = 1024 (two stages, one warp per FFT) measured 9% slower on cfg3 (27.8 vs 25.5 ms:
+// 168 registers, 12 warps/SM) and was dropped.
+template <int N>
+constexpr int half_v() { return 16; }
+
 template <int N>
 struct HalfCfg {
-  static constexpr int V = 16;
+  static constexpr int V = half_v<N>();
   static constexpr int T = N / V;  // threads per FFT
   static constexpr size_t kSmem = size_t(hpadded_len<N>()) * sizeof(double2);
-  static constexpr int kMinBlocks = 65536 / (T * 128) < 8 ? 65536 / (T * 128) : 8;
+  static constexpr int kMinBlocks = T == 32 ? 12 : (65536 / (T * 128) < 8 ? 65536 / (T * 128) : 8);
   static_assert(T % 32 == 0, "one FFT per whole warps");
 };
 
@@ -246,7 +265,7 @@ __global__ void __launch_bounds__(HalfCfg<N>::T, HalfCfg<N>::kMinBlocks)
   const int64_t nitems = (nvec + 1) / 2;
   const double hs = 0.5 * scale;
   double* oa = reinterpret_cast<double*>(hbuf);
-  double* ob = oa + opad(N);
+  double* ob = oa + opad<V>(N);
   for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x) {
     const int64_t g0 = 2 * item;
     const bool has_b = g0 + 1 < nvec;
@@ -266,12 +285,12 @@ __global__ void __launch_bounds__(HalfCfg<N>::T, HalfCfg<N>::kMinBlocks)
     }
     // (half_fft_post's first barrier orders these reads before hbuf is overwritten, and
     // the previous item's stores from hbuf before this item's first write)
-    half_fft_post<N>(x, hbuf, tw2, t, hs, red, oa, ob);
+    half_fft_post<N, V>(x, hbuf, tw2, t, hs, red, oa, ob);
     __syncthreads();
     double* da = dst + g0 * n;
-    for (int e = t; e < n; e += T) da[e] = oa[opad(e)];
+    for (int e = t; e < n; e += T) da[e] = oa[opad<V>(e)];
     if (has_b)
-      for (int e = t; e < n; e += T) da[n + e] = ob[opad(e)];
+      for (int e = t; e < n; e += T) da[n + e] = ob[opad<V>(e)];
   }
 }
 
@@ -282,8 +301,9 @@ __global__ void __launch_bounds__(HalfCfg<N>::T, HalfCfg<N>::kMinBlocks)
 // and row offsets are chosen so that the tile's row accesses are bank-conflict free.
 template <int N>
 struct HalfStridedCfg {
-  static constexpr int V = 16, T = N / V, P = N >= 2048 ? 2 : 4, G = 2 * P;
+  static constexpr int V = half_v<N>(), T = N / V, P = N >= 2048 ? 2 : 4, G = 2 * P;
   static constexpr int kThreads = P * T;
+  static constexpr int kMinBlocks = T == 32 ? 3 : 2;
   // Row v of the tile starts at (v/2) kRegion + (v%2) kRowB; with kStep = 16/G these are
   // = kStep v (mod 16 doubles), so each half-warp's G x (16/G) row accesses of 8 bytes hit
   // distinct banks.
@@ -295,7 +315,7 @@ struct HalfStridedCfg {
 };
 
 template <int N>
-__global__ void __launch_bounds__(HalfStridedCfg<N>::kThreads, 2)
+__global__ void __launch_bounds__(HalfStridedCfg<N>::kThreads, HalfStridedCfg<N>::kMinBlocks)
     dst_half_strided_kernel(const double* __restrict__ src, double* __restrict__ dst,
                             int64_t inner, int64_t nvec, const double2* __restrict__ tw2,
                             double scale) {
@@ -339,12 +359,12 @@ __global__ void __launch_bounds__(HalfStridedCfg<N>::kThreads, 2)
         x[p] = half_pre(s, ra[m - 1], ra[mm - 1], rb[m - 1], rb[mm - 1]);
       }
     }
-    half_fft_post<N>(x, fbuf, tw2, t, hs, red[f], region, region + RB);
+    half_fft_post<N, V>(x, fbuf, tw2, t, hs, red[f], region, region + RB);
     __syncthreads();
     for (int e = threadIdx.x; e < G * n; e += C::kThreads) {
       const int v = e % G, kk = e / G;
       const int64_t b = vbase[v];
-      if (b >= 0) __stcs(dst + b + int64_t(kk) * inner, row(v)[opad(kk)]);
+      if (b >= 0) __stcs(dst + b + int64_t(kk) * inner, row(v)[opad<V>(kk)]);
     }
   }
 }
