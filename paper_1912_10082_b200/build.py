@@ -48,7 +48,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     log = []
     for src in CUDA_SOURCES:
         obj = objdir / (src + ".o")
-        cmd = [NVCC, *NVCC_FLAGS, "-c", str(CSRC / src), "-o", str(obj)]
+        extra = os.environ.get("STKG_NVCC_EXTRA", "").split()  # variant builds (tools/ab.sh)
+        cmd = [NVCC, *NVCC_FLAGS, *extra, "-c", str(CSRC / src), "-o", str(obj)]
         r = subprocess.run(cmd, capture_output=True, text=True)
         log.append(r.stdout + r.stderr)
         if r.returncode != 0:

@@ -27,6 +27,10 @@
 // the dst.cuh kernels.
 #pragma once
 
+#ifndef STKG_HALF_V
+#define STKG_HALF_V 16
+#endif
+
 #include "dst.cuh"
 
 namespace stkg {
@@ -87,7 +91,7 @@ __device__ __forceinline__ void fft_sync() {
 __host__ __device__ constexpr int hpidx(int i) { return i ^ (((i >> 3) ^ (i >> 6)) & 7); }
 // Buffer length (complex): N for the FFT, and 2 opad(N) doubles for the output staging.
 template <int N>
-constexpr int hpadded_len() { return N + N / 16; }
+constexpr int hpadded_len() { return N + N / (STKG_HALF_V < 16 ? STKG_HALF_V : 16); }
 
 // One Stockham stage (radix R; NS = product of the earlier radices) of a length-N FFT
 // whose T = N/V threads hold x[p] = value at position t + T p.  Computes in registers,
@@ -129,8 +133,10 @@ __device__ __forceinline__ void half_stage(double2 (&x)[V], double2* buf,
     for (int q = 0; q < R; ++q) buf[hpidx(base + q * NS)] = x[i + q * B];
   }
   fft_sync<T>();
+  if constexpr (NS * R < N) {  // the last stage's output is consumed from buf directly
 #pragma unroll
-  for (int p = 0; p < V; ++p) x[p] = buf[hpidx(t + T * p)];
+    for (int p = 0; p < V; ++p) x[p] = buf[hpidx(t + T * p)];
+  }
 }
 
 // All stages: radix V while V divides the remaining length, then the remainder radix.
@@ -240,14 +246,18 @@ __device__ __forceinline__ void half_fft_post(double2 (&x)[V], double2* buf,
 // for N = 1024 (two stages, one warp per FFT) measured 9% slower on cfg3 (27.8 vs 25.5 ms:
 // 168 registers, 12 warps/SM) and was dropped.
 template <int N>
-constexpr int half_v() { return 16; }
+constexpr int half_v() { return STKG_HALF_V; }
 
 template <int N>
 struct HalfCfg {
   static constexpr int V = half_v<N>();
   static constexpr int T = N / V;  // threads per FFT
   static constexpr size_t kSmem = size_t(hpadded_len<N>()) * sizeof(double2);
+#ifdef STKG_HALF_MINB
+  static constexpr int kMinBlocks = STKG_HALF_MINB;
+#else
   static constexpr int kMinBlocks = T == 32 ? 12 : (65536 / (T * 128) < 8 ? 65536 / (T * 128) : 8);
+#endif
   static_assert(T % 32 == 0, "one FFT per whole warps");
 };
 
@@ -301,14 +311,18 @@ __global__ void __launch_bounds__(HalfCfg<N>::T, HalfCfg<N>::kMinBlocks)
 // and row offsets are chosen so that the tile's row accesses are bank-conflict free.
 template <int N>
 struct HalfStridedCfg {
+#ifdef STKG_HALF_P
+  static constexpr int V = half_v<N>(), T = N / V, P = STKG_HALF_P, G = 2 * P;
+#else
   static constexpr int V = half_v<N>(), T = N / V, P = N >= 2048 ? 2 : 4, G = 2 * P;
+#endif
   static constexpr int kThreads = P * T;
-  static constexpr int kMinBlocks = T == 32 ? 3 : 2;
+  static constexpr int kMinBlocks = 65536 / (kThreads * 128) < 1 ? 1 : 65536 / (kThreads * 128);
   // Row v of the tile starts at (v/2) kRegion + (v%2) kRowB; with kStep = 16/G these are
   // = kStep v (mod 16 doubles), so each half-warp's G x (16/G) row accesses of 8 bytes hit
   // distinct banks.
   static constexpr int kStep = 16 / G;
-  static constexpr int kRowB = N + N / 16 + kStep;                 // doubles: offset of row b
+  static constexpr int kRowB = N + N / V + kStep;                  // doubles: offset of row b
   static constexpr int kRegion = 2 * hpadded_len<N>() + 2 * kStep;  // doubles per pair
   static constexpr size_t kSmem = size_t(P) * kRegion * sizeof(double);
   static_assert(T % 32 == 0, "one FFT per whole warps");
