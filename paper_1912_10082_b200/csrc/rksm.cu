@@ -38,46 +38,48 @@ constexpr int kTsCols = 4;   // V columns per block in the tall-skinny Gram
 constexpr int kTsRhs = 8;    // W columns per pass
 constexpr unsigned kEw = 148 * 8;
 
+// Tall-skinny Gram V(:, c0 + 0..k)^T W(:, 0..b): CTA (g, cb) covers rows of slab g (of
+// gridDim.x slabs) and the 32 V columns of block cb, each warp 4 columns; lanes stride the
+// rows.  The 8 warps read the same W rows, so W crosses L2 once per column block (not once
+// per 4 columns).  Partials [(j k + c) gridDim.x + g] are summed in index order by
+// reduce_rows_kernel: deterministic for given sizes.
 template <int B>
 __global__ void __launch_bounds__(256) ts_gram_kernel(const double* __restrict__ V, int64_t n,
                                                       int k, const double* __restrict__ W,
                                                       int b, double* __restrict__ partials) {
-  __shared__ double red[8][kTsCols * B];
-  const int c0 = blockIdx.y * kTsCols;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c0 = blockIdx.y * (8 * kTsCols) + warp * kTsCols;
+  const int64_t rows = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t r0 = int64_t(blockIdx.x) * rows;
+  const int64_t r1 = r0 + rows < n ? r0 + rows : n;
   double s[kTsCols][B];
 #pragma unroll
   for (int c = 0; c < kTsCols; ++c)
 #pragma unroll
     for (int j = 0; j < B; ++j) s[c][j] = 0.0;
-  for (int64_t i = int64_t(blockIdx.x) * 256 + threadIdx.x; i < n; i += int64_t(gridDim.x) * 256) {
-    double w[B];
+  if (c0 < k) {
+    for (int64_t i = r0 + lane; i < r1; i += 32) {
+      double w[B];
 #pragma unroll
-    for (int j = 0; j < B; ++j) w[j] = j < b ? W[int64_t(j) * n + i] : 0.0;
+      for (int j = 0; j < B; ++j) w[j] = j < b ? W[int64_t(j) * n + i] : 0.0;
 #pragma unroll
-    for (int c = 0; c < kTsCols; ++c) {
-      if (c0 + c < k) {
-        const double v = V[int64_t(c0 + c) * n + i];
+      for (int c = 0; c < kTsCols; ++c) {
+        if (c0 + c < k) {
+          const double v = V[int64_t(c0 + c) * n + i];
 #pragma unroll
-        for (int j = 0; j < B; ++j) s[c][j] += v * w[j];
+          for (int j = 0; j < B; ++j) s[c][j] = fma(v, w[j], s[c][j]);
+        }
       }
     }
   }
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int c = 0; c < kTsCols; ++c)
 #pragma unroll
     for (int j = 0; j < B; ++j) {
       const double t = warp_sum(s[c][j]);
-      if (lane == 0) red[warp][c * B + j] = t;
+      if (lane == 0 && c0 + c < k && j < b)
+        partials[(int64_t(j) * k + c0 + c) * gridDim.x + blockIdx.x] = t;
     }
-  __syncthreads();
-  if (threadIdx.x < kTsCols * B) {
-    double t = 0.0;
-#pragma unroll
-    for (int w = 0; w < 8; ++w) t += red[w][threadIdx.x];
-    const int c = threadIdx.x / B, j = threadIdx.x % B;
-    if (c0 + c < k && j < b) partials[(int64_t(j) * k + c0 + c) * gridDim.x + blockIdx.x] = t;
-  }
 }
 
 // Row r = j * kk + c of the partials -> out[j * ld + c] (a kk x bb block of a column-major
@@ -218,10 +220,13 @@ class Rksm {
       const int bb = static_cast<int>(std::min<int64_t>(kTsRhs, b - j0));
       for (int64_t c0 = 0; c0 < k; c0 += 1024) {
         const int kk = static_cast<int>(std::min<int64_t>(1024, k - c0));
-        dim3 grid(kReduceBlocks, static_cast<unsigned>(ceil_div(kk, kTsCols)));
+        const int cblocks = static_cast<int>(ceil_div(kk, 8 * kTsCols));
+        const int slabs = static_cast<int>(std::max<int64_t>(
+            16, std::min<int64_t>(kReduceBlocks, 2 * kReduceBlocks / cblocks)));
+        dim3 grid(static_cast<unsigned>(slabs), static_cast<unsigned>(cblocks));
         ts_gram_kernel<kTsRhs><<<grid, 256, 0, s_>>>(V + c0 * n_, n_, kk, W + j0 * n_, bb,
                                                      partials_.p);
-        reduce_rows_kernel<<<kk * bb, 256, 0, s_>>>(partials_.p, kReduceBlocks, kk, k,
+        reduce_rows_kernel<<<kk * bb, 256, 0, s_>>>(partials_.p, slabs, kk, k,
                                                     Hd + j0 * k + c0);
         STKG_CUDA_CHECK(cudaGetLastError());
       }
