@@ -23,8 +23,9 @@
 // Twiddles come from the 2N-th-root table the plan already holds (stride 2), and
 // sin(pi m / N) = -Im of its m-th entry.
 //
-// Used for N in {512, 1024, 2048} (T >= 32: each FFT owns whole warps); smaller axes keep
-// the dst.cuh kernels.
+// Used by 2D/3D plans for N in [16, 1024] (heat.cu::dst_pass).  FFTs with T <= 32 threads
+// are aligned lane segments (several per warp, warp-level barriers and segmented shuffles);
+// T = 64 (N = 1024) spans two warps.  N = 2048 and 1D plans keep the dst.cuh kernels.
 #pragma once
 
 #ifndef STKG_HALF_V
@@ -72,11 +73,11 @@ __device__ __forceinline__ void dft_small<16>(double2 (&u)[16]) {
   }
 }
 
-// Barrier over the threads of one FFT: a warp barrier when the FFT is exactly one warp
-// (its shared region is private to that warp), else a CTA barrier.
+// Barrier over the threads of one FFT: a warp barrier when the FFT fits in one warp (its
+// shared region is private to the warp's FFTs), else a CTA barrier.
 template <int T>
 __device__ __forceinline__ void fft_sync() {
-  if constexpr (T == 32) {
+  if constexpr (T <= 32) {  // FFTs are aligned lane segments: the warp runs them in lockstep
     __syncwarp();
   } else {
     __syncthreads();
@@ -156,21 +157,24 @@ __device__ __forceinline__ void half_fft_stages(double2 (&x)[V], double2* buf,
 template <int V>
 __device__ __forceinline__ int opad(int e) { return e + e / V; }
 
-// Inclusive prefix sum of (a, b) over the T threads of one FFT (T a multiple of 32; the
-// FFT's warps are warp0 .. warp0 + T/32 - 1, red has 2 T/32 doubles for this FFT).
+// Inclusive prefix sum of (a, b) over the T threads of one FFT.  T <= 32: the FFT is an
+// aligned segment of T lanes (segmented shuffles); T > 32: whole warps, cross-warp totals
+// through red (2 T/32 doubles for this FFT).
 template <int T>
 __device__ __forceinline__ void fft_scan2(double& a, double& b, double* red, int t) {
-  const int lane = t & 31, warp = t >> 5;
+  constexpr int W = T < 32 ? T : 32;
+  const int lane = t & (W - 1);
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const double ta = __shfl_up_sync(0xffffffffu, a, o);
-    const double tb = __shfl_up_sync(0xffffffffu, b, o);
+  for (int o = 1; o < W; o <<= 1) {
+    const double ta = __shfl_up_sync(0xffffffffu, a, o, W);
+    const double tb = __shfl_up_sync(0xffffffffu, b, o, W);
     if (lane >= o) {
       a += ta;
       b += tb;
     }
   }
   if constexpr (T > 32) {
+    const int warp = t >> 5;
     if (lane == 31) {
       red[2 * warp] = a;
       red[2 * warp + 1] = b;
@@ -241,91 +245,117 @@ __device__ __forceinline__ void half_fft_post(double2 (&x)[V], double2* buf,
   }
 }
 
-// Values per thread.  16 everywhere: radix 16, 16, 4 for N = 1024 (two warps per FFT) and
-// radix 16, 16, 2 for N = 512 (one warp per FFT, warp-level barriers).  A radix-32 variant
+// Values per thread: 16 (radix-16 stages, then the remainder radix).  A radix-32 variant
 // for N = 1024 (two stages, one warp per FFT) measured 9% slower on cfg3 (27.8 vs 25.5 ms:
-// 168 registers, 12 warps/SM) and was dropped.
+// 168 registers, 12 warps/SM) and V = 8 15% slower; see DESIGN.md's tuning log.
 template <int N>
 constexpr int half_v() { return STKG_HALF_V; }
 
+// Contiguous-axis configuration: F FFTs (vector pairs) per CTA so that a CTA has at least
+// 64 threads; each FFT owns T = N/V threads (an aligned lane segment when T <= 32).
 template <int N>
 struct HalfCfg {
   static constexpr int V = half_v<N>();
-  static constexpr int T = N / V;  // threads per FFT
-  static constexpr size_t kSmem = size_t(hpadded_len<N>()) * sizeof(double2);
+  static constexpr int T = N / V;             // threads per FFT
+  static constexpr int F = T >= 64 ? 1 : 64 / T;  // FFTs per CTA
+  static constexpr int kThreads = F * T;
+  static constexpr int kBuf = hpadded_len<N>();  // complex per FFT buffer
+  static constexpr size_t kSmem = size_t(F) * kBuf * sizeof(double2);
 #ifdef STKG_HALF_MINB
   static constexpr int kMinBlocks = STKG_HALF_MINB;
 #else
-  static constexpr int kMinBlocks = T == 32 ? 12 : (65536 / (T * 128) < 8 ? 65536 / (T * 128) : 8);
+  static constexpr int kMinBlocks = 65536 / (kThreads * 128) < 8 ? 65536 / (kThreads * 128) : 8;
 #endif
-  static_assert(T % 32 == 0, "one FFT per whole warps");
+  static_assert(T <= 32 || T % 32 == 0, "FFTs are lane segments or whole warps");
 };
 
-// Contiguous axis (vectors of length n = N - 1 back to back): one CTA transforms a pair of
-// vectors per step (persistent grid).  dst may alias src (an item is read before written).
+// Contiguous axis (vectors of length n = N - 1 back to back): a CTA step transforms F
+// consecutive vector pairs (persistent grid); the 2F outputs leave as one contiguous block.
+// dst may alias src (an item is read completely before it is written).
 template <int N>
-__global__ void __launch_bounds__(HalfCfg<N>::T, HalfCfg<N>::kMinBlocks)
+__global__ void __launch_bounds__(HalfCfg<N>::kThreads, HalfCfg<N>::kMinBlocks)
     dst_half_kernel(const double* src, double* dst, int64_t nvec,
                     const double2* __restrict__ tw2, double scale) {
   using C = HalfCfg<N>;
-  constexpr int V = C::V, T = C::T, n = N - 1;
+  constexpr int V = C::V, T = C::T, F = C::F, n = N - 1;
   extern __shared__ __align__(16) double2 hbuf[];
-  __shared__ double red[2 * (T / 32)];
-  const int t = threadIdx.x;
-  const int64_t nitems = (nvec + 1) / 2;
-  const double hs = 0.5 * scale;
-  double* oa = reinterpret_cast<double*>(hbuf);
+  __shared__ double red[T > 32 ? 2 * (T / 32) : 2];
+  const int f = F == 1 ? 0 : static_cast<int>(threadIdx.x) / T;
+  const int t = F == 1 ? static_cast<int>(threadIdx.x) : static_cast<int>(threadIdx.x) % T;
+  double2* fbuf = hbuf + f * C::kBuf;
+  double* oa = reinterpret_cast<double*>(fbuf);
   double* ob = oa + opad<V>(N);
+  const int64_t npairs = (nvec + 1) / 2;
+  const int64_t nitems = (npairs + F - 1) / F;
+  const double hs = 0.5 * scale;
   for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x) {
-    const int64_t g0 = 2 * item;
-    const bool has_b = g0 + 1 < nvec;
-    const double* sa = src + g0 * n;
+    const int64_t g0 = 2 * (item * F + f);  // first vector of this FFT's pair
+    const bool has_a = F == 1 || g0 < nvec, has_b = g0 + 1 < nvec;
+    const double* sa = src + (has_a ? g0 : 0) * n;
     const double* sb = has_b ? sa + n : sa;
     double2 x[V];
 #pragma unroll
     for (int p = 0; p < V; ++p) {
       const int m = t + T * p;
       x[p] = make_double2(0.0, 0.0);
-      if (m > 0) {
+      if (m > 0 && has_a) {
         const int mm = N - m;  // in 1..N-1 as well
         const double s = -__ldg(&tw2[m].y);
         const double xb = has_b ? sb[m - 1] : 0.0, xbm = has_b ? sb[mm - 1] : 0.0;
         x[p] = half_pre(s, sa[m - 1], sa[mm - 1], xb, xbm);
       }
     }
-    // (half_fft_post's first barrier orders these reads before hbuf is overwritten, and
-    // the previous item's stores from hbuf before this item's first write)
-    half_fft_post<N, V>(x, hbuf, tw2, t, hs, red, oa, ob);
+    // (half_fft_post's first barrier orders these reads before fbuf is overwritten, and
+    // the previous item's stores from fbuf before this item's first write: the trailing
+    // __syncthreads below)
+    half_fft_post<N, V>(x, fbuf, tw2, t, hs, red, oa, ob);
     __syncthreads();
-    double* da = dst + g0 * n;
-    for (int e = t; e < n; e += T) da[e] = oa[opad<V>(e)];
-    if (has_b)
-      for (int e = t; e < n; e += T) da[n + e] = ob[opad<V>(e)];
+    if constexpr (F == 1) {
+      double* da = dst + g0 * n;
+      for (int e = t; e < n; e += T) da[e] = oa[opad<V>(e)];
+      if (has_b)
+        for (int e = t; e < n; e += T) da[n + e] = ob[opad<V>(e)];
+    } else {
+      // the item's vectors [2 item F, 2 item F + 2F) are contiguous in memory
+      const int64_t v0 = 2 * item * F;
+      const int nv = static_cast<int>(nvec - v0 < 2 * F ? nvec - v0 : 2 * F);
+      double* d0 = dst + v0 * n;
+      for (int e = threadIdx.x; e < nv * n; e += C::kThreads) {
+        const int q = e / n, idx = e - q * n;  // vector q of the item
+        const double* o_q = reinterpret_cast<const double*>(hbuf + (q >> 1) * C::kBuf) +
+                            ((q & 1) ? opad<V>(N) : 0);
+        d0[e] = o_q[opad<V>(idx)];
+      }
+      __syncthreads();  // other FFTs' buffers were read: next item may overwrite them
+    }
   }
 }
 
 // Strided axis (inner > 1; element j of vector (o, i) at (o n + j) inner + i).  A tile is
 // G = 2P neighbouring vectors (rows of 8G contiguous bytes), staged by cp.async; the P
-// pairs run their FFTs side by side (P T threads), each in its own shared region that
-// holds first the two input rows, then the FFT, then the two output rows.  Region pitch
-// and row offsets are chosen so that the tile's row accesses are bank-conflict free.
+// pairs run their FFTs side by side (P T threads, P T >= 128), each in its own shared
+// region that holds first the two input rows, then the FFT, then the two output rows.
+// Region pitch and row offsets are chosen so that the tile's row accesses are bank-conflict
+// free.
 template <int N>
 struct HalfStridedCfg {
+  static constexpr int V = half_v<N>(), T = N / V;
 #ifdef STKG_HALF_P
-  static constexpr int V = half_v<N>(), T = N / V, P = STKG_HALF_P, G = 2 * P;
+  static constexpr int P = STKG_HALF_P;
 #else
-  static constexpr int V = half_v<N>(), T = N / V, P = N >= 2048 ? 2 : 4, G = 2 * P;
+  static constexpr int P = T >= 32 ? 4 : 128 / T;
 #endif
+  static constexpr int G = 2 * P;
   static constexpr int kThreads = P * T;
   static constexpr int kMinBlocks = 65536 / (kThreads * 128) < 1 ? 1 : 65536 / (kThreads * 128);
-  // Row v of the tile starts at (v/2) kRegion + (v%2) kRowB; with kStep = 16/G these are
-  // = kStep v (mod 16 doubles), so each half-warp's G x (16/G) row accesses of 8 bytes hit
-  // distinct banks.
-  static constexpr int kStep = 16 / G;
+  // Row v of the tile starts at (v/2) kRegion + (v%2) kRowB; with kStep = max(1, 16/G) these
+  // are = kStep v (mod 16 doubles), so each half-warp's row accesses of 8 bytes hit distinct
+  // banks.
+  static constexpr int kStep = G >= 16 ? 1 : 16 / G;
   static constexpr int kRowB = N + N / V + kStep;                  // doubles: offset of row b
   static constexpr int kRegion = 2 * hpadded_len<N>() + 2 * kStep;  // doubles per pair
   static constexpr size_t kSmem = size_t(P) * kRegion * sizeof(double);
-  static_assert(T % 32 == 0, "one FFT per whole warps");
+  static_assert(T <= 32 || T % 32 == 0, "FFTs are lane segments or whole warps");
 };
 
 template <int N>
@@ -338,7 +368,7 @@ __global__ void __launch_bounds__(HalfStridedCfg<N>::kThreads, HalfStridedCfg<N>
   constexpr int RB = C::kRowB, RG = C::kRegion;
   extern __shared__ __align__(16) double smem[];
   __shared__ int64_t vbase[G];
-  __shared__ double red[P][2 * (T / 32)];
+  __shared__ double red[P][T > 32 ? 2 * (T / 32) : 2];
   const int f = threadIdx.x / T, t = threadIdx.x % T;
   double* region = smem + f * RG;
   double2* fbuf = reinterpret_cast<double2*>(region);
@@ -347,9 +377,9 @@ __global__ void __launch_bounds__(HalfStridedCfg<N>::kThreads, HalfStridedCfg<N>
   auto row = [&](int v) { return smem + (v >> 1) * RG + (v & 1) * RB; };
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     __syncthreads();  // the previous tile's stores have read the staging rows
-    if (threadIdx.x < G) {
-      const int64_t g = tile * G + threadIdx.x;
-      vbase[threadIdx.x] = g < nvec ? (g / inner) * n * inner + g % inner : -1;
+    for (int v = threadIdx.x; v < G; v += C::kThreads) {
+      const int64_t g = tile * G + v;
+      vbase[v] = g < nvec ? (g / inner) * n * inner + g % inner : -1;
     }
     __syncthreads();
     for (int e = threadIdx.x; e < G * n; e += C::kThreads) {

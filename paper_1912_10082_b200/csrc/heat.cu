@@ -406,7 +406,7 @@ void launch_dst(const stkg_heat& h, int a, const double* src, double* dst, int64
   STKG_CUDA_CHECK(cudaGetLastError());
 }
 
-// Half-length kernels (dst_half.cuh) for N = n + 1 in {512, 1024}.
+// Half-length kernels (dst_half.cuh) for N = n + 1 in [16, 1024].
 template <int N>
 void launch_dst_half(const stkg_heat& h, int a, const double* src, double* dst, int64_t inner,
                      int64_t outer) {
@@ -420,12 +420,12 @@ void launch_dst_half(const stkg_heat& h, int a, const double* src, double* dst, 
                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            static_cast<int>(C::kSmem)));
       int b = 0;
-      STKG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, dst_half_kernel<N>, C::T,
-                                                                    C::kSmem));
+      STKG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, dst_half_kernel<N>,
+                                                                    C::kThreads, C::kSmem));
       return std::max(b, 1);
     }();
-    const int64_t blocks = std::min<int64_t>(ceil_div(nvec, 2), int64_t(148) * per_sm);
-    dst_half_kernel<N><<<static_cast<unsigned>(blocks), C::T, C::kSmem, h.stream>>>(
+    const int64_t blocks = std::min<int64_t>(ceil_div(nvec, 2 * C::F), int64_t(148) * per_sm);
+    dst_half_kernel<N><<<static_cast<unsigned>(blocks), C::kThreads, C::kSmem, h.stream>>>(
         src, dst, nvec, tw2, scale);
   } else {
     using C = HalfStridedCfg<N>;
@@ -462,6 +462,11 @@ void dst_pass(const stkg_heat& h, int a, const double* src, double* dst, int64_t
     switch (h.n[a] + 1) {
       // N = 2048 keeps the padded 2N kernel: the half-length recurrence's sqrt(N) error
       // growth costs 1D n = 2047 the 1e-10 residual gate (3e-10 measured)
+      case 16: return launch_dst_half<16>(h, a, src, dst, inner, outer);
+      case 32: return launch_dst_half<32>(h, a, src, dst, inner, outer);
+      case 64: return launch_dst_half<64>(h, a, src, dst, inner, outer);
+      case 128: return launch_dst_half<128>(h, a, src, dst, inner, outer);
+      case 256: return launch_dst_half<256>(h, a, src, dst, inner, outer);
       case 512: return launch_dst_half<512>(h, a, src, dst, inner, outer);
       case 1024: return launch_dst_half<1024>(h, a, src, dst, inner, outer);
       default: break;

@@ -217,7 +217,8 @@ def test_factored_load_equals_dense_load(stk, orc, cuda, ndim, n, nt, rank):
 @pytest.mark.parametrize("ndim,n,nt", [(1, 15, 7), (1, 255, 256), (2, 15, 5), (2, 63, 17),
                                        (2, 127, 4), (3, 15, 6), (3, 31, 3), (1, 2047, 3),
                                        (2, 1023, 2), (1, 511, 9), (2, 511, 3), (3, 511, 1),
-                                       (2, 2047, 1), (1, 1023, 5)])
+                                       (2, 2047, 1), (1, 1023, 5), (2, 255, 4), (3, 127, 2),
+                                       (2, 31, 3), (3, 63, 1)])
 def test_dst_backend_equals_dense_backend(stk, cuda, ndim, n, nt):
     """The P1 fast-sine-transform backend computes the same solve_projected_heat_with as the
     dense DMMA backend on the closed-form eigenbasis (X = S diag(mu^-1/2))."""
