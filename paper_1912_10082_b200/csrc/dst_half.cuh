@@ -141,14 +141,25 @@ __device__ __forceinline__ void half_stage(double2 (&x)[V], double2* buf,
 }
 
 // All stages: radix V while V divides the remaining length, then the remainder radix.
-template <int N, int V, int NS>
+// Stops before the stage whose NS reaches STOP (STOP = N: run them all).
+template <int N, int V, int NS, int STOP = N>
 __device__ __forceinline__ void half_fft_stages(double2 (&x)[V], double2* buf,
                                                 const double2* __restrict__ tw2, int t) {
-  if constexpr (NS < N) {
+  if constexpr (NS < STOP) {
     constexpr int rem = N / NS;
     constexpr int R = rem >= V ? V : rem;
     half_stage<N, V, R, NS>(x, buf, tw2, t);
-    half_fft_stages<N, V, NS * R>(x, buf, tw2, t);
+    half_fft_stages<N, V, NS * R, STOP>(x, buf, tw2, t);
+  }
+}
+
+// NS of the last Stockham stage of the length-N plan.
+template <int N, int V, int NS = 1>
+constexpr int last_stage_ns() {
+  if constexpr (N / NS <= V) {
+    return NS;
+  } else {
+    return last_stage_ns<N, V, NS * V>();
   }
 }
 
@@ -196,52 +207,150 @@ __device__ __forceinline__ double2 half_pre(double s, double xa, double xam, dou
   return make_double2(fma(s, xa + xam, 0.5 * (xa - xam)), fma(s, xb + xbm, 0.5 * (xb - xbm)));
 }
 
-// FFT (x holds the pre-processed inputs), post-processing and prefix scan; writes the
-// n outputs of both vectors into oa / ob at opad(e).  buf may overlap oa/ob.
+// Post-processing of the outputs k < N/2 (a thread owns a set of k and, for each, both
+// Z_k and Z_{N-k}): B_k -> X_{2k} at index 2k - 1; A_k parked at index 2k.  Then the
+// prefix scan over k: thread t re-reads the A of k = t H .. t H + H - 1 (consecutive),
+// scans serially and across threads, and writes X_{2k+1} back to index 2k.
 template <int N, int V>
-__device__ __forceinline__ void half_fft_post(double2 (&x)[V], double2* buf,
-                                             const double2* __restrict__ tw2, int t, double hs,
-                                             double* red, double* oa, double* ob) {
+__device__ __forceinline__ void half_scan_odd(int t, double* red, double* oa, double* ob) {
   constexpr int T = N / V, H = V / 2;
-  half_fft_stages<N, V, 1>(x, buf, tw2, t);
-  // thread t owns k = t H + i (i < H) of the half spectrum k < N/2
-  double Aa[H], Ab[H], Ba[H], Bb[H];
-#pragma unroll
-  for (int i = 0; i < H; ++i) {
-    const int k = t * H + i;
-    const double2 zk = buf[hpidx(k)];
-    const double2 zm = buf[hpidx(k == 0 ? 0 : N - k)];
-    Aa[i] = hs * (zk.x + zm.x);
-    Ab[i] = hs * (zk.y + zm.y);
-    Ba[i] = hs * (zm.y - zk.y);
-    Bb[i] = hs * (zk.x - zm.x);
-  }
-  if (t == 0) {
-    Aa[0] *= 0.5;
-    Ab[0] *= 0.5;
-  }
+  double Aa[H], Ab[H];
   double sa = 0.0, sb = 0.0;
 #pragma unroll
   for (int i = 0; i < H; ++i) {
-    sa += Aa[i];
-    sb += Ab[i];
+    const int k = t * H + i;
+    sa += oa[opad<V>(2 * k)];
+    sb += ob[opad<V>(2 * k)];
     Aa[i] = sa;
     Ab[i] = sb;
   }
   double ea = sa, eb = sb;
   fft_scan2<T>(ea, eb, red, t);
-  ea -= sa;  // exclusive offsets
+  ea -= sa;
   eb -= sb;
-  fft_sync<T>();  // all reads of Z are done: buf may be overwritten by the outputs
 #pragma unroll
   for (int i = 0; i < H; ++i) {
     const int k = t * H + i;
-    if (k > 0) {  // X_{2k} -> index 2k - 1
-      oa[opad<V>(2 * k - 1)] = Ba[i];
-      ob[opad<V>(2 * k - 1)] = Bb[i];
-    }
-    oa[opad<V>(2 * k)] = Aa[i] + ea;  // X_{2k+1} -> index 2k
+    oa[opad<V>(2 * k)] = Aa[i] + ea;
     ob[opad<V>(2 * k)] = Ab[i] + eb;
+  }
+}
+
+// FFT (x holds the pre-processed inputs), post-processing and prefix scan; writes the
+// n outputs of both vectors into oa / ob at opad(e).  buf may overlap oa/ob.
+//
+// When the last Stockham stage gives every thread B >= 2 butterflies, it is fused with the
+// post-processing: thread t takes the mirrored butterflies j and NS - j (thread 0 the
+// multiples of T), so Z_k and Z_{N-k} meet in its registers and the last stage's output
+// never goes to shared memory.
+template <int N, int V>
+__device__ __forceinline__ void half_fft_post(double2 (&x)[V], double2* buf,
+                                             const double2* __restrict__ tw2, int t, double hs,
+                                             double* red, double* oa, double* ob) {
+  constexpr int T = N / V, H = V / 2;
+  constexpr int NSL = last_stage_ns<N, V>();
+  constexpr int RL = N / NSL;   // radix of the last stage
+  constexpr int BL = NSL / T;   // its butterflies per thread
+  if constexpr (BL >= 2 && NSL > 1) {
+    half_fft_stages<N, V, 1, NSL>(x, buf, tw2, t);  // leaves the stage-(L-1) output in buf
+    // butterflies of this thread: jj[0..BL/2) and their mirrors jj[BL/2 + i] = NSL - jj[i]
+    int jj[BL];
+#pragma unroll
+    for (int i = 0; i < BL / 2; ++i) {
+      jj[i] = t == 0 ? T * i : t + T * i;
+      jj[BL / 2 + i] = t == 0 ? T * (BL / 2 + i) : NSL - (t + T * i);
+    }
+    double2 z[BL][RL];
+#pragma unroll
+    for (int b = 0; b < BL; ++b) {
+      const int j = jj[b];
+#pragma unroll
+      for (int q = 0; q < RL; ++q) z[b][q] = buf[hpidx(j + NSL * q)];
+      if (j > 0) {
+        const double2 w = __ldg(tw2 + 2 * j);  // exp(-2 pi i j / N)
+        double2 wr = w;
+#pragma unroll
+        for (int q = 1; q < RL; ++q) {
+          if (q > 1) wr = cmul(wr, w);
+          z[b][q] = cmul(z[b][q], wr);
+        }
+      }
+      dft_small<RL>(z[b]);  // z[b][q] = Z_{j + NSL q}
+    }
+    fft_sync<T>();  // every thread has read buf: the output staging may overwrite it
+#pragma unroll
+    for (int b = 0; b < BL; ++b) {
+      const int j = jj[b];
+#pragma unroll
+      for (int q = 0; q < RL / 2; ++q) {  // k = j + NSL q < N/2
+        const int k = j + NSL * q;
+        double2 zm;
+        if (t == 0) {
+          // thread 0 holds the multiples of T: j = T i pairs with NSL - j = T (BL - i)
+          // (b < BL/2: i = b; b >= BL/2: i = b); j = 0 and j = NSL/2 pair with themselves
+          const int bi = (j == 0) ? b : (BL - b) % BL;
+          const int qm = (j == 0) ? (RL - q) % RL : RL - 1 - q;
+          zm = z[bi][qm];
+        } else {
+          const int bm = b < BL / 2 ? b + BL / 2 : b - BL / 2;
+          zm = z[bm][RL - 1 - q];
+        }
+        const double2 zk = z[b][q];
+        double Aa = hs * (zk.x + zm.x), Ab = hs * (zk.y + zm.y);
+        if (k == 0) {
+          Aa *= 0.5;
+          Ab *= 0.5;
+        } else {
+          oa[opad<V>(2 * k - 1)] = hs * (zm.y - zk.y);
+          ob[opad<V>(2 * k - 1)] = hs * (zk.x - zm.x);
+        }
+        oa[opad<V>(2 * k)] = Aa;
+        ob[opad<V>(2 * k)] = Ab;
+      }
+    }
+    fft_sync<T>();
+    half_scan_odd<N, V>(t, red, oa, ob);
+  } else {
+    half_fft_stages<N, V, 1>(x, buf, tw2, t);
+    // thread t owns k = t H + i (i < H) of the half spectrum k < N/2
+    double Aa[H], Ab[H], Ba[H], Bb[H];
+#pragma unroll
+    for (int i = 0; i < H; ++i) {
+      const int k = t * H + i;
+      const double2 zk = buf[hpidx(k)];
+      const double2 zm = buf[hpidx(k == 0 ? 0 : N - k)];
+      Aa[i] = hs * (zk.x + zm.x);
+      Ab[i] = hs * (zk.y + zm.y);
+      Ba[i] = hs * (zm.y - zk.y);
+      Bb[i] = hs * (zk.x - zm.x);
+    }
+    if (t == 0) {
+      Aa[0] *= 0.5;
+      Ab[0] *= 0.5;
+    }
+    double sa = 0.0, sb = 0.0;
+#pragma unroll
+    for (int i = 0; i < H; ++i) {
+      sa += Aa[i];
+      sb += Ab[i];
+      Aa[i] = sa;
+      Ab[i] = sb;
+    }
+    double ea = sa, eb = sb;
+    fft_scan2<T>(ea, eb, red, t);
+    ea -= sa;  // exclusive offsets
+    eb -= sb;
+    fft_sync<T>();  // all reads of Z are done: buf may be overwritten by the outputs
+#pragma unroll
+    for (int i = 0; i < H; ++i) {
+      const int k = t * H + i;
+      if (k > 0) {  // X_{2k} -> index 2k - 1
+        oa[opad<V>(2 * k - 1)] = Ba[i];
+        ob[opad<V>(2 * k - 1)] = Bb[i];
+      }
+      oa[opad<V>(2 * k)] = Aa[i] + ea;  // X_{2k+1} -> index 2k
+      ob[opad<V>(2 * k)] = Ab[i] + eb;
+    }
   }
 }
 
