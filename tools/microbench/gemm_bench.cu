@@ -73,6 +73,14 @@ int main() {
     GemmProblem p; p.M = n; p.K = n; p.N = 1025; p.A = X; p.lda = n; p.B = F; p.ldb = n; p.C = C; p.ldc = n;
     shapes.push_back({"single 1023x1023 * 1023x1025", p});
   }
+  for (int ks : {2, 3, 4}) {  // split-K emulation: ks K-slices of the single shape as a batch
+    GemmProblem p; p.M = n; p.K = (n + ks - 1) / ks; p.N = 1025; p.batch = ks; p.A = X; p.lda = n;
+    p.strideA = p.K * n; p.B = F; p.ldb = n; p.strideB = p.K; p.C = C; p.ldc = n;
+    p.strideC = n * 1025;
+    static char names[3][64];
+    snprintf(names[ks - 2], 64, "splitK%d 1023x%dx1025 (batch)", ks, (int)p.K);
+    shapes.push_back({names[ks - 2], p});
+  }
   for (auto& s : shapes) {
     const double flops = 2.0 * s.p.M * s.p.N * s.p.K * s.p.batch;
     const size_t outn = s.p.M * s.p.N * s.p.batch;  // ldc == M here
