@@ -290,6 +290,54 @@ def rksm_leg(stk, inputs, with_cpu=True, name="cfg1"):
     return out
 
 
+def wave_leg(stk, inputs, with_cpu=True, cpu_iters=10):
+    """SURVEY 8(a) rows a8-a10 on BASELINE config 4 (1D wave, cubic splines, 1023 x 1025):
+    the reference's GMRES + TwoTermPrecond for a fixed 300-iteration budget and the PCG
+    performance path, timed on the device; the reference-faithful oracle GMRES (numpy +
+    multithreaded BLAS) timed per iteration on the host for a bounded number of iterations."""
+    import torch
+    cfg = inputs.CONFIGS["cfg4"]
+    sm = stk.wave_space_matrices(stk.SpaceGrid1D(0.0, 1.0, cfg.nh))
+    tm = stk.wave_time_matrices(stk.TimeGrid(cfg.nt, 1.0))
+    plan = stk.WavePlan(sm, tm)
+    Fh = inputs.wave_rhs_host(cfg)
+    F = torch.tensor(Fh, device="cuda")
+    plan.gmres(F, stk.GmresConfig(tol=1e-9, maxit=5))  # warm-up
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    _, rg = plan.gmres(F, stk.GmresConfig(tol=1e-9, maxit=300))
+    torch.cuda.synchronize()
+    tg = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    _, rp = plan.pcg(F, tol=1e-7, maxit=6000)
+    torch.cuda.synchronize()
+    tp = time.perf_counter() - t0
+    N = cfg.nh * (cfg.nt + 1)
+    out = {"workload": cfg.name, "unknowns": N,
+           "gmres": {"iterations": rg.iterations, "final_relres": rg.final_relres,
+                     "s": tg, "ms_per_iteration": 1e3 * tg / max(rg.iterations, 1)},
+           "pcg": {"iterations": rp.iterations, "final_relres": rp.final_relres, "tol": 1e-7,
+                   "s": tp, "ms_per_iteration": 1e3 * tp / max(rp.iterations, 1),
+                   "unknowns_per_s": N / tp}}
+    if with_cpu:
+        sys.path.insert(0, str(ROOT))
+        from oracle import oracle as orc
+        sb = np.stack([sm.M.band, sm.A.band, sm.Q.band])
+        tb = np.stack([tm.Q.band, tm.D.band, tm.M.band])
+        ws = orc.WaveSystemNP(sb, tb)
+        b = np.ascontiguousarray(Fh).ravel()
+        t0 = time.perf_counter()
+        _, its, _ = ws.gmres(b, tol=1e-14, maxit=cpu_iters)
+        tc = time.perf_counter() - t0
+        out["cpu_oracle_gmres"] = {"iterations": its, "s": tc,
+                                   "ms_per_iteration": 1e3 * tc / max(its, 1),
+                                   "cores": os.cpu_count(), "kind": "port",
+                                   "sample": f"{its} reference-faithful GMRES iterations "
+                                             "(numpy/scipy, MGS + re-orth, dense eigenbasis "
+                                             "preconditioner) on the full config-4 system"}
+    return out
+
+
 def run_ours(args):
     import torch
     rank, world, local = dist_env()
@@ -378,6 +426,8 @@ def run_ours(args):
         line["alt_path"] = alt_res
     if rank == 0 and not args.no_rksm:
         line["rksm"] = rksm_leg(stk, inputs, with_cpu=(world == 1 and not args.no_cpu))
+    if rank == 0 and not args.no_wave:
+        line["wave"] = wave_leg(stk, inputs, with_cpu=(world == 1 and not args.no_cpu))
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu_t = cpu_reference_run(cfg, args.ref_sample)
         cpu_v = cfg.nx * args.ref_sample / cpu_t
@@ -406,6 +456,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-rksm", action="store_true", help="skip the RKSM (cfg1) side leg")
+    ap.add_argument("--no-wave", action="store_true", help="skip the wave (cfg4) side leg")
     ap.add_argument("--no-alt", action="store_true", help="skip timing the other transform backend")
     ap.add_argument("--transform", choices=["dst", "dense"], default="dst",
                     help="headline backend: P1 fast sine transforms (dst) or dense DMMA GEMMs")
