@@ -31,6 +31,10 @@ class CudaError(StkError, RuntimeError):
     """CUDA runtime failure (no reference counterpart)."""
 
 
+# status codes of include/stk_gpu.h
+STKG_OK, STKG_ARGUMENT, STKG_DEFINITENESS, STKG_SINGULARITY, STKG_SOLVABILITY, STKG_NUMERIC, \
+    STKG_CUDA = range(7)
+
 _BY_CODE = {1: ArgumentError, 2: DefinitenessError, 3: SingularityError, 4: SolvabilityError,
             5: NumericError, 6: CudaError}
 
