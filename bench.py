@@ -312,8 +312,17 @@ def wave_leg(stk, inputs, with_cpu=True, cpu_iters=10):
     _, rp = plan.pcg(F, tol=1e-7, maxit=6000)
     torch.cuda.synchronize()
     tp = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    _, _, rr = plan.solve_refined(F, tol=1e-10, inner_tol=1e-6, max_refine=6)
+    torch.cuda.synchronize()
+    tr = time.perf_counter() - t0
     N = cfg.nh * (cfg.nt + 1)
     out = {"workload": cfg.name, "unknowns": N,
+           "refined_dd": {"tol": 1e-10, "rounds": len(rr.rel_res_history) - 1,
+                          "pcg_iterations": rr.iterations, "final_relres_dd": rr.final_relres,
+                          "history": rr.rel_res_history, "converged": rr.converged, "s": tr,
+                          "note": "mixed-precision iterative refinement, residual in "
+                                  "double-double (stkg_wave_solve_refined)"},
            "gmres": {"iterations": rg.iterations, "final_relres": rg.final_relres,
                      "s": tg, "ms_per_iteration": 1e3 * tg / max(rg.iterations, 1)},
            "pcg": {"iterations": rp.iterations, "final_relres": rp.final_relres, "tol": 1e-7,

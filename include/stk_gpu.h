@@ -242,6 +242,22 @@ int stkg_gmres(stkg_wave* plan, const double* b, double* x, const stkg_gmres_con
  * Stops on the recursively updated ||r||/||b|| <= tol; final_relres is the true one. */
 int stkg_pcg(stkg_wave* plan, const double* b, double* x, double tol, int maxit,
              stkg_report* report);
+/* r = b - B (x_hi + x_lo) evaluated in double-double arithmetic (error-free products of the
+ * band coefficients, compensated sums), returned rounded to FP64 in r (device, may be NULL),
+ * with ||r||_2 / ||b||_2 in *relres.  x_lo may be NULL (treated as 0).  SURVEY F5: at config
+ * 4 the FP64-evaluated residual itself has an error floor near 1e-8..1e-7, so a 1e-10 bar
+ * can only be checked (and met) with an extended-precision residual. */
+int stkg_wave_residual_dd(stkg_wave* plan, const double* b, const double* x_hi,
+                          const double* x_lo, double* r, double* relres);
+/* Mixed-precision iterative refinement for the wave system: the solution
+ * is kept as an unevaluated double-double sum x_hi + x_lo; each round computes the residual
+ * in double-double (stkg_wave_residual_dd), solves B d = r with PCG to inner_tol, and adds d
+ * with a two-sum.  Stops when the double-double relative residual is <= tol or after
+ * max_refine corrections.  report: iterations = total PCG iterations; rel_res_history = the
+ * double-double relative residual before each correction and at the end. */
+int stkg_wave_solve_refined(stkg_wave* plan, const double* b, double* x_hi, double* x_lo,
+                            double tol, int max_refine, double inner_tol, int inner_maxit,
+                            stkg_report* report);
 
 #ifdef __cplusplus
 }

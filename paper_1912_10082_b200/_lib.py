@@ -123,6 +123,11 @@ SIGNATURES = {
                              C.POINTER(Report)]),
     "stkg_pcg": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_int,
                            C.POINTER(Report)]),
+    "stkg_wave_residual_dd": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                        C.c_void_p, C.POINTER(C.c_double)]),
+    "stkg_wave_solve_refined": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                          C.c_double, C.c_int, C.c_double, C.c_int,
+                                          C.POINTER(Report)]),
 }
 
 

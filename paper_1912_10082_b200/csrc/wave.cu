@@ -104,6 +104,93 @@ __global__ void __launch_bounds__(KThreads) wave_apply_kernel(
   }
 }
 
+// ---------------------------------------------------- double-double residual (F5) --
+// Error-free transformations written with the _rn intrinsics so that the compiler cannot
+// contract them into FMAs.
+struct DD {
+  double hi, lo;
+};
+__device__ __forceinline__ DD two_sum(double a, double b) {
+  const double s = __dadd_rn(a, b);
+  const double bb = __dsub_rn(s, a);
+  const double e = __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb));
+  return {s, e};
+}
+__device__ __forceinline__ DD fast_two_sum(double a, double b) {  // |a| >= |b|
+  const double s = __dadd_rn(a, b);
+  return {s, __dsub_rn(b, __dsub_rn(s, a))};
+}
+__device__ __forceinline__ DD dd_add(DD a, DD b) {
+  DD s = two_sum(a.hi, b.hi);
+  const DD t = two_sum(a.lo, b.lo);
+  s.lo = __dadd_rn(s.lo, t.hi);
+  s = fast_two_sum(s.hi, s.lo);
+  s.lo = __dadd_rn(s.lo, t.lo);
+  return fast_two_sum(s.hi, s.lo);
+}
+__device__ __forceinline__ DD dd_mul(DD a, DD b) {
+  const double p = __dmul_rn(a.hi, b.hi);
+  double e = fma(a.hi, b.hi, -p);                  // exact low part of a.hi * b.hi
+  e = fma(a.hi, b.lo, e);
+  e = fma(a.lo, b.hi, e);
+  return fast_two_sum(p, e);
+}
+
+// r = b - sum_p S_p U T_p^T with U = xh + xl, out(i, j) = sum_p sum_a sum_b S_p[a][i]
+// T_p[b][j] U(i + a - 3, j + b - 3) (the K5 stencil written per output), all in
+// double-double.  One thread per output; called a few times per solve.
+__global__ void __launch_bounds__(256) wave_residual_dd_kernel(
+    const double* __restrict__ bvec, const double* __restrict__ xh, const double* __restrict__ xl,
+    double* __restrict__ r, int64_t nh, int64_t nt, const double* __restrict__ S0,
+    const double* __restrict__ S1, const double* __restrict__ S2, const double* __restrict__ T0,
+    const double* __restrict__ T1, const double* __restrict__ T2) {
+  const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= nh * nt) return;
+  const int64_t i = e % nh, j = e / nh;
+  const double* S[3] = {S0, S1, S2};
+  const double* T[3] = {T0, T1, T2};
+  DD acc = {0.0, 0.0};
+  for (int p = 0; p < kTerms; ++p) {
+    for (int bb = 0; bb < kBand; ++bb) {
+      const int64_t jj = j + bb - kHalf;
+      if (jj < 0 || jj >= nt) continue;
+      const double tc = T[p][bb * nt + j];
+      if (tc == 0.0) continue;
+      for (int a = 0; a < kBand; ++a) {
+        const int64_t ii = i + a - kHalf;
+        if (ii < 0 || ii >= nh) continue;
+        const double sc = S[p][a * nh + i];
+        if (sc == 0.0) continue;
+        const double cp = __dmul_rn(sc, tc);
+        const DD coef = {cp, fma(sc, tc, -cp)};  // exact product of the two coefficients
+        const int64_t o = jj * nh + ii;
+        acc = dd_add(acc, dd_mul(coef, DD{xh[o], xl ? xl[o] : 0.0}));
+      }
+    }
+  }
+  const DD res = dd_add(DD{bvec[e], 0.0}, DD{-acc.hi, -acc.lo});
+  r[e] = __dadd_rn(res.hi, res.lo);
+}
+
+// (xh, xl) += d as a double-double sum.
+__global__ void dd_accumulate_kernel(double* __restrict__ xh, double* __restrict__ xl,
+                                     const double* __restrict__ d, int64_t n) {
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const DD s = dd_add(DD{xh[e], xl[e]}, DD{d[e], 0.0});
+    xh[e] = s.hi;
+    xl[e] = s.lo;
+  }
+}
+
+double residual_dd(stkg_wave& w, const double* b, const double* xh, const double* xl, double* r) {
+  wave_residual_dd_kernel<<<static_cast<unsigned>(ceil_div(w.N, 256)), 256, 0, w.stream>>>(
+      b, xh, xl, r, w.nh, w.nt, w.S[0].p, w.S[1].p, w.S[2].p, w.T[0].p, w.T[1].p, w.T[2].p);
+  STKG_CUDA_CHECK(cudaGetLastError());
+  const double nb = knorm(w.krylov, b);
+  return nb > 0.0 ? knorm(w.krylov, r) / nb : 0.0;
+}
+
 std::vector<double> transpose(const double* X, int64_t n) {
   std::vector<double> t(static_cast<size_t>(n * n));
   for (int64_t j = 0; j < n; ++j)
@@ -274,6 +361,73 @@ int stkg_pcg(stkg_wave* wv, const double* b, double* x, double tol, int maxit,
     const DevOp apply = [&](const double* in, double* out) { apply_op(w, in, out); };
     const DevOp precond = [&](const double* in, double* out) { precond_solve(w, in, out); };
     pcg_run(w.krylov, apply, precond, b, x, tol, maxit, rep);
+  });
+}
+
+int stkg_wave_residual_dd(stkg_wave* wv, const double* b, const double* x_hi,
+                          const double* x_lo, double* r, double* relres) {
+  return guarded([&] {
+    STKG_REQUIRE(wv && b && x_hi && relres, STKG_ARGUMENT, "residual_dd: null argument");
+    stkg_wave& w = *wv;
+    w.krylov.ensure(0, 0);
+    DevBuf tmp;
+    double* rr = r;
+    if (!rr) {
+      tmp.alloc(w.N);
+      rr = tmp.p;
+    }
+    *relres = residual_dd(w, b, x_hi, x_lo, rr);
+  });
+}
+
+int stkg_wave_solve_refined(stkg_wave* wv, const double* b, double* x_hi, double* x_lo,
+                            double tol, int max_refine, double inner_tol, int inner_maxit,
+                            stkg_report* rep) {
+  return guarded([&] {
+    STKG_REQUIRE(wv && b && x_hi && x_lo, STKG_ARGUMENT, "solve_refined: null argument");
+    STKG_REQUIRE(wv->has_precond, STKG_ARGUMENT, "solve_refined: no preconditioner in plan");
+    STKG_REQUIRE(max_refine >= 0 && inner_maxit >= 1, STKG_ARGUMENT,
+                 "solve_refined: bad iteration limits");
+    const auto t0 = std::chrono::steady_clock::now();
+    stkg_wave& w = *wv;
+    w.krylov.ensure(0, 0);
+    const DevOp apply = [&](const double* in, double* out) { apply_op(w, in, out); };
+    const DevOp precond = [&](const double* in, double* out) { precond_solve(w, in, out); };
+    DevBuf r(w.N), d(w.N);
+    STKG_CUDA_CHECK(cudaMemsetAsync(x_hi, 0, sizeof(double) * w.N, w.stream));
+    STKG_CUDA_CHECK(cudaMemsetAsync(x_lo, 0, sizeof(double) * w.N, w.stream));
+    int total = 0, len = 0;
+    double relres = 1.0;
+    bool converged = false;
+    auto push = [&](double v) {
+      if (rep && rep->rel_res_history && len < rep->history_capacity) rep->rel_res_history[len] = v;
+      ++len;
+    };
+    for (int k = 0;; ++k) {
+      relres = residual_dd(w, b, x_hi, x_lo, r.p);
+      push(relres);
+      if (relres <= tol) {
+        converged = true;
+        break;
+      }
+      if (k == max_refine) break;
+      stkg_report inner{};
+      pcg_run(w.krylov, apply, precond, r.p, d.p, inner_tol, inner_maxit, &inner);
+      total += inner.iterations;
+      dd_accumulate_kernel<<<148 * 8, 256, 0, w.stream>>>(x_hi, x_lo, d.p, w.N);
+      STKG_CUDA_CHECK(cudaGetLastError());
+    }
+    STKG_CUDA_CHECK(cudaStreamSynchronize(w.stream));
+    if (rep) {
+      rep->iterations = total;
+      rep->converged = converged ? 1 : 0;
+      rep->stagnated = 0;
+      rep->final_relres = relres;
+      rep->history_length = len;
+      rep->mu_mem = 0;
+      rep->wall_time_s =
+          std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    }
   });
 }
 

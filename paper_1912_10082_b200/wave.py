@@ -151,6 +151,36 @@ class WavePlan:
                            C.byref(rep)))
         return x, _report(rep, hist)
 
+    def residual_dd(self, b, x_hi, x_lo=None, out=None) -> float:
+        """||b - B (x_hi + x_lo)|| / ||b|| with the residual evaluated in double-double
+        (stkg_wave_residual_dd); the FP64-rounded residual vector lands in out if given."""
+        self._chk(b)
+        self._chk(x_hi)
+        rel = C.c_double()
+        check(lib.stkg_wave_residual_dd(
+            self._h, C.c_void_p(_dev_ptr(b)), C.c_void_p(_dev_ptr(x_hi)),
+            C.c_void_p(_dev_ptr(x_lo) if x_lo is not None else None),
+            C.c_void_p(_dev_ptr(out) if out is not None else None), C.byref(rel)))
+        return rel.value
+
+    def solve_refined(self, b, tol: float = 1e-10, max_refine: int = 6,
+                      inner_tol: float = 1e-6, inner_maxit: int = 6000):
+        """Mixed-precision iterative refinement (stkg_wave_solve_refined): returns
+        (x_hi, x_lo, SolveReport) with the solution x_hi + x_lo as a double-double pair;
+        rel_res_history holds the double-double relative residual per round."""
+        import torch
+        self._chk(b)
+        xh = torch.empty_like(b)
+        xl = torch.empty_like(b)
+        hist = np.zeros(max_refine + 2)
+        rep = Report()
+        rep.rel_res_history = _np_ptr(hist)
+        rep.history_capacity = hist.size
+        check(lib.stkg_wave_solve_refined(self._h, C.c_void_p(_dev_ptr(b)), C.c_void_p(_dev_ptr(xh)),
+                                          C.c_void_p(_dev_ptr(xl)), tol, max_refine, inner_tol,
+                                          inner_maxit, C.byref(rep)))
+        return xh, xl, _report(rep, hist)
+
 
 class WaveOperator:
     """vec(M_h U Q_t^T + A_h U (D_t + D_t^T) + Q_h U M_t) (stk/outer_krylov.hpp:168-191)."""

@@ -175,3 +175,59 @@ def test_generic_gmres_callback_seam(stk, ref_bands, cuda):
     x, r = stk.gmres(lambda v: d * v, None, torch.ones(5, dtype=torch.float64, device="cuda"),
                      stk.GmresConfig(tol=1e-12, maxit=10))
     assert r.iterations <= 5 and torch.allclose(x, 1.0 / d, rtol=1e-12)
+
+
+# ------------------------------------------- extended-precision residual and refinement --
+def _longdouble_residual(orc, sb, tb, b, xh, xl):
+    """b - B x in numpy longdouble (64-bit mantissa) with B from the raw bands."""
+    L = np.longdouble
+    dense = lambda band: orc.band_sparse(band).toarray().astype(L)
+    Mh, Ah, Qh = (dense(sb[k]) for k in range(3))
+    Qt, Dt, Mt = (dense(tb[k]) for k in range(3))
+    E = Dt + Dt.T
+    nh, nt = sb.shape[2], tb.shape[2]
+    U = (xh.astype(L) + xl.astype(L)).reshape(nt, nh).T
+    out = (Mh @ U) @ Qt.T + (Ah @ U) @ E + (Qh @ U) @ Mt
+    r = b.astype(L) - out.T.ravel()
+    return float(np.sqrt(np.sum(r * r)) / np.sqrt(np.sum(b.astype(L) ** 2)))
+
+
+def test_residual_dd_vs_longdouble(stk, orc, ref_bands, cuda):
+    """stkg_wave_residual_dd agrees with an independent 64-bit-mantissa evaluation, and both
+    sit far below what the FP64 residual can resolve for a PCG iterate."""
+    sb, tb = ref_bands["space_31_3"], ref_bands["time_33_3"]
+    plan = plan_from_bands(stk, sb, tb)
+    rng = np.random.default_rng(11)
+    b = rng.standard_normal(plan.N)
+    x, _ = plan.pcg(dev(b), tol=1e-12, maxit=3000)
+    xh = host(x)
+    xl = rng.standard_normal(plan.N) * 1e-20  # a genuine low part
+    rel_dd = plan.residual_dd(dev(b), x, dev(xl))
+    rel_ld = _longdouble_residual(orc, sb, tb, b, xh, xl)
+    assert abs(rel_dd - rel_ld) <= 1e-3 * rel_ld + 1e-17
+
+
+def test_refined_solve_small(stk, orc, ref_bands, cuda):
+    sb, tb = ref_bands["space_31_3"], ref_bands["time_33_3"]
+    plan = plan_from_bands(stk, sb, tb)
+    b = np.random.default_rng(12).standard_normal(plan.N)
+    xh, xl, rep = plan.solve_refined(dev(b), tol=1e-14, inner_tol=1e-6)
+    assert rep.converged and rep.final_relres <= 1e-14
+    assert _longdouble_residual(orc, sb, tb, b, host(xh), host(xl)) <= 1e-14
+    h = rep.rel_res_history
+    assert h[0] == 1.0 and all(b2 < b1 for b1, b2 in zip(h, h[1:]))
+
+
+def test_cfg4_refined_to_north_star_tolerance(stk, cuda):
+    """Config 4 to the north_star wave bar (1e-10), measured on the double-double residual:
+    FP64 PCG alone stalls near 1e-7; two to three refinement rounds reach it."""
+    from paper_1912_10082_b200 import inputs
+    cfg = inputs.CONFIGS["cfg4"]
+    sm = stk.wave_space_matrices(stk.SpaceGrid1D(0.0, 1.0, cfg.nh))
+    tm = stk.wave_time_matrices(stk.TimeGrid(cfg.nt, 1.0))
+    plan = stk.WavePlan(sm, tm)
+    F = dev(inputs.wave_rhs_host(cfg))
+    xh, xl, rep = plan.solve_refined(F, tol=1e-10, inner_tol=1e-6, max_refine=6)
+    print("cfg4 refined", rep.rel_res_history, rep.iterations, rep.wall_time_s)
+    assert rep.converged and rep.final_relres <= 1e-10
+    assert plan.residual_dd(F, xh, xl) <= 1e-10
