@@ -391,6 +391,23 @@ class WavePlan {
     check(stkg_pcg(w_, b, x, tol, maxit, &r));
     return detail::to_report(r, hist);
   }
+  // ||b - B (x_hi + x_lo)|| / ||b|| with the residual in double-double (x_lo may be null).
+  double residual_dd(const double* b, const double* x_hi, const double* x_lo = nullptr,
+                     double* r = nullptr) {
+    double rel = 0.0;
+    check(stkg_wave_residual_dd(w_, b, x_hi, x_lo, r, &rel));
+    return rel;
+  }
+  // Mixed-precision iterative refinement; the solution is the pair x_hi + x_lo.
+  SolveReport solve_refined(const double* b, double* x_hi, double* x_lo, double tol = 1e-10,
+                            int max_refine = 6, double inner_tol = 1e-6, int inner_maxit = 6000) {
+    std::vector<double> hist(static_cast<size_t>(max_refine) + 2);
+    stkg_report r{};
+    r.rel_res_history = hist.data();
+    r.history_capacity = static_cast<int>(hist.size());
+    check(stkg_wave_solve_refined(w_, b, x_hi, x_lo, tol, max_refine, inner_tol, inner_maxit, &r));
+    return detail::to_report(r, hist);
+  }
 
   static std::vector<double> dense(const Band7& b) {
     std::vector<double> m(static_cast<size_t>(b.n * b.n), 0.0);

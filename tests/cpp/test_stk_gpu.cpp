@@ -136,6 +136,12 @@ int main() {
     cfg.maxit = 500;
     SolveReport r1 = plan.gmres(db.data(), x1.data(), cfg);
     EXPECT(r1.converged && r1.final_relres < 1e-10);
+    {
+      DeviceBuffer xh(N), xl(N);
+      SolveReport rr = plan.solve_refined(db.data(), xh.data(), xl.data(), 1e-13);
+      EXPECT(rr.converged && rr.final_relres <= 1e-13);
+      EXPECT(plan.residual_dd(db.data(), xh.data(), xl.data()) <= 1e-13);
+    }
     for (size_t i = 1; i < r1.rel_res_history.size(); ++i)
       EXPECT(r1.rel_res_history[i] <= r1.rel_res_history[i - 1] * (1 + 1e-12));
     SolveReport r2 = plan.pcg(db.data(), x2.data(), 1e-12, 2000);
