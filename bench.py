@@ -142,6 +142,15 @@ def cpu_reference_run(cfg, steps: int, seed: int = 0):
     return time.perf_counter() - t0
 
 
+def binding_from_profiles():
+    """The resource that actually bounds the half-length DST kernels (ncu, committed)."""
+    p = ROOT / "profiles" / "traffic.json"
+    try:
+        return json.loads(p.read_text()).get("dst_half_binding_resource")
+    except Exception:
+        return None
+
+
 def traffic_from_profiles(kind: str = "gemm"):
     p = ROOT / "profiles" / "traffic.json"
     if p.exists():
@@ -234,6 +243,7 @@ def _timed_path(stk, inputs, cfg, transform, args, stream, barrier, F, U, with_c
                 "achieved": achieved, "peak": HBM_GBS, "unit": "GB/s",
                 "frac": achieved / HBM_GBS,
                 "traffic": traffic_from_profiles("dst_half" if half else "dst"),
+                "binding_resource": binding_from_profiles() if half else None,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs",
                 "flop_per_unknown_per_pass": fft_flops,
                 "whole_solve_frac": ((2 * cfg.ndim + 1) * 16.0 * N * args.steps / (ms / 1e3) / 1e9)
