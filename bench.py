@@ -142,6 +142,34 @@ def cpu_reference_run(cfg, steps: int, seed: int = 0):
     return time.perf_counter() - t0
 
 
+def cpu_cn_run(cfg, steps: int = 16, seed: int = 0):
+    """The reference's own CPU heat solver for a full-rank load: crank_nicolson
+    (stk/cn_baseline.hpp:26-48; SimplicialLLT -> SuperLU), single thread as the reference
+    runs it.  Times the factorisation plus `steps` steps; the full solve is
+    extrapolated linearly in n_t (SPEC.md:523 records CN as linear in N_t)."""
+    import scipy.sparse.linalg as spl
+    from oracle import oracle as O
+    from paper_1912_10082_b200 import inputs
+    F = inputs.heat_rhs_host(cfg, seed, nsteps=steps)
+    m, a = O.fem1d_matrices(0.0, 1.0, cfg.n)
+    M, A = O.tensor_sparse([m] * cfg.ndim, [a] * cfg.ndim)
+    dt = 1.0 / cfg.nt
+    t0 = time.perf_counter()
+    lu = spl.splu((M + (dt / 2.0) * A).tocsc())
+    t_fac = time.perf_counter() - t0
+    rhs = (M - (dt / 2.0) * A).tocsr()
+    u = np.zeros(F.shape[1])
+    t0 = time.perf_counter()
+    for l in range(steps):
+        u = lu.solve(rhs @ u + F[l])
+    t_step = (time.perf_counter() - t0) / steps
+    t_full = t_fac + cfg.nt * t_step
+    return {"value": cfg.unknowns / t_full, "unit": UNIT, "cores": 1, "kind": "port",
+            "factor_s": t_fac, "step_s": t_step, "full_solve_s_extrapolated": t_full,
+            "sample": f"crank_nicolson (SuperLU, 1 thread): factorisation + {steps} of "
+                      f"{cfg.nt} steps of {cfg.name}, extrapolated linearly in n_t"}
+
+
 def binding_from_profiles():
     """The resource that actually bounds the half-length DST kernels (ncu, committed)."""
     p = ROOT / "profiles" / "traffic.json"
@@ -450,6 +478,8 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu_t = cpu_reference_run(cfg, args.ref_sample)
         cpu_v = cfg.nx * args.ref_sample / cpu_t
+        if not args.no_cn:
+            line["cpu_reference_cn"] = cpu_cn_run(cfg)
         line["cpu_baseline"] = {"value": cpu_v, "unit": UNIT, "cores": os.cpu_count(),
                                 "kind": "port",
                                 "sample": f"oracle heat_decoupled (numpy+BLAS), "
@@ -476,6 +506,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-rksm", action="store_true", help="skip the RKSM (cfg1) side leg")
     ap.add_argument("--no-wave", action="store_true", help="skip the wave (cfg4) side leg")
+    ap.add_argument("--no-cn", action="store_true",
+                    help="skip the single-thread Crank-Nicolson CPU reference timing")
     ap.add_argument("--no-alt", action="store_true", help="skip timing the other transform backend")
     ap.add_argument("--transform", choices=["dst", "dense"], default="dst",
                     help="headline backend: P1 fast sine transforms (dst) or dense DMMA GEMMs")
