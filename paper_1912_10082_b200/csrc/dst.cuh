@@ -19,12 +19,6 @@
 #include "common.cuh"
 #include "gemm_f64.cuh"  // cp_async8 / commit / wait
 
-#ifndef STKG_DST_THREADS
-#define STKG_DST_THREADS 256
-#endif
-#ifndef STKG_DST_CTAS
-#define STKG_DST_CTAS 2
-#endif
 
 namespace stkg {
 

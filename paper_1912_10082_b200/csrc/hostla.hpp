@@ -43,99 +43,6 @@ inline double frob(const Mat& A) {
   return std::sqrt(s);
 }
 
-// Diagonally pivoted Cholesky of a symmetric positive semi-definite Gram matrix G (m x m):
-// G(perm, perm) = R^T R with R upper (rank x m, stored m x m).  Stops when the next pivot
-// is <= tol^2 * (largest pivot) -- the Gram-matrix analogue of a rank-revealing QR with
-// relative threshold tol on |R_ii|.  Returns the rank.
-inline int pivoted_cholesky(Mat G, int m, double tol, std::vector<int>& perm, Mat& R) {
-  perm.resize(m);
-  std::iota(perm.begin(), perm.end(), 0);
-  R.assign(static_cast<size_t>(m) * m, 0.0);
-  double first = -1.0;
-  int rank = 0;
-  for (int k = 0; k < m; ++k) {
-    int piv = k;
-    for (int i = k + 1; i < m; ++i)
-      if (at(G, m, i, i) > at(G, m, piv, piv)) piv = i;
-    const double d = at(G, m, piv, piv);
-    if (first < 0.0) first = d;
-    if (!(d > tol * tol * first) || !(d > 0.0)) break;
-    if (piv != k) {  // symmetric swap of rows/cols k and piv, and of the computed R columns
-      for (int i = 0; i < m; ++i) std::swap(at(G, m, i, k), at(G, m, i, piv));
-      for (int j = 0; j < m; ++j) std::swap(at(G, m, k, j), at(G, m, piv, j));
-      for (int i = 0; i < k; ++i) std::swap(at(R, m, i, k), at(R, m, i, piv));
-      std::swap(perm[k], perm[piv]);
-    }
-    const double rkk = std::sqrt(at(G, m, k, k));
-    at(R, m, k, k) = rkk;
-    for (int j = k + 1; j < m; ++j) at(R, m, k, j) = at(G, m, k, j) / rkk;
-    for (int i = k + 1; i < m; ++i)
-      for (int j = k + 1; j < m; ++j) at(G, m, i, j) -= at(R, m, k, i) * at(R, m, k, j);
-    rank = k + 1;
-  }
-  return rank;
-}
-
-// Plain Cholesky G = R^T R (R upper).  Returns false when G is not (numerically) s.p.d.
-inline bool cholesky_upper(const Mat& G, int m, Mat& R) {
-  R.assign(static_cast<size_t>(m) * m, 0.0);
-  for (int j = 0; j < m; ++j) {
-    for (int i = 0; i <= j; ++i) {
-      double s = at(G, m, i, j);
-      for (int k = 0; k < i; ++k) s -= at(R, m, k, i) * at(R, m, k, j);
-      if (i == j) {
-        if (!(s > 0.0)) return false;
-        at(R, m, j, j) = std::sqrt(s);
-      } else {
-        at(R, m, i, j) = s / at(R, m, i, i);
-      }
-    }
-  }
-  return true;
-}
-
-// Inverse of an upper triangular r x r matrix stored with leading dimension ld.
-inline Mat upper_inverse(const Mat& R, int r, int ld) {
-  Mat X(static_cast<size_t>(r) * r, 0.0);
-  for (int j = r - 1; j >= 0; --j) {
-    at(X, r, j, j) = 1.0 / at(R, ld, j, j);
-    for (int i = j - 1; i >= 0; --i) {
-      double s = 0.0;
-      for (int k = i + 1; k <= j; ++k) s += at(R, ld, i, k) * at(X, r, k, j);
-      at(X, r, i, j) = -s / at(R, ld, i, i);
-    }
-  }
-  return X;
-}
-
-// R factor (n x n upper) of a Householder QR of A (m x n, m >= n); A is destroyed.
-inline Mat householder_r(Mat A, int m, int n) {
-  const int kmax = std::min(m, n);
-  for (int k = 0; k < kmax; ++k) {
-    double norm = 0.0;
-    for (int i = k; i < m; ++i) norm += at(A, m, i, k) * at(A, m, i, k);
-    norm = std::sqrt(norm);
-    if (norm == 0.0) continue;
-    const double alpha = at(A, m, k, k) > 0 ? -norm : norm;
-    std::vector<double> v(m - k);
-    for (int i = k; i < m; ++i) v[i - k] = at(A, m, i, k);
-    v[0] -= alpha;
-    double vn = 0.0;
-    for (double x : v) vn += x * x;
-    if (vn == 0.0) continue;
-    for (int j = k; j < n; ++j) {
-      double s = 0.0;
-      for (int i = k; i < m; ++i) s += v[i - k] * at(A, m, i, j);
-      s = 2.0 * s / vn;
-      for (int i = k; i < m; ++i) at(A, m, i, j) -= s * v[i - k];
-    }
-  }
-  Mat R(static_cast<size_t>(n) * n, 0.0);
-  for (int j = 0; j < n; ++j)
-    for (int i = 0; i <= std::min(j, m - 1); ++i) at(R, n, i, j) = at(A, m, i, j);
-  return R;
-}
-
 // One-sided Jacobi SVD of A (m x n, m >= n): A = U diag(s) V^T, s descending.
 inline void jacobi_svd(Mat A, int m, int n, std::vector<double>& s, Mat& U, Mat& V) {
   V.assign(static_cast<size_t>(n) * n, 0.0);
