@@ -871,6 +871,8 @@ int stkg_heat_destroy(stkg_heat* h) {
     if (h->stream) cudaStreamSynchronize(h->stream);
     else cudaDeviceSynchronize();
     if (h->pinned) cudaFreeHost(h->pinned);
+    for (int c = 0; c < 2; ++c)
+      for (auto e : h->prof_ev[c]) cudaEventDestroy(e);  // profiling left enabled
     for (int b = 0; b < 2; ++b) {
       if (h->ev_h2d[b]) cudaEventDestroy(h->ev_h2d[b]);
       if (h->ev_comp[b]) cudaEventDestroy(h->ev_comp[b]);
