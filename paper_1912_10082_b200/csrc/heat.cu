@@ -57,12 +57,23 @@ __global__ void __launch_bounds__(256) heat_scan_kernel(
   const double wi = wgt(i);  // 1 in the dense backend
   double y = l0 > 0 ? carry[i] : 0.0;
   double* col = Y + i;
-  constexpr int U = 8;
+#ifndef STKG_SCAN_U
+#define STKG_SCAN_U 8
+#endif
+  constexpr int U = STKG_SCAN_U;
   int64_t j = 0;
-  for (; j + U <= ntc; j += U) {
-    double g[U];
+  // software-pipelined: the next block's U loads are in flight while this block's
+  // dependent recurrence runs
+  double g[U];
+  if (ntc >= U) {
 #pragma unroll
-    for (int u = 0; u < U; ++u) g[u] = __ldcs(col + (j + u) * nx);
+    for (int u = 0; u < U; ++u) g[u] = __ldcs(col + u * nx);
+  }
+  for (; j + U <= ntc; j += U) {
+    double gn[U];
+    const bool more = j + 2 * U <= ntc;
+#pragma unroll
+    for (int u = 0; u < U; ++u) gn[u] = more ? __ldcs(col + (j + U + u) * nx) : 0.0;
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t l = l0 + j + u;
@@ -72,6 +83,8 @@ __global__ void __launch_bounds__(256) heat_scan_kernel(
       y = rhs / piv;
       __stcs(col + (j + u) * nx, wi * y);
     }
+#pragma unroll
+    for (int u = 0; u < U; ++u) g[u] = gn[u];
   }
   for (; j < ntc; ++j) {
     const int64_t l = l0 + j;
