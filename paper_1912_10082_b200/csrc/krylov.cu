@@ -45,8 +45,25 @@ __global__ void __launch_bounds__(kReduceThreads) gemv_t_kernel(
   __shared__ double red[kReduceThreads / 32];
   const int c0 = blockIdx.y * kGemvCols;
   double s[kGemvCols] = {0.0, 0.0, 0.0, 0.0};
-  for (int64_t i = int64_t(blockIdx.x) * kReduceThreads + threadIdx.x; i < N;
-       i += int64_t(gridDim.x) * kReduceThreads) {
+  // kRowU rows per step: their 5 kRowU loads are independent and in flight together
+  constexpr int kRowU = 4;
+  const int64_t stride = int64_t(gridDim.x) * kReduceThreads;
+  int64_t i = int64_t(blockIdx.x) * kReduceThreads + threadIdx.x;
+  for (; i + (kRowU - 1) * stride < N; i += kRowU * stride) {
+    double wi[kRowU], v[kRowU][kGemvCols];
+#pragma unroll
+    for (int r = 0; r < kRowU; ++r) {
+      wi[r] = w[i + r * stride];
+#pragma unroll
+      for (int c = 0; c < kGemvCols; ++c)
+        v[r][c] = c0 + c < m ? V[int64_t(c0 + c) * N + i + r * stride] : 0.0;
+    }
+#pragma unroll
+    for (int r = 0; r < kRowU; ++r)
+#pragma unroll
+      for (int c = 0; c < kGemvCols; ++c) s[c] += v[r][c] * wi[r];
+  }
+  for (; i < N; i += stride) {
     const double wi = w[i];
 #pragma unroll
     for (int c = 0; c < kGemvCols; ++c)
@@ -69,13 +86,13 @@ __global__ void __launch_bounds__(kReduceThreads) gemv_n_update_kernel(
        i += int64_t(gridDim.x) * kReduceThreads) {
     double acc = w[i];
     int c = 0;
-    for (; c + 4 <= m; c += 4) {
-      const double v0 = V[int64_t(c) * N + i], v1 = V[int64_t(c + 1) * N + i];
-      const double v2 = V[int64_t(c + 2) * N + i], v3 = V[int64_t(c + 3) * N + i];
-      acc -= h[c] * v0;
-      acc -= h[c + 1] * v1;
-      acc -= h[c + 2] * v2;
-      acc -= h[c + 3] * v3;
+    // 8 columns per step: 8 independent loads in flight per thread
+    for (; c + 8 <= m; c += 8) {
+      double v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q] = V[int64_t(c + q) * N + i];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc -= h[c + q] * v[q];
     }
     for (; c < m; ++c) acc -= h[c] * V[int64_t(c) * N + i];
     w[i] = acc;
