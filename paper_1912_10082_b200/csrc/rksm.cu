@@ -246,6 +246,39 @@ class Rksm {
     return H;
   }
 
+  // Several Grams with one device->host read: gram_batch({{V, k, W, b}, ...}).
+  struct GramReq {
+    const double* V;
+    int64_t k;
+    const double* W;
+    int64_t b;
+  };
+  std::vector<hla::Mat> gram_batch(const std::vector<GramReq>& reqs) {
+    size_t total = 0;
+    for (const auto& r : reqs) total += static_cast<size_t>(r.k * r.b);
+    std::vector<hla::Mat> out(reqs.size());
+    if (total == 0) {
+      for (size_t q = 0; q < reqs.size(); ++q) out[q].assign(static_cast<size_t>(reqs[q].k * reqs[q].b), 0.0);
+      return out;
+    }
+    double* hd = scratch(kSlotGram, total);
+    size_t off = 0;
+    for (const auto& r : reqs) {
+      if (r.k > 0 && r.b > 0) gram_dev(r.V, r.k, r.W, r.b, hd + off);
+      off += static_cast<size_t>(r.k * r.b);
+    }
+    double* hp = pinned(total);
+    STKG_CUDA_CHECK(cudaMemcpyAsync(hp, hd, sizeof(double) * total, cudaMemcpyDeviceToHost, s_));
+    STKG_CUDA_CHECK(cudaStreamSynchronize(s_));
+    off = 0;
+    for (size_t q = 0; q < reqs.size(); ++q) {
+      const size_t n = static_cast<size_t>(reqs[q].k * reqs[q].b);
+      out[q].assign(hp + off, hp + off + n);
+      off += n;
+    }
+    return out;
+  }
+
   // W(:, 0:b) -= V(:, 0:k) Hd (k x b, device, ld k); asynchronous.
   void update_dev(double* W, int64_t b, const double* V, int64_t k, const double* Hd) {
     if (k == 0 || b == 0) return;
@@ -364,18 +397,16 @@ class Rksm {
     for (int64_t j = 0; j < b; ++j) orig[j] = static_cast<int>(j);
     std::vector<double> norm0(b);
     double maxpiv = 0.0;
-    {
-      hla::Mat G = gram(W, b, W, b);
-      for (int64_t j = 0; j < b; ++j) {
-        norm0[j] = std::sqrt(std::max(G[j * b + j], 0.0));
-        maxpiv = std::max(maxpiv, norm0[j]);
-      }
+    hla::Mat G0 = gram(W, b, W, b);  // also the first step's Gram (saves a round trip)
+    for (int64_t j = 0; j < b; ++j) {
+      norm0[j] = std::sqrt(std::max(G0[j * b + j], 0.0));
+      maxpiv = std::max(maxpiv, norm0[j]);
     }
     double* tmp = scratch(kSlotTmp, static_cast<size_t>(n_));
     int r = 0;
     while (r < b && maxpiv > 0.0) {
       const int64_t m = b - r;
-      hla::Mat G = gram(W + r * n_, m, W + r * n_, m);
+      hla::Mat G = r == 0 ? G0 : gram(W + r * n_, m, W + r * n_, m);
       int64_t p = 0;
       for (int64_t j = 1; j < m; ++j)
         if (G[j * m + j] > G[p * m + p]) p = j;
@@ -391,15 +422,15 @@ class Rksm {
       }
       double* q = W + r * n_;
       if (nrm < 0.5 * norm0[orig[r]]) {  // DGKS: cancellation -> one more full projection
-        if (k_prev > 0) update(q, 1, prev, k_prev, gram(prev, k_prev, q, 1));
-        if (r > 0) update(q, 1, W, r, gram(W, r, q, 1));
+        // (coefficients stay on the device: no host round trip until the norm)
+        if (k_prev > 0) project_out(q, 1, prev, k_prev);
+        if (r > 0) project_out(q, 1, W, r);
         nrm = std::sqrt(std::max(gram(q, 1, q, 1)[0], 0.0));
         if (!(nrm > tol * maxpiv)) break;
       }
       scale(q, 1.0 / nrm);
       if (m > 1)
-        for (int pass = 0; pass < 2; ++pass)
-          update(q + n_, m - 1, q, 1, gram(q, 1, q + n_, m - 1));
+        for (int pass = 0; pass < 2; ++pass) project_out(q + n_, m - 1, q, 1);
       ++r;
     }
     if (Rout) {
@@ -415,6 +446,14 @@ class Rksm {
   void scale(double* x, double alpha) {
     scale_kernel<<<kEw, 256, 0, s_>>>(x, n_, alpha);
     STKG_CUDA_CHECK(cudaGetLastError());
+  }
+
+  // W(:, 0:b) -= V(:, 0:k) (V^T W) with the coefficients kept on the device.
+  void project_out(double* W, int64_t b, const double* V, int64_t k) {
+    if (k == 0 || b == 0) return;
+    double* hd = scratch(kSlotGs, static_cast<size_t>(k * b));
+    gram_dev(V, k, W, b, hd);
+    update_dev(W, b, V, k, hd);
   }
 
   // Two block classical Gram-Schmidt passes of W (n x b) against V(:, 0:k) (:213)
@@ -575,8 +614,12 @@ void Rksm::run(int64_t rank, const double* L, const double* R, double* U_left, d
     MV.cols = AV.cols = k;
     // --- projections V^T M V, V^T A V grown by the new columns (:180-183)
     {
-      hla::Mat cm = gram(V.col(0), k, MV.col(k_done), b);  // k x b
-      hla::Mat ca = gram(V.col(0), k, AV.col(k_done), b);
+      // one device->host read for V^T M V_new, V^T A V_new and V_new^T f1
+      auto g3 = gram_batch({{V.col(0), k, MV.col(k_done), b},
+                            {V.col(0), k, AV.col(k_done), b},
+                            {V.col(k_done), b, V.col(0), rf}});
+      hla::Mat& cm = g3[0];  // k x b
+      hla::Mat& ca = g3[1];
       hla::Mat nhm(static_cast<size_t>(k * k)), nha(static_cast<size_t>(k * k));
       for (int64_t j = 0; j < k_done; ++j)
         for (int64_t i = 0; i < k_done; ++i) {
@@ -608,7 +651,7 @@ void Rksm::run(int64_t rank, const double* L, const double* R, double* U_left, d
       hla::Mat nf(static_cast<size_t>(k * rf));
       for (int64_t j = 0; j < rf; ++j)
         for (int64_t i = 0; i < k_done; ++i) nf[j * k + i] = vtf1[j * k_done + i];
-      hla::Mat cf = gram(V.col(k_done), b, V.col(0), rf);  // b x rf
+      hla::Mat& cf = g3[2];  // b x rf
       for (int64_t j = 0; j < rf; ++j)
         for (int64_t i = 0; i < b; ++i) nf[j * k + k_done + i] = cf[j * b + i];
       vtf1.swap(nf);
@@ -639,9 +682,12 @@ void Rksm::run(int64_t rank, const double* L, const double* R, double* U_left, d
       // new rows for old columns: Q_new^T [f1 | MV_old | AV_old]
       const int64_t qn = q - q_old;
       if (qn > 0) {
-        hla::Mat a1 = gram(Q.col(q_old), qn, V.col(0), rf);
-        hla::Mat a2 = k_done > 0 ? gram(Q.col(q_old), qn, MV.col(0), k_done) : hla::Mat();
-        hla::Mat a3 = k_done > 0 ? gram(Q.col(q_old), qn, AV.col(0), k_done) : hla::Mat();
+        auto ga = gram_batch({{Q.col(q_old), qn, V.col(0), rf},
+                              {Q.col(q_old), qn, MV.col(0), k_done},
+                              {Q.col(q_old), qn, AV.col(0), k_done}});
+        hla::Mat& a1 = ga[0];
+        hla::Mat& a2 = ga[1];
+        hla::Mat& a3 = ga[2];
         for (int64_t j = 0; j < rf; ++j)
           for (int64_t i = 0; i < qn; ++i) nT[j * q + q_old + i] = a1[j * qn + i];
         for (int64_t j = 0; j < k_done; ++j)
@@ -651,8 +697,9 @@ void Rksm::run(int64_t rank, const double* L, const double* R, double* U_left, d
           }
       }
       // new columns (all rows): Q^T MV_new, Q^T AV_new
-      hla::Mat b2 = gram(Q.col(0), q, MV.col(k_done), b);
-      hla::Mat b3 = gram(Q.col(0), q, AV.col(k_done), b);
+      auto gb = gram_batch({{Q.col(0), q, MV.col(k_done), b}, {Q.col(0), q, AV.col(k_done), b}});
+      hla::Mat& b2 = gb[0];
+      hla::Mat& b3 = gb[1];
       for (int64_t j = 0; j < b; ++j)
         for (int64_t i = 0; i < q; ++i) {
           nT[(rf + k_done + j) * q + i] = b2[j * q + i];
