@@ -22,8 +22,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc" if Path("/usr/local/cud
 CUDA_SOURCES = ["heat.cu", "wave.cu", "krylov.cu", "rksm.cu", "runtime.cu"]
 HOST_SOURCES = ["host_assembly.cpp", "errors.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
-                     "--expt-relaxed-constexpr"]
+NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler",
+                     "-fopenmp", "-Xptxas", "-v", "--expt-relaxed-constexpr"]
 CXX_FLAGS = ["-O3", "-std=c++17", "-fPIC", "-fopenmp"]
 
 

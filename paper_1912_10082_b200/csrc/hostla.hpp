@@ -19,6 +19,8 @@ inline double at(const Mat& a, int ld, int i, int j) { return a[static_cast<size
 // C (m x p) = A (m x q) * B (q x p)
 inline Mat matmul(const Mat& A, const Mat& B, int m, int q, int p) {
   Mat C(static_cast<size_t>(m) * p, 0.0);
+  // columns of C are independent: threads split them once the product is large enough
+#pragma omp parallel for schedule(static) if (static_cast<double>(m) * q * p > 4e6)
   for (int j = 0; j < p; ++j)
     for (int l = 0; l < q; ++l) {
       const double b = B[static_cast<size_t>(j) * q + l];

@@ -538,6 +538,29 @@ hla::Mat projected_heat(const hla::Mat& X, const std::vector<double>& lam, const
   return hla::matmul(X, yt, k, k, nt);
 }
 
+// Optional per-phase wall-clock breakdown (STKG_RKSM_TIMING=1: synchronises at each mark
+// and prints the totals to stderr at the end of the solve).
+struct PhaseTimer {
+  bool on = std::getenv("STKG_RKSM_TIMING") != nullptr;
+  cudaStream_t s = nullptr;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  void mark(int phase) {
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    const auto t = std::chrono::steady_clock::now();
+    acc[phase] += std::chrono::duration<double>(t - t0).count();
+    t0 = t;
+  }
+  void print() const {
+    if (!on) return;
+    static const char* names[8] = {"apply M,A", "projections", "residual basis", "T update",
+                                   "pencil+projected", "residual norm", "shifted solve",
+                                   "expansion GS+QR"};
+    for (int i = 0; i < 8; ++i) std::fprintf(stderr, "rksm %-18s %8.3f s\n", names[i], acc[i]);
+  }
+};
+
 void report_push(stkg_report* rep, double v) {
   if (!rep) return;
   if (rep->rel_res_history && rep->history_length < rep->history_capacity)
@@ -604,14 +627,18 @@ void Rksm::run(int64_t rank, const double* L, const double* R, double* U_left, d
   std::vector<double> history;
   const int total_iters = o_.fixed_iters > 0 ? o_.fixed_iters : o_.maxit;
   int it = 0;
+  PhaseTimer tm;
+  tm.s = s_;
   for (it = 1; it <= total_iters; ++it) {
     const int64_t k = V.cols, b = k - k_done;
+    tm.mark(7);
     // --- M V_new, A V_new
     MV.reserve(k, s_);
     AV.reserve(k, s_);
     apply_M(V.col(k_done), MV.col(k_done), b);
     apply_A(V.col(k_done), AV.col(k_done), b);
     MV.cols = AV.cols = k;
+    tm.mark(0);
     // --- projections V^T M V, V^T A V grown by the new columns (:180-183)
     {
       // one device->host read for V^T M V_new, V^T A V_new and V_new^T f1
@@ -656,6 +683,7 @@ void Rksm::run(int64_t rank, const double* L, const double* R, double* U_left, d
         for (int64_t i = 0; i < b; ++i) nf[j * k + k_done + i] = cf[j * b + i];
       vtf1.swap(nf);
     }
+    tm.mark(1);
     // --- residual basis: orthonormalise [MV_new, AV_new] against Q and append
     const int64_t q_old = Q.cols;
     {
@@ -670,6 +698,7 @@ void Rksm::run(int64_t rank, const double* L, const double* R, double* U_left, d
         Q.cols += add;
       }
     }
+    tm.mark(2);
     // --- T = Q^T [f1 | MV | AV]: (q x m), grown by new rows and new columns
     {
       const int64_t q = Q.cols, m = rf + 2 * k, m_old = rf + 2 * k_done;
@@ -708,6 +737,7 @@ void Rksm::run(int64_t rank, const double* L, const double* R, double* U_left, d
       T.swap(nT);
     }
     k_done = k;
+    tm.mark(3);
     // --- projected pencil and projected heat solve (:184-188)
     hla::Mat X(static_cast<size_t>(k * k));
     std::vector<double> lam(k);
@@ -720,6 +750,7 @@ void Rksm::run(int64_t rank, const double* L, const double* R, double* U_left, d
     hla::Mat g = hla::matmul(vtf1, f2T, static_cast<int>(k), rf, nt);  // k x nt
     y = projected_heat(X, lam, h_, g, static_cast<int>(k));
     kfinal = k;
+    tm.mark(4);
     // --- factored residual (:190-191): ||T W^T|| with W = [f2 | -D^T y^T | -C^T y^T]
     {
       const int64_t q = Q.cols, m = rf + 2 * k;
@@ -751,12 +782,14 @@ void Rksm::run(int64_t rank, const double* L, const double* R, double* U_left, d
         break;
       }
     }
+    tm.mark(5);
     // --- next pole and space expansion (:193-224)
     const double sigma = shifts.empty() ? -lam_max : next_shift(shifts, ritz, lam_min, lam_max);
     shifts.push_back(sigma);
     V.reserve(k + newest_b, s_);
     double* w = V.col(k);
     shifted_solve(V.col(newest0), w, newest_b, sigma);
+    tm.mark(6);
     block_gs(w, newest_b, V.col(0), k);
     const int add = orthonormalize(w, newest_b, 1e-12, nullptr, V.col(0), k);
     if (add == 0) {
@@ -767,6 +800,8 @@ void Rksm::run(int64_t rank, const double* L, const double* R, double* U_left, d
     newest_b = add;
     V.cols = k + add;
   }
+  tm.mark(7);
+  tm.print();
   if (rep) rep->iterations = std::min(it, total_iters);
   if (const char* dir = std::getenv("STKG_RKSM_DUMP")) {  // debugging aid: raw basis dump
     auto dump = [&](const char* name, const double* d, int64_t count, bool device) {
