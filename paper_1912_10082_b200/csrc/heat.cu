@@ -884,6 +884,7 @@ int stkg_heat_destroy(stkg_heat* h) {
     if (h->stream) cudaStreamSynchronize(h->stream);
     else cudaDeviceSynchronize();
     if (h->pinned) cudaFreeHost(h->pinned);
+    if (h->rk_pin) cudaFreeHost(h->rk_pin);
     for (int c = 0; c < 2; ++c)
       for (auto e : h->prof_ev[c]) cudaEventDestroy(e);  // profiling left enabled
     for (int b = 0; b < 2; ++b) {

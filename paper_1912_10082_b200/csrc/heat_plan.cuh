@@ -52,6 +52,12 @@ struct stkg_heat {
   std::vector<double> lam_h[3], d_diag_h, d_sup_h, c_diag_h, c_sup_h;
   std::vector<double> m_diag_h[3], m_off_h[3], a_diag_h[3], a_off_h[3];
   bool has_operator = false;
+  // rational Krylov workspace (rksm.cu), kept across calls so that repeated solves do not
+  // allocate: growable device scratch slots, fixed reduction buffers, pinned staging
+  DevBuf rk_slots[16];
+  DevBuf rk_partials, rk_hdev, rk_ones, rk_zeros;
+  double* rk_pin = nullptr;
+  size_t rk_pin_n = 0;
   DevBuf m_diag[3], m_off[3], a_diag[3], a_off[3];
   DevBuf scratch;   // nx * nt, device solve
   DevBuf lfac;      // 2 * nx * rank, transformed load factors (factored solve)

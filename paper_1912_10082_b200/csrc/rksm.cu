@@ -177,20 +177,21 @@ struct Block {
 
 class Rksm {
  public:
-  Rksm(stkg_heat& h, const stkg_rksm_options& o) : h_(h), o_(o), n_(h.nx), nt_(h.nt) {
+  Rksm(stkg_heat& h, const stkg_rksm_options& o)
+      : h_(h), o_(o), n_(h.nx), nt_(h.nt), partials_(h.rk_partials), hdev_(h.rk_hdev),
+        ones_(h.rk_ones), zeros_(h.rk_zeros), slots_(h.rk_slots), hpin_(h.rk_pin),
+        hpin_n_(h.rk_pin_n) {
     s_ = h.stream;
-    partials_.alloc(static_cast<size_t>(kReduceBlocks) * 16 * 1024);
-    hdev_.alloc(16 * 1024);
-    ones_.alloc(kTsRhs * 2);
-    zeros_.alloc(kTsRhs * 2);
-    std::vector<double> one(kTsRhs * 2, 1.0), zero(kTsRhs * 2, 0.0);
-    ones_.upload(one.data(), one.size(), s_);
-    zeros_.upload(zero.data(), zero.size(), s_);
-    STKG_CUDA_CHECK(cudaStreamSynchronize(s_));
-  }
-
-  ~Rksm() {
-    if (hpin_) cudaFreeHost(hpin_);
+    if (!partials_.p) {  // first use of this plan: fixed buffers
+      partials_.alloc(static_cast<size_t>(kReduceBlocks) * 16 * 1024);
+      hdev_.alloc(16 * 1024);
+      ones_.alloc(kTsRhs * 2);
+      zeros_.alloc(kTsRhs * 2);
+      std::vector<double> one(kTsRhs * 2, 1.0), zero(kTsRhs * 2, 0.0);
+      ones_.upload(one.data(), one.size(), s_);
+      zeros_.upload(zero.data(), zero.size(), s_);
+      STKG_CUDA_CHECK(cudaStreamSynchronize(s_));
+    }
   }
 
   // ------------------------------------------------------------- device helpers ----
@@ -475,12 +476,14 @@ class Rksm {
   stkg_rksm_options o_;
   int64_t n_, nt_;
   cudaStream_t s_;
-  DevBuf partials_, hdev_, ones_, zeros_;
+  // workspace lives in the plan (stkg_heat::rk_*) and persists across calls
+  DevBuf &partials_, &hdev_, &ones_, &zeros_;
   enum { kSlotGram, kSlotUpd, kSlotGemm, kSlotT0, kSlotT1, kSlotW0, kSlotTmp, kSlotGs, kSlotRes,
          kSlots };
-  DevBuf slots_[kSlots];
-  double* hpin_ = nullptr;
-  size_t hpin_n_ = 0;
+  static_assert(kSlots <= 16, "stkg_heat::rk_slots");
+  DevBuf* slots_;
+  double*& hpin_;
+  size_t& hpin_n_;
 };
 
 // adaptive_next_shift (stk/rksm.hpp:67-102): 200 log-spaced candidates in
