@@ -3,9 +3,13 @@
 // through the tensor generalized eigenbasis, i.e. solve_projected_heat_with
 // (stk/sylvester.hpp:117-142) with X = X_x (x) X_y (x) X_z:
 //   K2  forward transforms  G~ = X^T F      (:126)    -> batched DMMA GEMMs per axis
+//                                                        (dense backend), or FP64 fast
+//                                                        sine transforms (P1_DST backend:
+//                                                        dst.cuh, dst_half.cuh)
 //   K3  per-mode recurrence (D + lambda_i C)^T y_i = g~_i   (:128-140) -> mode-parallel scan
 //   K2  inverse transforms  U = X Y~        (:141)
-// and the K1 operator/residual kernel  out = M U D + A U C  (KronOp::apply, :32-38).
+// and the K1 operator/residual kernel  out = M U D + A U C  (KronOp::apply, :32-38), the
+// factored-load solve, and the host-buffer pipeline (stkg_heat_solve_host).
 #include <algorithm>
 #include <chrono>
 #include <cmath>
