@@ -160,14 +160,38 @@ struct Tri {  // symmetric tridiagonal 1D factor
   }
 };
 
-// Point tiles of 256 per CTA (x slowest ... z fastest); the U tile with a 1-wide halo is
-// staged in shared memory by cp.async in a 6-deep ring over time slices (5 slices in
-// flight while slice l is applied), so every U and F value crosses HBM once and the
+// Tiles of 256 PT points per CTA (x slowest ... fastest axis last); each of the 256
+// threads owns PT consecutive points along the fastest axis, so the per-slice overheads
+// (ring wait, barrier, copies, time coefficients) are paid once per PT points and a
+// thread's 3-point stencils along the fastest axis share loaded values.  The U tile with a
+// 1-wide halo (and the F tile for the residual) is staged in shared memory by cp.async in a
+// kStages-deep ring over time slices, so every U and F value crosses HBM once and the
 // loads for future slices cover the HBM latency.
+// Measured (tools/k1_probe.py): 2 points per thread is 5% faster on cfg3 (2D) and 21% on
+// cfg5 (3D) than 1; 4 raises registers past two CTAs per SM and loses; 1D keeps 1 (its
+// grids are small and a wider tile idles).
+template <int NDIM>
+constexpr int apply_pt() { return NDIM == 1 ? 1 : 2; }
 template <int NDIM> struct ApplyTile;
-template <> struct ApplyTile<1> { static constexpr int BX = 256, BY = 1, BZ = 1; };
-template <> struct ApplyTile<2> { static constexpr int BX = 8, BY = 32, BZ = 1; };
-template <> struct ApplyTile<3> { static constexpr int BX = 4, BY = 4, BZ = 16; };
+template <> struct ApplyTile<1> {
+  static constexpr int PT = apply_pt<1>(), BX = 256 * PT, BY = 1, BZ = 1, kStages = 6;
+};
+template <> struct ApplyTile<2> {
+  static constexpr int PT = apply_pt<2>(), BX = 8, BY = 32 * PT, BZ = 1, kStages = 6;
+};
+template <> struct ApplyTile<3> {
+  static constexpr int PT = apply_pt<3>(), BX = 4, BY = 4, BZ = 16 * PT, kStages = 6;
+};
+
+template <int NDIM, bool RESIDUAL>
+struct ApplySmem {
+  using T = ApplyTile<NDIM>;
+  static constexpr int HX = T::BX + 2, HY = T::BY + (NDIM >= 2 ? 2 : 0);
+  static constexpr int HZ = T::BZ + (NDIM == 3 ? 2 : 0);
+  static constexpr int TE = HX * HY * HZ;              // halo tile per slice
+  static constexpr int TF = RESIDUAL ? 256 * T::PT : 0;  // F tile per slice
+  static constexpr size_t kBytes = size_t(T::kStages) * (TE + TF) * sizeof(double);
+};
 
 template <int NDIM, bool RESIDUAL>
 __global__ void __launch_bounds__(256) heat_apply_kernel(
@@ -177,31 +201,34 @@ __global__ void __launch_bounds__(256) heat_apply_kernel(
     const double* __restrict__ c_diag, const double* __restrict__ c_sup,
     double* __restrict__ partials) {
   using T = ApplyTile<NDIM>;
-  constexpr int SY = NDIM >= 2 ? 3 : 1, SZ = NDIM == 3 ? 3 : 1;
-  constexpr int HX = T::BX + 2, HY = T::BY + (NDIM >= 2 ? 2 : 0), HZ = T::BZ + (NDIM == 3 ? 2 : 0);
-  constexpr int TE = HX * HY * HZ;
-  constexpr int kStages = 6;  // slices in flight per CTA: enough bytes to cover HBM latency
-  __shared__ double su[kStages][TE];
-  __shared__ double sf[kStages][256];
+  using SM = ApplySmem<NDIM, RESIDUAL>;
+  constexpr int kPT = T::PT;
+  constexpr int HY = SM::HY, HZ = SM::HZ, TE = SM::TE, TF = SM::TF;
+  constexpr int kStages = T::kStages;
+  extern __shared__ __align__(16) double asmem[];
+  double* su = asmem;                      // [kStages][TE]
+  double* sf = asmem + kStages * TE;       // [kStages][TF]
 
-  const int64_t tiles_x = (n0 + T::BX - 1) / T::BX, tiles_y = (n1 + T::BY - 1) / T::BY;
-  const int64_t tiles_z = (n2 + T::BZ - 1) / T::BZ;
-  int64_t b = blockIdx.x;
-  const int64_t tz = b % tiles_z;
-  b /= tiles_z;
-  const int64_t ty = b % tiles_y;
-  const int64_t tx = b / tiles_y;
-  (void)tiles_x;
+  const int64_t tiles_y = (n1 + T::BY - 1) / T::BY, tiles_z = (n2 + T::BZ - 1) / T::BZ;
+  int64_t blk = blockIdx.x;
+  const int64_t tz = blk % tiles_z;
+  blk /= tiles_z;
+  const int64_t ty = blk % tiles_y;
+  const int64_t tx = blk / tiles_y;
   const int64_t x0 = tx * T::BX, y0 = ty * T::BY, z0 = tz * T::BZ;
   const int tid = threadIdx.x;
-  const int lx = tid / (T::BY * T::BZ), ly = (tid / T::BZ) % T::BY, lz = tid % T::BZ;
-  const int64_t ix = x0 + lx, iy = y0 + ly, iz = z0 + lz;
-  const bool valid = ix < n0 && iy < n1 && iz < n2;
+  constexpr int TYT = NDIM == 2 ? T::BY / kPT : (NDIM == 3 ? T::BY : 1);
+  constexpr int TZT = NDIM == 3 ? T::BZ / kPT : 1;
+  const int lx = tid / (TYT * TZT), ly = (tid / TZT) % TYT, lz = tid % TZT;
+  const int64_t ix = x0 + (NDIM == 1 ? kPT * lx : lx);
+  const int64_t iy = y0 + (NDIM == 2 ? kPT * ly : ly);
+  const int64_t iz = z0 + (NDIM == 3 ? kPT * lz : 0);
   const int64_t nx = n0 * n1 * n2;
-  const int64_t p = (ix * n1 + iy) * n2 + iz;
+  const int64_t nf = NDIM == 1 ? n0 : (NDIM == 2 ? n1 : n2);
+  const int64_t ifast = NDIM == 1 ? ix : (NDIM == 2 ? iy : iz);
+  const bool row_ok = ix < n0 && iy < n1 && iz < n2;
+  const int64_t p0 = (ix * n1 + iy) * n2 + iz;
 
-  // Each thread copies at most kPer halo elements per slice; their in-slice offsets and
-  // validity are fixed for the whole time loop (computed once).
   constexpr int kPer = (TE + 255) / 256;
   int64_t hoff[kPer];
   uint32_t hok = 0;
@@ -216,6 +243,19 @@ __global__ void __launch_bounds__(256) heat_apply_kernel(
     hoff[k] = ok ? (gx * n1 + gy) * n2 + gz : 0;
     if (ok) hok |= 1u << k;
   }
+  int64_t foff[kPT];
+  uint32_t fok = 0;
+  if constexpr (RESIDUAL) {
+#pragma unroll
+    for (int k = 0; k < kPT; ++k) {
+      const int e = tid + 256 * k;
+      const int fx = e / (T::BY * T::BZ), fy = (e / T::BZ) % T::BY, fz = e % T::BZ;
+      const int64_t gx = x0 + fx, gy = y0 + fy, gz = z0 + fz;
+      const bool ok = gx < n0 && gy < n1 && gz < n2;
+      foff[k] = ok ? (gx * n1 + gy) * n2 + gz : 0;
+      if (ok) fok |= 1u << k;
+    }
+  }
   auto load_slice = [&](int stage, int64_t l) {
     const bool lin = l < nt;
     const double* Ul = U + l * nx;
@@ -224,36 +264,41 @@ __global__ void __launch_bounds__(256) heat_apply_kernel(
       const int e = tid + 256 * k;
       if (e < TE) {
         const bool ok = lin && ((hok >> k) & 1u);
-        cp_async8(&su[stage][e], ok ? Ul + hoff[k] : U, ok);
+        cp_async8(&su[stage * TE + e], ok ? Ul + hoff[k] : U, ok);
       }
     }
-    if (RESIDUAL) {
-      const bool ok = lin && valid;
-      cp_async8(&sf[stage][tid], ok ? F + l * nx + p : F, ok);
+    if constexpr (RESIDUAL) {
+      const double* Fl = F + l * nx;
+#pragma unroll
+      for (int k = 0; k < kPT; ++k) {
+        const bool ok = lin && ((fok >> k) & 1u);
+        cp_async8(&sf[stage * TF + tid + 256 * k], ok ? Fl + foff[k] : F, ok);
+      }
     }
   };
 
-  // 1D weights of the point (zero outside the grid)
-  double wmx[3], wax[3], wmy[SY], way[SY], wmz[SZ], waz[SZ];
+  auto wts = [&](const Tri& t, int64_t i, int64_t n, int q, bool valid) {
+    return (valid && i + q - 1 >= 0 && i + q - 1 < n) ? t.w(i, q - 1) : 0.0;
+  };
+  double wmf[kPT][3], waf[kPT][3];
+  const Tri& mf = NDIM == 1 ? m0 : (NDIM == 2 ? m1 : m2);
+  const Tri& af = NDIM == 1 ? a0 : (NDIM == 2 ? a1 : a2);
+#pragma unroll
+  for (int p = 0; p < kPT; ++p) {
+    const bool v = row_ok && ifast + p < nf;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      wmf[p][q] = wts(mf, ifast + p, nf, q, v);
+      waf[p][q] = wts(af, ifast + p, nf, q, v);
+    }
+  }
+  double wmx[3], wax[3], wmy[3], way[3];
 #pragma unroll
   for (int q = 0; q < 3; ++q) {
-    const bool in = valid && ix + q - 1 >= 0 && ix + q - 1 < n0;
-    wmx[q] = in ? m0.w(ix, q - 1) : 0.0;
-    wax[q] = in ? a0.w(ix, q - 1) : 0.0;
-  }
-#pragma unroll
-  for (int q = 0; q < SY; ++q) {
-    const int d = SY == 1 ? 0 : q - 1;
-    const bool in = valid && iy + d >= 0 && iy + d < n1;
-    wmy[q] = NDIM >= 2 ? (in ? m1.w(iy, d) : 0.0) : 1.0;
-    way[q] = NDIM >= 2 ? (in ? a1.w(iy, d) : 0.0) : 0.0;
-  }
-#pragma unroll
-  for (int q = 0; q < SZ; ++q) {
-    const int d = SZ == 1 ? 0 : q - 1;
-    const bool in = valid && iz + d >= 0 && iz + d < n2;
-    wmz[q] = NDIM == 3 ? (in ? m2.w(iz, d) : 0.0) : 1.0;
-    waz[q] = NDIM == 3 ? (in ? a2.w(iz, d) : 0.0) : 0.0;
+    wmx[q] = NDIM >= 2 ? wts(m0, ix, n0, q, row_ok) : 0.0;
+    wax[q] = NDIM >= 2 ? wts(a0, ix, n0, q, row_ok) : 0.0;
+    wmy[q] = NDIM == 3 ? wts(m1, iy, n1, q, row_ok) : 0.0;
+    way[q] = NDIM == 3 ? wts(a1, iy, n1, q, row_ok) : 0.0;
   }
 
 #pragma unroll
@@ -262,62 +307,82 @@ __global__ void __launch_bounds__(256) heat_apply_kernel(
     cp_async_commit();
   }
   double rr = 0.0, ff = 0.0;
-  // out_l = d_l (M U_l) + ds_{l-1} (M U_{l-1}) + c_l (A U_l) + cs_{l-1} (A U_{l-1}): the
-  // stencil is applied to one slice per step and (M U, A U) of the previous slice are
-  // carried in registers.
-  double mu_prev = 0.0, au_prev = 0.0;
-  const int base = (lx * HY + (NDIM >= 2 ? ly : 0)) * HZ + (NDIM == 3 ? lz : 0);
-  // 3-point sums start from the first product (no 0 + x / 0 * x that IEEE forbids folding)
+  double mu_prev[kPT], au_prev[kPT];
+#pragma unroll
+  for (int p = 0; p < kPT; ++p) mu_prev[p] = au_prev[p] = 0.0;
+  const int hbase = NDIM == 1 ? kPT * lx
+                              : (NDIM == 2 ? lx * HY + kPT * ly : (lx * HY + ly) * HZ + kPT * lz);
   auto dot3 = [](const double* w, double a, double b, double c) {
     return fma(w[2], c, fma(w[1], b, w[0] * a));
   };
-  int cur = 0, nxt = kStages - 1;  // ring positions of slice l and slice l + kStages - 1
+  auto line = [&](const double* r, double (&m)[kPT], double (&a)[kPT]) {
+    double v[kPT + 2];
+#pragma unroll
+    for (int k = 0; k < kPT + 2; ++k) v[k] = r[k];
+#pragma unroll
+    for (int p = 0; p < kPT; ++p) {
+      m[p] = dot3(wmf[p], v[p], v[p + 1], v[p + 2]);
+      a[p] = dot3(waf[p], v[p], v[p + 1], v[p + 2]);
+    }
+  };
+  int cur = 0, nxt = kStages - 1;
   for (int64_t l = 0; l < nt; ++l) {
     cp_async_wait<kStages - 2>();
-    __syncthreads();  // slice l landed for all threads; slice l-1's stage is free
+    __syncthreads();
     load_slice(nxt, l + kStages - 1);
     cp_async_commit();
-    const double* t = su[cur] + base;
-    double mu, au;
+    const double* t = su + cur * TE + hbase;
+    double mu[kPT], au[kPT];
     if constexpr (NDIM == 1) {
-      mu = dot3(wmx, t[0], t[1], t[2]);
-      au = dot3(wax, t[0], t[1], t[2]);
+      line(t, mu, au);
+    } else if constexpr (NDIM == 2) {
+      double mr[3][kPT], ar[3][kPT];
+#pragma unroll
+      for (int qx = 0; qx < 3; ++qx) line(t + qx * HY, mr[qx], ar[qx]);
+#pragma unroll
+      for (int p = 0; p < kPT; ++p) {
+        mu[p] = dot3(wmx, mr[0][p], mr[1][p], mr[2][p]);
+        au[p] = dot3(wax, mr[0][p], mr[1][p], mr[2][p]) + dot3(wmx, ar[0][p], ar[1][p], ar[2][p]);
+      }
     } else {
-      double my[3], ay[3];
+      double my[3][kPT], ay[3][kPT];
 #pragma unroll
       for (int qx = 0; qx < 3; ++qx) {
-        if constexpr (NDIM == 2) {
-          const double* r = t + qx * HY;
-          my[qx] = dot3(wmy, r[0], r[1], r[2]);
-          ay[qx] = dot3(way, r[0], r[1], r[2]);
-        } else {
-          double mz[3], az[3];
+        double mz[3][kPT], az[3][kPT];
 #pragma unroll
-          for (int qy = 0; qy < 3; ++qy) {
-            const double* r = t + (qx * HY + qy) * HZ;
-            mz[qy] = dot3(wmz, r[0], r[1], r[2]);
-            az[qy] = dot3(waz, r[0], r[1], r[2]);
-          }
-          my[qx] = dot3(wmy, mz[0], mz[1], mz[2]);
-          ay[qx] = dot3(way, mz[0], mz[1], mz[2]) + dot3(wmy, az[0], az[1], az[2]);
+        for (int qy = 0; qy < 3; ++qy) line(t + (qx * HY + qy) * HZ, mz[qy], az[qy]);
+#pragma unroll
+        for (int p = 0; p < kPT; ++p) {
+          my[qx][p] = dot3(wmy, mz[0][p], mz[1][p], mz[2][p]);
+          ay[qx][p] = dot3(way, mz[0][p], mz[1][p], mz[2][p]) + dot3(wmy, az[0][p], az[1][p], az[2][p]);
         }
       }
-      mu = dot3(wmx, my[0], my[1], my[2]);
-      au = dot3(wax, my[0], my[1], my[2]) + dot3(wmx, ay[0], ay[1], ay[2]);
+#pragma unroll
+      for (int p = 0; p < kPT; ++p) {
+        mu[p] = dot3(wmx, my[0][p], my[1][p], my[2][p]);
+        au[p] = dot3(wax, my[0][p], my[1][p], my[2][p]) + dot3(wmx, ay[0][p], ay[1][p], ay[2][p]);
+      }
     }
     const double dd = d_diag[l], cd = c_diag[l];
-    double acc = dd * mu + cd * au;
-    if (l > 0) acc += d_sup[l - 1] * mu_prev + c_sup[l - 1] * au_prev;
-    mu_prev = mu;
-    au_prev = au;
-    if (valid) {
-      if (RESIDUAL) {
-        const double f = sf[cur][tid];
-        const double r = f - acc;
-        rr += r * r;
-        ff += f * f;
-      } else {
-        out[l * nx + p] = acc;
+    const double ds = l > 0 ? d_sup[l - 1] : 0.0, cs = l > 0 ? c_sup[l - 1] : 0.0;
+#pragma unroll
+    for (int p = 0; p < kPT; ++p) {
+      double acc = dd * mu[p] + cd * au[p];
+      if (l > 0) acc += ds * mu_prev[p] + cs * au_prev[p];
+      mu_prev[p] = mu[p];
+      au_prev[p] = au[p];
+      if (row_ok && ifast + p < nf) {
+        if constexpr (RESIDUAL) {
+          const int e = NDIM == 1 ? kPT * lx + p
+                                  : (NDIM == 2 ? lx * T::BY + kPT * ly + p
+                                               : (lx * T::BY + ly) * T::BZ + kPT * lz + p);
+          const double f = sf[cur * TF + e];
+          const double r = f - acc;
+          rr += r * r;
+          ff += f * f;
+        } else {
+          out[l * nx + p0 + p] = acc;
+        }
       }
     }
     cur = cur + 1 == kStages ? 0 : cur + 1;
@@ -670,7 +735,15 @@ void launch_apply(stkg_heat& h, const double* U, const double* F, double* out, i
     m[i] = Tri{h.m_diag[i].p, h.m_off[i].p};
     a[i] = Tri{h.a_diag[i].p, h.a_off[i].p};
   }
-  heat_apply_kernel<NDIM, RES><<<blocks, 256, 0, h.stream>>>(
+  using SM = ApplySmem<NDIM, RES>;
+  static const bool configured = [] {
+    STKG_CUDA_CHECK(cudaFuncSetAttribute(heat_apply_kernel<NDIM, RES>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(SM::kBytes)));
+    return true;
+  }();
+  (void)configured;
+  heat_apply_kernel<NDIM, RES><<<blocks, 256, SM::kBytes, h.stream>>>(
       U, F, out, h.n[0], h.n[1], h.n[2], nt, m[0], m[1], m[2], a[0], a[1], a[2], dd, ds, cd, cs,
       h.partials.p);
   STKG_CUDA_CHECK(cudaGetLastError());
