@@ -391,3 +391,28 @@ def test_dst_mixed_axis_lengths(stk, cuda, ns, nt):
     assert rel(Us, Ud) < 2e-12
     rr, _ = ps.residual(dev(Us), dev(F))
     assert rr < 1e-10
+
+
+@pytest.mark.parametrize("transform", ["dense", "dst"])
+def test_nonuniform_time_bidiagonals(stk, orc, cuda, transform):
+    """General (non-uniform) temporal bidiagonals D, C: the recurrence uses every step's own
+    coefficients (stk/sylvester.hpp:128-140); both backends against the dense oracle."""
+    rng = np.random.default_rng(17)
+    n, nt = 31, 9
+    g = stk.SpaceGrid1D(0.0, 1.0, n)
+    e = stk.p1_eigpair(g)
+    M, A = stk.fem1d_matrices(g)
+    D = stk.Bidiagonal(rng.uniform(1.0, 2.0, nt), rng.uniform(-1.0, -0.2, nt - 1))
+    Cm = stk.Bidiagonal(rng.uniform(0.01, 0.1, nt), rng.uniform(0.01, 0.1, nt - 1))
+    kw = dict(transform=transform)
+    if transform == "dst":
+        kw["p1_h"] = [g.fem_h] * 2
+    plan = stk.HeatPlan(stk.TensorEigPair([e, e]), D, Cm, [M, M], [A, A], **kw)
+    F = rng.standard_normal((nt, n * n))
+    U = host(plan.solve(dev(F)))
+    rr, _ = plan.residual(dev(U), dev(F))
+    assert rr < 1e-12
+    Xk = np.kron(e.X, e.X)
+    lk = (e.lambdas[:, None] + e.lambdas[None, :]).ravel()
+    Uref = orc.solve_projected_heat_with_dense(Xk, lk, (D.diag, D.sup), (Cm.diag, Cm.sup), F)
+    assert rel(U, Uref) < 1e-12

@@ -231,3 +231,16 @@ def test_cfg4_refined_to_north_star_tolerance(stk, cuda):
     print("cfg4 refined", rep.rel_res_history, rep.iterations, rep.wall_time_s)
     assert rep.converged and rep.final_relres <= 1e-10
     assert plan.residual_dd(F, xh, xl) <= 1e-10
+
+
+def test_restarted_gmres(stk, ref_bands, cuda):
+    """GmresConfig.restart > 0 (stk/outer_krylov.hpp:18-28): restarted cycles still reach the
+    tolerance on the true residual, and the history has one entry per iteration."""
+    sb, tb = ref_bands["space_16_3"], ref_bands["time_16_3"]
+    plan = plan_from_bands(stk, sb, tb)
+    b = dev(np.random.default_rng(21).standard_normal(plan.N))
+    x, rep = plan.gmres(b, stk.GmresConfig(tol=1e-10, maxit=600, restart=15))
+    assert rep.converged and rep.final_relres <= 1e-9
+    assert len(rep.rel_res_history) == rep.iterations
+    xf, repf = plan.gmres(b, stk.GmresConfig(tol=1e-10, maxit=600, restart=0))
+    assert repf.iterations <= rep.iterations  # full GMRES never needs more iterations
