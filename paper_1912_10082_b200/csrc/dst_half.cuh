@@ -460,7 +460,11 @@ struct HalfStridedCfg {
   // Row v of the tile starts at (v/2) kRegion + (v%2) kRowB; with kStep = max(1, 16/G) these
   // are = kStep v (mod 16 doubles), so each half-warp's row accesses of 8 bytes hit distinct
   // banks.
+#ifdef STKG_HALF_KSTEP
+  static constexpr int kStep = STKG_HALF_KSTEP;
+#else
   static constexpr int kStep = G >= 16 ? 1 : 16 / G;
+#endif
   static constexpr int kRowB = N + N / V + kStep;                  // doubles: offset of row b
   static constexpr int kRegion = 2 * hpadded_len<N>() + 2 * kStep;  // doubles per pair
   static constexpr size_t kSmem = size_t(P) * kRegion * sizeof(double);
