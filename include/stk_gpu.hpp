@@ -17,6 +17,7 @@
 #include <cstddef>
 #include <cstdint>
 #include <functional>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -175,13 +176,21 @@ class DeviceBuffer {
 };
 
 // ------------------------------------------------------------------------ heat -------
+// Transform backend of a heat plan (stkg_heat_desc::transform).
+enum class Transform {
+  Dense = STKG_TRANSFORM_DENSE,  // any EigPair: each axis a DMMA GEMM with X / X^T
+  P1Dst = STKG_TRANSFORM_P1_DST  // uniform P1 grids: FP64 fast sine transforms (X not read)
+};
+
 class HeatPlan {
  public:
   // axes: per-axis EigPairs of the tensor pencil (x slowest); m/a: per-axis 1D factors of
-  // KronOp (optional; needed for apply/residual).
+  // KronOp (optional; needed for apply/residual).  transform = P1Dst needs the grid spacing
+  // of every axis in p1_h (the closed-form uniform-P1 basis; n + 1 a power of two).
   HeatPlan(const std::vector<EigPair>& axes, const Bidiagonal& d, const Bidiagonal& c,
            const std::vector<Tridiagonal>* m = nullptr, const std::vector<Tridiagonal>* a = nullptr,
-           void* stream = nullptr, int64_t time_chunk = 0) {
+           void* stream = nullptr, int64_t time_chunk = 0, Transform transform = Transform::Dense,
+           const std::vector<double>* p1_h = nullptr) {
     if (axes.empty() || axes.size() > 3) throw ArgumentError("HeatPlan: 1 to 3 spatial axes");
     if (c.diag.size() != d.diag.size())
       throw ArgumentError("solve_projected_heat: D and C sizes differ");
@@ -210,6 +219,12 @@ class HeatPlan {
     desc.d_sup = d.sup.empty() ? d.diag.data() : d.sup.data();
     desc.c_sup = c.sup.empty() ? c.diag.data() : c.sup.data();
     desc.time_chunk = time_chunk;
+    desc.transform = static_cast<int>(transform);
+    if (transform == Transform::P1Dst) {
+      if (!p1_h || p1_h->size() != axes.size())
+        throw ArgumentError("HeatPlan: Transform::P1Dst needs p1_h per axis");
+      for (size_t i = 0; i < axes.size(); ++i) desc.p1_h[i] = (*p1_h)[i];
+    }
     check(stkg_heat_create(&h_, &desc, stream));
   }
   HeatPlan(const HeatPlan&) = delete;
@@ -246,6 +261,23 @@ class HeatPlan {
   stkg_heat* h_ = nullptr;
   int64_t nx_ = 0, nt_ = 0;
 };
+
+// The tensor P1/Q1 heat plan of ndim uniform axes (n interior nodes on (a, b)) and n_t
+// backward-difference steps on (0, T), with the spatial factors for apply/residual.
+inline std::unique_ptr<HeatPlan> heat_plan_p1_uniform(int ndim, int n, int nt, double T = 1.0,
+                                                      double a = 0.0, double b = 1.0,
+                                                      Transform transform = Transform::P1Dst,
+                                                      void* stream = nullptr) {
+  auto dc = heat_time_matrices(nt, T);
+  auto ma = fem1d_matrices(a, b, n);
+  const EigPair e = p1_eigpair(a, b, n);
+  const std::vector<EigPair> axes(static_cast<size_t>(ndim), e);
+  const std::vector<Tridiagonal> ms(static_cast<size_t>(ndim), ma.first);
+  const std::vector<Tridiagonal> as(static_cast<size_t>(ndim), ma.second);
+  const std::vector<double> h(static_cast<size_t>(ndim), (b - a) / (n + 1));
+  return std::make_unique<HeatPlan>(axes, dc.first, dc.second, &ms, &as, stream, 0, transform,
+                                    &h);
+}
 
 // solve_projected_heat_with(eig, d, c, g) with a tensor EigPair and host G (N_h x N_t).
 inline std::vector<double> solve_projected_heat_with(const std::vector<EigPair>& axes,

@@ -93,6 +93,30 @@ int main() {
         for (int i = 0; i < n; ++i) ur[static_cast<size_t>(j) * n + i] += L[c * n + i] * R[c * nt + j];
     EXPECT(rel(ur, ud) <= 1e-6);
   }
+  // Transform::P1Dst (fast sine transforms) equals Transform::Dense on a 2D P1 grid
+  {
+    const int n = 63, nt = 8;
+    auto pd = heat_plan_p1_uniform(2, n, nt, 1.0, 0.0, 1.0, Transform::Dense);
+    auto ps = heat_plan_p1_uniform(2, n, nt, 1.0, 0.0, 1.0, Transform::P1Dst);
+    std::mt19937_64 rng(11);
+    std::normal_distribution<double> nd;
+    std::vector<double> F(static_cast<size_t>(n) * n * nt);
+    for (auto& v : F) v = nd(rng);
+    DeviceBuffer dF(F), u1(F.size()), u2(F.size());
+    pd->solve(dF.data(), u1.data());
+    ps->solve(dF.data(), u2.data());
+    EXPECT(rel(u2.download(), u1.download()) < 1e-12);
+    EXPECT(ps->residual(u2.data(), dF.data()) < 1e-12);
+    bool threw = false;
+    try {
+      auto e = p1_eigpair(0.0, 1.0, n);
+      auto dc = heat_time_matrices(nt, 1.0);
+      HeatPlan bad({e}, dc.first, dc.second, nullptr, nullptr, nullptr, 0, Transform::P1Dst);
+    } catch (const stk::ArgumentError&) {
+      threw = true;
+    }
+    EXPECT(threw);  // P1Dst without p1_h
+  }
   // SingularityError (stk/sylvester.hpp:133-135)
   {
     EigPair e{{2.0}, {1.0}};
