@@ -75,12 +75,18 @@ __device__ __forceinline__ void dft_small<16>(double2 (&u)[16]) {
 
 // Barrier over the threads of one FFT: a warp barrier when the FFT fits in one warp (its
 // shared region is private to the warp's FFTs), else a CTA barrier.
+// bar > 0: the FFT's own named barrier (bar.sync bar, T) so that several FFTs of one CTA
+// do not wait for each other inside their stages; bar == 0: the CTA barrier.
 template <int T>
-__device__ __forceinline__ void fft_sync() {
+__device__ __forceinline__ void fft_sync(int bar = 0) {
   if constexpr (T <= 32) {  // FFTs are aligned lane segments: the warp runs them in lockstep
     __syncwarp();
   } else {
-    __syncthreads();
+    if (bar > 0) {
+      asm volatile("bar.sync %0, %1;\n" ::"r"(bar), "n"(T) : "memory");
+    } else {
+      __syncthreads();
+    }
   }
 }
 
@@ -99,7 +105,7 @@ constexpr int hpadded_len() { return N + N / (STKG_HALF_V < 16 ? STKG_HALF_V : 1
 // writes the stage output to buf, and re-reads the thread's values for the next stage.
 template <int N, int V, int R, int NS>
 __device__ __forceinline__ void half_stage(double2 (&x)[V], double2* buf,
-                                           const double2* __restrict__ tw2, int t) {
+                                           const double2* __restrict__ tw2, int t, int bar) {
   constexpr int T = N / V;
   constexpr int B = V / R;                   // butterflies per thread
   constexpr int kStep = (2 * N) / (NS * R);  // tw2 index of exp(-2 pi i / (NS R))
@@ -125,7 +131,7 @@ __device__ __forceinline__ void half_stage(double2 (&x)[V], double2* buf,
 #pragma unroll
     for (int q = 0; q < R; ++q) x[i + q * B] = u[q];
   }
-  fft_sync<T>();  // every thread has consumed the previous contents of buf
+  fft_sync<T>(bar);  // every thread has consumed the previous contents of buf
 #pragma unroll
   for (int i = 0; i < B; ++i) {
     const int j = t + T * i;
@@ -133,7 +139,7 @@ __device__ __forceinline__ void half_stage(double2 (&x)[V], double2* buf,
 #pragma unroll
     for (int q = 0; q < R; ++q) buf[hpidx(base + q * NS)] = x[i + q * B];
   }
-  fft_sync<T>();
+  fft_sync<T>(bar);
   if constexpr (NS * R < N) {  // the last stage's output is consumed from buf directly
 #pragma unroll
     for (int p = 0; p < V; ++p) x[p] = buf[hpidx(t + T * p)];
@@ -144,12 +150,12 @@ __device__ __forceinline__ void half_stage(double2 (&x)[V], double2* buf,
 // Stops before the stage whose NS reaches STOP (STOP = N: run them all).
 template <int N, int V, int NS, int STOP = N>
 __device__ __forceinline__ void half_fft_stages(double2 (&x)[V], double2* buf,
-                                                const double2* __restrict__ tw2, int t) {
+                                                const double2* __restrict__ tw2, int t, int bar) {
   if constexpr (NS < STOP) {
     constexpr int rem = N / NS;
     constexpr int R = rem >= V ? V : rem;
-    half_stage<N, V, R, NS>(x, buf, tw2, t);
-    half_fft_stages<N, V, NS * R, STOP>(x, buf, tw2, t);
+    half_stage<N, V, R, NS>(x, buf, tw2, t, bar);
+    half_fft_stages<N, V, NS * R, STOP>(x, buf, tw2, t, bar);
   }
 }
 
@@ -172,7 +178,7 @@ __device__ __forceinline__ int opad(int e) { return e + e / V; }
 // aligned segment of T lanes (segmented shuffles); T > 32: whole warps, cross-warp totals
 // through red (2 T/32 doubles for this FFT).
 template <int T>
-__device__ __forceinline__ void fft_scan2(double& a, double& b, double* red, int t) {
+__device__ __forceinline__ void fft_scan2(double& a, double& b, double* red, int t, int bar) {
   constexpr int W = T < 32 ? T : 32;
   const int lane = t & (W - 1);
 #pragma unroll
@@ -190,7 +196,7 @@ __device__ __forceinline__ void fft_scan2(double& a, double& b, double* red, int
       red[2 * warp] = a;
       red[2 * warp + 1] = b;
     }
-    __syncthreads();
+    fft_sync<T>(bar);
     double oa = 0.0, ob = 0.0;
     for (int w = 0; w < warp; ++w) {
       oa += red[2 * w];
@@ -212,7 +218,8 @@ __device__ __forceinline__ double2 half_pre(double s, double xa, double xam, dou
 // prefix scan over k: thread t re-reads the A of k = t H .. t H + H - 1 (consecutive),
 // scans serially and across threads, and writes X_{2k+1} back to index 2k.
 template <int N, int V>
-__device__ __forceinline__ void half_scan_odd(int t, double* red, double* oa, double* ob) {
+__device__ __forceinline__ void half_scan_odd(int t, double* red, double* oa, double* ob,
+                                              int bar) {
   constexpr int T = N / V, H = V / 2;
   double Aa[H], Ab[H];
   double sa = 0.0, sb = 0.0;
@@ -225,7 +232,7 @@ __device__ __forceinline__ void half_scan_odd(int t, double* red, double* oa, do
     Ab[i] = sb;
   }
   double ea = sa, eb = sb;
-  fft_scan2<T>(ea, eb, red, t);
+  fft_scan2<T>(ea, eb, red, t, bar);
   ea -= sa;
   eb -= sb;
 #pragma unroll
@@ -246,13 +253,13 @@ __device__ __forceinline__ void half_scan_odd(int t, double* red, double* oa, do
 template <int N, int V>
 __device__ __forceinline__ void half_fft_post(double2 (&x)[V], double2* buf,
                                              const double2* __restrict__ tw2, int t, double hs,
-                                             double* red, double* oa, double* ob) {
+                                             double* red, double* oa, double* ob, int bar = 0) {
   constexpr int T = N / V, H = V / 2;
   constexpr int NSL = last_stage_ns<N, V>();
   constexpr int RL = N / NSL;   // radix of the last stage
   constexpr int BL = NSL / T;   // its butterflies per thread
   if constexpr (BL >= 2 && NSL > 1) {
-    half_fft_stages<N, V, 1, NSL>(x, buf, tw2, t);  // leaves the stage-(L-1) output in buf
+    half_fft_stages<N, V, 1, NSL>(x, buf, tw2, t, bar);  // leaves the stage-(L-1) output in buf
     // butterflies of this thread: jj[0..BL/2) and their mirrors jj[BL/2 + i] = NSL - jj[i]
     int jj[BL];
 #pragma unroll
@@ -277,7 +284,7 @@ __device__ __forceinline__ void half_fft_post(double2 (&x)[V], double2* buf,
       }
       dft_small<RL>(z[b]);  // z[b][q] = Z_{j + NSL q}
     }
-    fft_sync<T>();  // every thread has read buf: the output staging may overwrite it
+    fft_sync<T>(bar);  // every thread has read buf: the output staging may overwrite it
 #pragma unroll
     for (int b = 0; b < BL; ++b) {
       const int j = jj[b];
@@ -308,10 +315,10 @@ __device__ __forceinline__ void half_fft_post(double2 (&x)[V], double2* buf,
         ob[opad<V>(2 * k)] = Ab;
       }
     }
-    fft_sync<T>();
-    half_scan_odd<N, V>(t, red, oa, ob);
+    fft_sync<T>(bar);
+    half_scan_odd<N, V>(t, red, oa, ob, bar);
   } else {
-    half_fft_stages<N, V, 1>(x, buf, tw2, t);
+    half_fft_stages<N, V, 1>(x, buf, tw2, t, bar);
     // thread t owns k = t H + i (i < H) of the half spectrum k < N/2
     double Aa[H], Ab[H], Ba[H], Bb[H];
 #pragma unroll
@@ -337,10 +344,10 @@ __device__ __forceinline__ void half_fft_post(double2 (&x)[V], double2* buf,
       Ab[i] = sb;
     }
     double ea = sa, eb = sb;
-    fft_scan2<T>(ea, eb, red, t);
+    fft_scan2<T>(ea, eb, red, t, bar);
     ea -= sa;  // exclusive offsets
     eb -= sb;
-    fft_sync<T>();  // all reads of Z are done: buf may be overwritten by the outputs
+    fft_sync<T>(bar);  // all reads of Z are done: buf may be overwritten by the outputs
 #pragma unroll
     for (int i = 0; i < H; ++i) {
       const int k = t * H + i;
@@ -516,7 +523,7 @@ __global__ void __launch_bounds__(HalfStridedCfg<N>::kThreads, HalfStridedCfg<N>
         x[p] = half_pre(s, ra[m - 1], ra[mm - 1], rb[m - 1], rb[mm - 1]);
       }
     }
-    half_fft_post<N, V>(x, fbuf, tw2, t, hs, red[f], region, region + RB);
+    half_fft_post<N, V>(x, fbuf, tw2, t, hs, red[f], region, region + RB, P > 1 ? 1 + f : 0);
     __syncthreads();
     for (int e = threadIdx.x; e < G * n; e += C::kThreads) {
       const int v = e % G, kk = e / G;
