@@ -213,21 +213,51 @@ __device__ __forceinline__ double2 half_pre(double s, double xa, double xam, dou
   return make_double2(fma(s, xa + xam, 0.5 * (xa - xam)), fma(s, xb + xbm, 0.5 * (xb - xbm)));
 }
 
+// Output staging of the n transformed values of both vectors of a pair.
+// OutSplit: two arrays of doubles (one per vector) at opad(e), read back per vector by the
+// contiguous-axis stores.  OutPair: one array of double2 (a_e, b_e) at e + e/16, read back
+// as 16-byte rows by the strided 16-byte kernel; the e/16 pad keeps the post-processing's
+// stride-2 writes and the scan's stride-16 reads conflict-free.
+template <int V>
+struct OutSplit {
+  double* oa;
+  double* ob;
+  __device__ __forceinline__ void put(int e, double a, double b) const {
+    oa[opad<V>(e)] = a;
+    ob[opad<V>(e)] = b;
+  }
+  __device__ __forceinline__ void get(int e, double& a, double& b) const {
+    a = oa[opad<V>(e)];
+    b = ob[opad<V>(e)];
+  }
+};
+struct OutPair {
+  double2* o;
+  __device__ __forceinline__ static int idx(int e) { return e + (e >> 4); }
+  __device__ __forceinline__ void put(int e, double a, double b) const { o[idx(e)] = make_double2(a, b); }
+  __device__ __forceinline__ void get(int e, double& a, double& b) const {
+    const double2 v = o[idx(e)];
+    a = v.x;
+    b = v.y;
+  }
+};
+
 // Post-processing of the outputs k < N/2 (a thread owns a set of k and, for each, both
 // Z_k and Z_{N-k}): B_k -> X_{2k} at index 2k - 1; A_k parked at index 2k.  Then the
 // prefix scan over k: thread t re-reads the A of k = t H .. t H + H - 1 (consecutive),
 // scans serially and across threads, and writes X_{2k+1} back to index 2k.
-template <int N, int V>
-__device__ __forceinline__ void half_scan_odd(int t, double* red, double* oa, double* ob,
-                                              int bar) {
+template <int N, int V, class Out>
+__device__ __forceinline__ void half_scan_odd(int t, double* red, const Out& out, int bar) {
   constexpr int T = N / V, H = V / 2;
   double Aa[H], Ab[H];
   double sa = 0.0, sb = 0.0;
 #pragma unroll
   for (int i = 0; i < H; ++i) {
     const int k = t * H + i;
-    sa += oa[opad<V>(2 * k)];
-    sb += ob[opad<V>(2 * k)];
+    double a, b;
+    out.get(2 * k, a, b);
+    sa += a;
+    sb += b;
     Aa[i] = sa;
     Ab[i] = sb;
   }
@@ -238,22 +268,21 @@ __device__ __forceinline__ void half_scan_odd(int t, double* red, double* oa, do
 #pragma unroll
   for (int i = 0; i < H; ++i) {
     const int k = t * H + i;
-    oa[opad<V>(2 * k)] = Aa[i] + ea;
-    ob[opad<V>(2 * k)] = Ab[i] + eb;
+    out.put(2 * k, Aa[i] + ea, Ab[i] + eb);
   }
 }
 
 // FFT (x holds the pre-processed inputs), post-processing and prefix scan; writes the
-// n outputs of both vectors into oa / ob at opad(e).  buf may overlap oa/ob.
+// n outputs of both vectors through out (OutSplit / OutPair).  buf may overlap out.
 //
 // When the last Stockham stage gives every thread B >= 2 butterflies, it is fused with the
 // post-processing: thread t takes the mirrored butterflies j and NS - j (thread 0 the
 // multiples of T), so Z_k and Z_{N-k} meet in its registers and the last stage's output
 // never goes to shared memory.
-template <int N, int V>
+template <int N, int V, class Out>
 __device__ __forceinline__ void half_fft_post(double2 (&x)[V], double2* buf,
                                              const double2* __restrict__ tw2, int t, double hs,
-                                             double* red, double* oa, double* ob, int bar = 0) {
+                                             double* red, const Out& out, int bar = 0) {
   constexpr int T = N / V, H = V / 2;
   constexpr int NSL = last_stage_ns<N, V>();
   constexpr int RL = N / NSL;   // radix of the last stage
@@ -308,15 +337,13 @@ __device__ __forceinline__ void half_fft_post(double2 (&x)[V], double2* buf,
           Aa *= 0.5;
           Ab *= 0.5;
         } else {
-          oa[opad<V>(2 * k - 1)] = hs * (zm.y - zk.y);
-          ob[opad<V>(2 * k - 1)] = hs * (zk.x - zm.x);
+          out.put(2 * k - 1, hs * (zm.y - zk.y), hs * (zk.x - zm.x));
         }
-        oa[opad<V>(2 * k)] = Aa;
-        ob[opad<V>(2 * k)] = Ab;
+        out.put(2 * k, Aa, Ab);
       }
     }
     fft_sync<T>(bar);
-    half_scan_odd<N, V>(t, red, oa, ob, bar);
+    half_scan_odd<N, V>(t, red, out, bar);
   } else {
     half_fft_stages<N, V, 1>(x, buf, tw2, t, bar);
     // thread t owns k = t H + i (i < H) of the half spectrum k < N/2
@@ -351,12 +378,8 @@ __device__ __forceinline__ void half_fft_post(double2 (&x)[V], double2* buf,
 #pragma unroll
     for (int i = 0; i < H; ++i) {
       const int k = t * H + i;
-      if (k > 0) {  // X_{2k} -> index 2k - 1
-        oa[opad<V>(2 * k - 1)] = Ba[i];
-        ob[opad<V>(2 * k - 1)] = Bb[i];
-      }
-      oa[opad<V>(2 * k)] = Aa[i] + ea;  // X_{2k+1} -> index 2k
-      ob[opad<V>(2 * k)] = Ab[i] + eb;
+      if (k > 0) out.put(2 * k - 1, Ba[i], Bb[i]);  // X_{2k} -> index 2k - 1
+      out.put(2 * k, Aa[i] + ea, Ab[i] + eb);       // X_{2k+1} -> index 2k
     }
   }
 }
@@ -385,13 +408,16 @@ struct HalfCfg {
   static_assert(T <= 32 || T % 32 == 0, "FFTs are lane segments or whole warps");
 };
 
-// Contiguous axis (vectors of length n = N - 1 back to back): a CTA step transforms F
-// consecutive vector pairs (persistent grid); the 2F outputs leave as one contiguous block.
-// dst may alias src (an item is read completely before it is written).
+// Contiguous axis (vector g of length n = N - 1 at src + g ld_src, written to dst + g ld_dst;
+// ld = n: back to back): a CTA step transforms F consecutive vector pairs (persistent grid).
+// ld_dst > n (the padded internal layout of heat.cu's device solve) also writes zeros into
+// the ld_dst - n pad entries, so that the padded lanes stay finite through later passes.
+// dst may alias src when ld_src == ld_dst (an item is read completely before it is written).
 template <int N>
 __global__ void __launch_bounds__(HalfCfg<N>::kThreads, HalfCfg<N>::kMinBlocks)
     dst_half_kernel(const double* src, double* dst, int64_t nvec,
-                    const double2* __restrict__ tw2, double scale) {
+                    const double2* __restrict__ tw2, double scale, int64_t ld_src,
+                    int64_t ld_dst) {
   using C = HalfCfg<N>;
   constexpr int V = C::V, T = C::T, F = C::F, n = N - 1;
   extern __shared__ __align__(16) double2 hbuf[];
@@ -404,11 +430,12 @@ __global__ void __launch_bounds__(HalfCfg<N>::kThreads, HalfCfg<N>::kMinBlocks)
   const int64_t npairs = (nvec + 1) / 2;
   const int64_t nitems = (npairs + F - 1) / F;
   const double hs = 0.5 * scale;
+  const int ldo = static_cast<int>(ld_dst);
   for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x) {
     const int64_t g0 = 2 * (item * F + f);  // first vector of this FFT's pair
     const bool has_a = F == 1 || g0 < nvec, has_b = g0 + 1 < nvec;
-    const double* sa = src + (has_a ? g0 : 0) * n;
-    const double* sb = has_b ? sa + n : sa;
+    const double* sa = src + (has_a ? g0 : 0) * ld_src;
+    const double* sb = has_b ? sa + ld_src : sa;
     double2 x[V];
 #pragma unroll
     for (int p = 0; p < V; ++p) {
@@ -424,23 +451,23 @@ __global__ void __launch_bounds__(HalfCfg<N>::kThreads, HalfCfg<N>::kMinBlocks)
     // (half_fft_post's first barrier orders these reads before fbuf is overwritten, and
     // the previous item's stores from fbuf before this item's first write: the trailing
     // __syncthreads below)
-    half_fft_post<N, V>(x, fbuf, tw2, t, hs, red, oa, ob);
+    half_fft_post<N, V>(x, fbuf, tw2, t, hs, red, OutSplit<V>{oa, ob});
     __syncthreads();
     if constexpr (F == 1) {
-      double* da = dst + g0 * n;
-      for (int e = t; e < n; e += T) da[e] = oa[opad<V>(e)];
+      double* da = dst + g0 * ld_dst;
+      for (int e = t; e < ldo; e += T) da[e] = e < n ? oa[opad<V>(e)] : 0.0;
       if (has_b)
-        for (int e = t; e < n; e += T) da[n + e] = ob[opad<V>(e)];
+        for (int e = t; e < ldo; e += T) da[ld_dst + e] = e < n ? ob[opad<V>(e)] : 0.0;
     } else {
-      // the item's vectors [2 item F, 2 item F + 2F) are contiguous in memory
+      // the item's vectors [2 item F, 2 item F + 2F) (back to back when ld_dst == n)
       const int64_t v0 = 2 * item * F;
       const int nv = static_cast<int>(nvec - v0 < 2 * F ? nvec - v0 : 2 * F);
-      double* d0 = dst + v0 * n;
-      for (int e = threadIdx.x; e < nv * n; e += C::kThreads) {
-        const int q = e / n, idx = e - q * n;  // vector q of the item
+      double* d0 = dst + v0 * ld_dst;
+      for (int e = threadIdx.x; e < nv * ldo; e += C::kThreads) {
+        const int q = e / ldo, idx = e - q * ldo;  // vector q of the item
         const double* o_q = reinterpret_cast<const double*>(hbuf + (q >> 1) * C::kBuf) +
                             ((q & 1) ? opad<V>(N) : 0);
-        d0[e] = o_q[opad<V>(idx)];
+        d0[e] = idx < n ? o_q[opad<V>(idx)] : 0.0;
       }
       __syncthreads();  // other FFTs' buffers were read: next item may overwrite them
     }
@@ -480,8 +507,7 @@ struct HalfStridedCfg {
 
 template <int N>
 __global__ void __launch_bounds__(HalfStridedCfg<N>::kThreads, HalfStridedCfg<N>::kMinBlocks)
-    dst_half_strided_kernel(const double* __restrict__ src, double* __restrict__ dst,
-                            int64_t inner, int64_t nvec, const double2* __restrict__ tw2,
+    dst_half_strided_kernel(const double* src, double* dst, int64_t inner, int64_t nvec, const double2* __restrict__ tw2,
                             double scale) {
   using C = HalfStridedCfg<N>;
   constexpr int V = C::V, T = C::T, P = C::P, G = C::G, n = N - 1;
@@ -523,12 +549,101 @@ __global__ void __launch_bounds__(HalfStridedCfg<N>::kThreads, HalfStridedCfg<N>
         x[p] = half_pre(s, ra[m - 1], ra[mm - 1], rb[m - 1], rb[mm - 1]);
       }
     }
-    half_fft_post<N, V>(x, fbuf, tw2, t, hs, red[f], region, region + RB, P > 1 ? 1 + f : 0);
+    half_fft_post<N, V>(x, fbuf, tw2, t, hs, red[f], OutSplit<V>{region, region + RB},
+                        P > 1 ? 1 + f : 0);
     __syncthreads();
     for (int e = threadIdx.x; e < G * n; e += C::kThreads) {
       const int v = e % G, kk = e / G;
       const int64_t b = vbase[v];
       if (b >= 0) __stcs(dst + b + int64_t(kk) * inner, row(v)[opad<V>(kk)]);
+    }
+  }
+}
+
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+
+// Strided axis, 16-byte variant for the padded internal layout of heat.cu's device solve
+// (fastest axis stored with pitch N = n + 1, so inner is a multiple of the tile width G and
+// every tile row is 16P-byte aligned).  The tile is staged by 16-byte cp.async into a
+// mirror of its global rows (row r = P chunks of 16 bytes, chunk c = the values (a_r, b_r)
+// of pair c), XOR-swizzled within the row -- the layout TMA's SWIZZLE_64B/128B modes
+// produce: cp.async coalesces a global row only when its shared destination is the same
+// contiguous segment (tools/microbench/ldgsts_probe.cu: 1.5x the L2 sectors and 1.8x the
+// time for the per-pair-region layout), and the swizzle makes the pre-processing's
+// reads of 8 consecutive rows of one pair conflict-free.  After every pair has read its
+// inputs (a CTA barrier), the tile space is reused by the pairs' FFT regions; the outputs
+// (OutPair) leave as 16-byte streaming stores.  In place is allowed (src == dst): a tile
+// is read completely before it is written.
+template <int N>
+struct HalfStrided2Cfg {
+  static constexpr int V = half_v<N>(), T = N / V;
+  static constexpr int P = T >= 32 ? 4 : 128 / T;  // vector pairs per tile
+  static constexpr int G = 2 * P;                  // vectors per tile
+  static constexpr int kThreads = P * T;
+  static constexpr int kMinBlocks = 65536 / (kThreads * 128) < 1 ? 1 : 65536 / (kThreads * 128);
+  // double2 per pair region (FFT, outputs), rounded to 128 bytes plus a skew: the output
+  // copy interleaves the P regions (q = e % P), so consecutive regions start 8/P (P = 4) or
+  // 1 (P >= 8) 16-byte bank groups apart and every quarter-warp phase of 8 16-byte reads
+  // hits 8 distinct groups
+  static constexpr int kRegion = (hpadded_len<N>() + 7) / 8 * 8 + (P >= 8 ? 1 : 8 / P);
+  static constexpr int kTile = (N - 1) * P;  // double2 of the staged tile
+  static constexpr int kSmemD2 = P * kRegion > kTile ? P * kRegion : kTile;
+  static constexpr size_t kSmem = size_t(kSmemD2) * sizeof(double2);
+  static_assert(T <= 32 || T % 32 == 0, "FFTs are lane segments or whole warps");
+  static_assert(P == 4 || P % 8 == 0, "tile rows of 64 bytes or multiples of 128 bytes");
+  static_assert(N - 1 + (N - 2) / 16 < kRegion, "OutPair staging fits the region");
+  // 16-byte chunk of pair c in tile row r: SWIZZLE_64B (P = 4) / SWIZZLE_128B (P >= 8)
+  __device__ __forceinline__ static int chunk(int r, int c) {
+    return P == 4 ? (c ^ ((r >> 1) & 3)) : (c ^ (r & 7));
+  }
+};
+
+template <int N>
+__global__ void __launch_bounds__(HalfStrided2Cfg<N>::kThreads, HalfStrided2Cfg<N>::kMinBlocks)
+    dst_half_strided2_kernel(const double* src, double* dst, int64_t inner, int64_t nvec,
+                             const double2* __restrict__ tw2, double scale) {
+  using C = HalfStrided2Cfg<N>;
+  constexpr int V = C::V, T = C::T, P = C::P, G = C::G, n = N - 1, RG = C::kRegion;
+  extern __shared__ __align__(128) double2 sreg[];
+  __shared__ double red[P][T > 32 ? 2 * (T / 32) : 2];
+  const int f = threadIdx.x / T, t = threadIdx.x % T;
+  double2* region = sreg + f * RG;
+  const int64_t ntiles = nvec / G;  // the host guarantees inner % G == 0
+  const double hs = 0.5 * scale;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t g = tile * G;
+    const int64_t base = (g / inner) * n * inner + g % inner;
+    __syncthreads();  // the previous tile's stores have read the regions
+    for (int e = threadIdx.x; e < P * n; e += C::kThreads) {
+      const int c = e % P, r = e / P;
+      cp_async16(sreg + r * P + C::chunk(r, c), src + base + int64_t(r) * inner + 2 * c);
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+    double2 x[V];
+#pragma unroll
+    for (int p = 0; p < V; ++p) {
+      const int m = t + T * p;
+      x[p] = make_double2(0.0, 0.0);
+      if (m > 0) {
+        const int r0 = m - 1, r1 = N - m - 1;
+        const double s = -__ldg(&tw2[m].y);
+        const double2 u = sreg[r0 * P + C::chunk(r0, f)], w = sreg[r1 * P + C::chunk(r1, f)];
+        x[p] = half_pre(s, u.x, w.x, u.y, w.y);
+      }
+    }
+    __syncthreads();  // every pair has read the tile: the regions may overwrite it
+    half_fft_post<N, V>(x, region, tw2, t, hs, red[f], OutPair{region}, P > 1 ? 1 + f : 0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < P * n; e += C::kThreads) {
+      const int q = e % P, kk = e / P;
+      __stcs(reinterpret_cast<double2*>(dst + base + int64_t(kk) * inner + 2 * q),
+             sreg[q * RG + OutPair::idx(kk)]);
     }
   }
 }

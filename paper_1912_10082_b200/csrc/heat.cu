@@ -441,6 +441,18 @@ ModeWeight mode_weight(const stkg_heat& h) {
                     h.ndim > 2 ? h.inv_mu[2].p : nullptr, h.n[1], h.n[2], h.ndim};
 }
 
+// The same over the padded internal layout (h.pitch > 0): n_last -> pitch, pad lanes get
+// lambda 0 and weight 0 (their transformed data are zero, and stay zero).
+int64_t padded_nx(const stkg_heat& h) { return h.nx / h.n[h.ndim - 1] * h.pitch; }
+ModeLambda mode_lambda_padded(const stkg_heat& h) {
+  if (h.ndim == 2) return ModeLambda{h.lam[0].p, h.lam_pad.p, nullptr, h.pitch, 1, 2};
+  return ModeLambda{h.lam[0].p, h.lam[1].p, h.lam_pad.p, h.n[1], h.pitch, 3};
+}
+ModeWeight mode_weight_padded(const stkg_heat& h) {
+  if (h.ndim == 2) return ModeWeight{h.inv_mu[0].p, h.inv_mu_pad.p, nullptr, h.pitch, 1, 2};
+  return ModeWeight{h.inv_mu[0].p, h.inv_mu[1].p, h.inv_mu_pad.p, h.n[1], h.pitch, 3};
+}
+
 template <int L>
 void launch_dst_strided(const stkg_heat& h, int a, const double* src, double* dst,
                         int64_t inner, int64_t outer) {
@@ -488,10 +500,13 @@ void launch_dst(const stkg_heat& h, int a, const double* src, double* dst, int64
   STKG_CUDA_CHECK(cudaGetLastError());
 }
 
-// Half-length kernels (dst_half.cuh) for N = n + 1 in [16, 1024].
+// Half-length kernels (dst_half.cuh) for N = n + 1 in [16, 1024].  Contiguous axis
+// (inner == 1): vector g at src + g ld_src -> dst + g ld_dst (ld 0 = n).  Strided axes:
+// dst_half_strided_kernel, or the 16-byte dst_half_strided2_kernel when `wide` (the padded
+// layout: inner a multiple of its tile width, 16-byte aligned buffers).
 template <int N>
 void launch_dst_half(const stkg_heat& h, int a, const double* src, double* dst, int64_t inner,
-                     int64_t outer) {
+                     int64_t outer, int64_t ld_src = 0, int64_t ld_dst = 0, bool wide = false) {
   const int64_t nvec = outer * inner;
   const double scale = std::sqrt(2.0 / static_cast<double>(N));
   const double2* tw2 = reinterpret_cast<const double2*>(h.twiddle[a].p);
@@ -508,7 +523,21 @@ void launch_dst_half(const stkg_heat& h, int a, const double* src, double* dst, 
     }();
     const int64_t blocks = std::min<int64_t>(ceil_div(nvec, 2 * C::F), int64_t(148) * per_sm);
     dst_half_kernel<N><<<static_cast<unsigned>(blocks), C::kThreads, C::kSmem, h.stream>>>(
-        src, dst, nvec, tw2, scale);
+        src, dst, nvec, tw2, scale, ld_src > 0 ? ld_src : N - 1, ld_dst > 0 ? ld_dst : N - 1);
+  } else if (wide && inner % HalfStrided2Cfg<N>::G == 0) {
+    using C = HalfStrided2Cfg<N>;
+    static const int per_sm = [] {
+      STKG_CUDA_CHECK(cudaFuncSetAttribute(dst_half_strided2_kernel<N>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(C::kSmem)));
+      int b = 0;
+      STKG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+          &b, dst_half_strided2_kernel<N>, C::kThreads, C::kSmem));
+      return std::max(b, 1);
+    }();
+    const int64_t blocks = std::min<int64_t>(nvec / C::G, int64_t(148) * per_sm);
+    dst_half_strided2_kernel<N><<<static_cast<unsigned>(blocks), C::kThreads, C::kSmem, h.stream>>>(
+        src, dst, inner, nvec, tw2, scale);
   } else {
     using C = HalfStridedCfg<N>;
     static const int per_sm = [] {
@@ -527,6 +556,14 @@ void launch_dst_half(const stkg_heat& h, int a, const double* src, double* dst, 
   STKG_CUDA_CHECK(cudaGetLastError());
 }
 
+bool padded_layout_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("STKG_PAD");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 bool use_dst_half() {
   static const bool on = [] {
     const char* e = std::getenv("STKG_DST_HALF");
@@ -535,25 +572,30 @@ bool use_dst_half() {
   return on;
 }
 
+// Half-length DST pass with explicit leading dimensions (contiguous axis) or the 16-byte
+// strided kernel (wide); false when N = n_a + 1 has no half-length kernel.
+bool dst_half_pass(const stkg_heat& h, int a, const double* src, double* dst, int64_t inner,
+                   int64_t outer, int64_t ld_src = 0, int64_t ld_dst = 0, bool wide = false) {
+  switch (h.n[a] + 1) {
+    // N = 2048 keeps the padded 2N kernel: the half-length recurrence's sqrt(N) error
+    // growth costs 1D n = 2047 the 1e-10 residual gate (3e-10 measured)
+    case 16: launch_dst_half<16>(h, a, src, dst, inner, outer, ld_src, ld_dst, wide); return true;
+    case 32: launch_dst_half<32>(h, a, src, dst, inner, outer, ld_src, ld_dst, wide); return true;
+    case 64: launch_dst_half<64>(h, a, src, dst, inner, outer, ld_src, ld_dst, wide); return true;
+    case 128: launch_dst_half<128>(h, a, src, dst, inner, outer, ld_src, ld_dst, wide); return true;
+    case 256: launch_dst_half<256>(h, a, src, dst, inner, outer, ld_src, ld_dst, wide); return true;
+    case 512: launch_dst_half<512>(h, a, src, dst, inner, outer, ld_src, ld_dst, wide); return true;
+    case 1024: launch_dst_half<1024>(h, a, src, dst, inner, outer, ld_src, ld_dst, wide); return true;
+    default: return false;
+  }
+}
+
 void dst_pass(const stkg_heat& h, int a, const double* src, double* dst, int64_t inner,
               int64_t outer) {
   // The half-length kernels trade accuracy for speed (their odd outputs are a prefix sum):
   // measured relres 2.6e-12 (2D, n = 1023) and 7e-13 (2D 511) but 5e-11 for 1D n = 1023,
   // too close to the 1e-10 gate -- so 1D plans keep the padded kernels.
-  if (use_dst_half() && h.ndim >= 2) {
-    switch (h.n[a] + 1) {
-      // N = 2048 keeps the padded 2N kernel: the half-length recurrence's sqrt(N) error
-      // growth costs 1D n = 2047 the 1e-10 residual gate (3e-10 measured)
-      case 16: return launch_dst_half<16>(h, a, src, dst, inner, outer);
-      case 32: return launch_dst_half<32>(h, a, src, dst, inner, outer);
-      case 64: return launch_dst_half<64>(h, a, src, dst, inner, outer);
-      case 128: return launch_dst_half<128>(h, a, src, dst, inner, outer);
-      case 256: return launch_dst_half<256>(h, a, src, dst, inner, outer);
-      case 512: return launch_dst_half<512>(h, a, src, dst, inner, outer);
-      case 1024: return launch_dst_half<1024>(h, a, src, dst, inner, outer);
-      default: break;
-    }
-  }
+  if (use_dst_half() && h.ndim >= 2 && dst_half_pass(h, a, src, dst, inner, outer)) return;
   switch (2 * (h.n[a] + 1)) {
     case 32: return launch_dst<32>(h, a, src, dst, inner, outer);
     case 64: return launch_dst<64>(h, a, src, dst, inner, outer);
@@ -637,9 +679,50 @@ void axis_pass(stkg_heat& h, int a, bool forward, const double* src, double* dst
 }  // namespace stkg
 
 namespace {
+// Full solve of ntc time slices starting at l0 (carry holds y_{l0-1} when l0 > 0), P1_DST
+// 2D/3D plans (h.pitch > 0).  Every intermediate lives in S in the padded layout (fastest
+// axis at pitch N = n + 1, pad entries zero), so that the strided passes run the 16-byte
+// kernel in place:  F -(fastest axis)-> S -(other axes, in place)-> S -(scan)-> S
+// -(other axes)-> S -(fastest axis)-> U.
+void run_chunk_padded(stkg_heat& h, const double* F, double* U, double* S, int64_t l0,
+                      int64_t ntc) {
+  const int d = h.ndim, last = d - 1;
+  const int64_t nl = h.n[last], P = h.pitch;
+  const int64_t lines = h.nx / nl * ntc;  // vectors along the fastest axis
+  static const bool oop = std::getenv("STKG_PAD_OOP") && std::getenv("STKG_PAD_OOP")[0] == '1';
+  double* S2 = oop ? S + padded_nx(h) * ntc : S;
+  auto strided = [&](int a) {
+    int64_t inner = P, outer = ntc;
+    for (int b = a + 1; b < last; ++b) inner *= h.n[b];
+    for (int b = 0; b < a; ++b) outer *= h.n[b];
+    ProfScope ps(h, 0);
+    dst_half_pass(h, a, S, S2, inner, outer, 0, 0, true);
+    std::swap(S, S2);
+  };
+  {
+    ProfScope ps(h, 0);
+    dst_half_pass(h, last, F, S, 1, lines, nl, P);
+  }
+  for (int a = last - 1; a >= 0; --a) strided(a);
+  {
+    const int64_t nxp = padded_nx(h);
+    ProfScope ps(h, 1);
+    heat_scan_kernel<<<static_cast<unsigned>(ceil_div(nxp, 256)), 256, 0, h.stream>>>(
+        S, nxp, ntc, l0, mode_lambda_padded(h), mode_weight_padded(h), h.d_diag.p, h.d_sup.p,
+        h.c_diag.p, h.c_sup.p, h.carry.p);
+    STKG_CUDA_CHECK(cudaGetLastError());
+  }
+  for (int a = 0; a < last; ++a) strided(a);
+  {
+    ProfScope ps(h, 0);
+    dst_half_pass(h, last, S, U, 1, lines, P, nl);
+  }
+}
+
 // Full solve of ntc time slices starting at l0 (carry holds y_{l0-1} when l0 > 0).
 // Passes alternate between U and S so that the last inverse pass lands in U.
 void run_chunk(stkg_heat& h, const double* F, double* U, double* S, int64_t l0, int64_t ntc) {
+  if (h.pitch > 0) return run_chunk_padded(h, F, U, S, l0, ntc);
   const int d = h.ndim, passes = 2 * d;
   const double* src = F;
   int k = 0;
@@ -685,9 +768,10 @@ int64_t l2_chunk_slices(const stkg_heat& h) {
 // F, U: slices [l0, l0 + ntc) (already offset).  Uses h.scratch (grown to one sub-chunk).
 void solve_range(stkg_heat& h, const double* F, double* U, int64_t l0, int64_t ntc) {
   const int64_t tc = std::min(l2_chunk_slices(h), ntc);
-  if (h.scratch.n < static_cast<size_t>(h.nx * tc)) {
+  const int64_t slice = h.pitch > 0 ? padded_nx(h) * (std::getenv("STKG_PAD_OOP") ? 2 : 1) : h.nx;
+  if (h.scratch.n < static_cast<size_t>(slice * tc)) {
     STKG_CUDA_CHECK(cudaStreamSynchronize(h.stream));
-    h.scratch.alloc(h.nx * tc);
+    h.scratch.alloc(slice * tc);
   }
   for (int64_t j = 0; j < ntc; j += tc) {
     const int64_t m = std::min(tc, ntc - j);
@@ -920,7 +1004,32 @@ int stkg_heat_create(stkg_heat** out, const stkg_heat_desc* desc, void* cuda_str
         STKG_CUDA_CHECK(cudaStreamSynchronize(s));
       }
     }
-    h->carry.alloc(h->nx);
+    // padded internal layout of the device solve (run_chunk_padded): P1_DST 2D/3D plans whose
+    // axes all have half-length kernels; STKG_PAD=0 keeps the unpadded passes
+    if (dst_mode && h->ndim >= 2 && use_dst_half() && padded_layout_enabled()) {
+      bool ok = true;
+      for (int a = 0; a < h->ndim; ++a) {
+        const int64_t N = h->n[a] + 1;
+        ok = ok && N >= 16 && N <= 1024 && (N & (N - 1)) == 0;
+      }
+      if (ok) {
+        const int last = h->ndim - 1;
+        const int64_t nl = h->n[last];
+        h->pitch = nl + 1;
+        std::vector<double> lp(desc->lambdas[last], desc->lambdas[last] + nl);
+        lp.push_back(0.0);
+        h->lam_pad.alloc(nl + 1);
+        h->lam_pad.upload(lp.data(), nl + 1, s);
+        std::vector<double> wp(nl + 1, 0.0);
+        STKG_CUDA_CHECK(cudaMemcpyAsync(wp.data(), h->inv_mu[last].p, nl * sizeof(double),
+                                        cudaMemcpyDeviceToHost, s));
+        STKG_CUDA_CHECK(cudaStreamSynchronize(s));
+        h->inv_mu_pad.alloc(nl + 1);
+        h->inv_mu_pad.upload(wp.data(), nl + 1, s);
+        STKG_CUDA_CHECK(cudaStreamSynchronize(s));
+      }
+    }
+    h->carry.alloc(h->pitch > 0 ? padded_nx(*h) : h->nx);
     h->partials.alloc(2 * apply_blocks(*h));
     h->scalars.alloc(4);
     STKG_CUDA_CHECK(cudaMallocHost(&h->pinned, 4 * sizeof(double)));

@@ -47,6 +47,10 @@ struct stkg_heat {
   int transform = STKG_TRANSFORM_DENSE;
   DevBuf inv_mu[3];  // P1_DST: 1/mu_k per axis (folded into the recurrence)
   DevBuf twiddle[3];  // P1_DST: exp(-2 pi i m / 2N) per axis, as double2
+  // P1_DST 2D/3D device solve: internal layout with the fastest axis stored at pitch
+  // N = n + 1 (0: unpadded); lam/inv_mu of that axis extended by a 0 for the pad lane
+  int64_t pitch = 0;
+  DevBuf lam_pad, inv_mu_pad;
   DevBuf d_diag, d_sup, c_diag, c_sup;
   // host copies used by the host-side parts of the rational Krylov solver
   std::vector<double> lam_h[3], d_diag_h, d_sup_h, c_diag_h, c_sup_h;
