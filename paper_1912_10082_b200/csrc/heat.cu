@@ -109,14 +109,25 @@ __global__ void __launch_bounds__(256) heat_scan_factored_kernel(
     const double* __restrict__ Lt, const double* __restrict__ R, int rank, double* __restrict__ Y,
     int64_t nx, int64_t nt, ModeLambda lam, ModeWeight wgt, const double* __restrict__ d_diag,
     const double* __restrict__ d_sup, const double* __restrict__ c_diag,
-    const double* __restrict__ c_sup) {
+    const double* __restrict__ c_sup, int64_t pitch, int64_t nl) {
+  // pitch > 0: Y in the padded layout (nx counts padded modes; Lt stays unpadded with
+  // nx / pitch * nl rows; pad lanes get a zero load)
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= nx) return;
   const double li = lam(i);
   const double wi = wgt(i);
+  int64_t iu = i, nxu = nx;
+  bool pad = false;
+  if (pitch > 0) {
+    const int64_t q = i / pitch, rr = i - q * pitch;
+    iu = q * nl + rr;
+    nxu = nx / pitch * nl;
+    pad = rr >= nl;
+  }
   double lt[kMaxFactorRank];
 #pragma unroll
-  for (int r = 0; r < kMaxFactorRank; ++r) lt[r] = r < rank ? Lt[int64_t(r) * nx + i] : 0.0;
+  for (int r = 0; r < kMaxFactorRank; ++r)
+    lt[r] = (r < rank && !pad) ? Lt[int64_t(r) * nxu + iu] : 0.0;
   double y = 0.0;
   for (int64_t l = 0; l < nt; ++l) {
     double g = 0.0;
@@ -689,15 +700,12 @@ void run_chunk_padded(stkg_heat& h, const double* F, double* U, double* S, int64
   const int d = h.ndim, last = d - 1;
   const int64_t nl = h.n[last], P = h.pitch;
   const int64_t lines = h.nx / nl * ntc;  // vectors along the fastest axis
-  static const bool oop = std::getenv("STKG_PAD_OOP") && std::getenv("STKG_PAD_OOP")[0] == '1';
-  double* S2 = oop ? S + padded_nx(h) * ntc : S;
   auto strided = [&](int a) {
     int64_t inner = P, outer = ntc;
     for (int b = a + 1; b < last; ++b) inner *= h.n[b];
     for (int b = 0; b < a; ++b) outer *= h.n[b];
     ProfScope ps(h, 0);
-    dst_half_pass(h, a, S, S2, inner, outer, 0, 0, true);
-    std::swap(S, S2);
+    dst_half_pass(h, a, S, S, inner, outer, 0, 0, true);
   };
   {
     ProfScope ps(h, 0);
@@ -717,6 +725,22 @@ void run_chunk_padded(stkg_heat& h, const double* F, double* U, double* S, int64
     ProfScope ps(h, 0);
     dst_half_pass(h, last, S, U, 1, lines, P, nl);
   }
+}
+
+// The inverse passes of run_chunk_padded alone (factored solve): S (padded, modified in
+// place) -> U.
+void inverse_passes_padded(stkg_heat& h, double* S, double* U, int64_t ntc) {
+  const int d = h.ndim, last = d - 1;
+  const int64_t nl = h.n[last], P = h.pitch;
+  for (int a = 0; a < last; ++a) {
+    int64_t inner = P, outer = ntc;
+    for (int b = a + 1; b < last; ++b) inner *= h.n[b];
+    for (int b = 0; b < a; ++b) outer *= h.n[b];
+    ProfScope ps(h, 0);
+    dst_half_pass(h, a, S, S, inner, outer, 0, 0, true);
+  }
+  ProfScope ps(h, 0);
+  dst_half_pass(h, last, S, U, 1, h.nx / nl * ntc, P, nl);
 }
 
 // Full solve of ntc time slices starting at l0 (carry holds y_{l0-1} when l0 > 0).
@@ -768,7 +792,7 @@ int64_t l2_chunk_slices(const stkg_heat& h) {
 // F, U: slices [l0, l0 + ntc) (already offset).  Uses h.scratch (grown to one sub-chunk).
 void solve_range(stkg_heat& h, const double* F, double* U, int64_t l0, int64_t ntc) {
   const int64_t tc = std::min(l2_chunk_slices(h), ntc);
-  const int64_t slice = h.pitch > 0 ? padded_nx(h) * (std::getenv("STKG_PAD_OOP") ? 2 : 1) : h.nx;
+  const int64_t slice = h.pitch > 0 ? padded_nx(h) : h.nx;
   if (h.scratch.n < static_cast<size_t>(slice * tc)) {
     STKG_CUDA_CHECK(cudaStreamSynchronize(h.stream));
     h.scratch.alloc(slice * tc);
@@ -1122,13 +1146,28 @@ int stkg_heat_solve_factored(stkg_heat* h, int64_t rank, const double* L, const 
       axis_pass(*h, a, true, src, dst, rank);
       src = dst;
     }
+    if (h->pitch > 0) {  // padded layout: Y~ in the scratch, inverse passes as run_chunk_padded
+      const int64_t nxp = padded_nx(*h), last = h->ndim - 1;
+      if (h->scratch.n < static_cast<size_t>(nxp * h->nt)) h->scratch.alloc(nxp * h->nt);
+      double* S = h->scratch.p;
+      {
+        ProfScope ps(*h, 1);
+        heat_scan_factored_kernel<<<static_cast<unsigned>(ceil_div(nxp, 256)), 256, 0, h->stream>>>(
+            src, R, static_cast<int>(rank), S, nxp, h->nt, mode_lambda_padded(*h),
+            mode_weight_padded(*h), h->d_diag.p, h->d_sup.p, h->c_diag.p, h->c_sup.p, h->pitch,
+            h->n[last]);
+        STKG_CUDA_CHECK(cudaGetLastError());
+      }
+      inverse_passes_padded(*h, S, U, h->nt);
+      return;
+    }
     // the recurrence writes Y~ where the first inverse pass reads it
     double* Y = (h->ndim % 2 == 0) ? U : h->scratch.p;
     {
       ProfScope ps(*h, 1);
       heat_scan_factored_kernel<<<static_cast<unsigned>(ceil_div(h->nx, 256)), 256, 0, h->stream>>>(
           src, R, static_cast<int>(rank), Y, h->nx, h->nt, mode_lambda(*h), mode_weight(*h), h->d_diag.p,
-          h->d_sup.p, h->c_diag.p, h->c_sup.p);
+          h->d_sup.p, h->c_diag.p, h->c_sup.p, 0, 0);
       STKG_CUDA_CHECK(cudaGetLastError());
     }
     inverse_passes(*h, Y, U, h->scratch.p, h->nt);

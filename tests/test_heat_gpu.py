@@ -416,3 +416,40 @@ def test_nonuniform_time_bidiagonals(stk, orc, cuda, transform):
     lk = (e.lambdas[:, None] + e.lambdas[None, :]).ravel()
     Uref = orc.solve_projected_heat_with_dense(Xk, lk, (D.diag, D.sup), (Cm.diag, Cm.sup), F)
     assert rel(U, Uref) < 1e-12
+
+
+_PAD_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_1912_10082_b200 as stk
+out = {}
+for ndim, n, nt in [(2, 1023, 3), (2, 255, 5), (3, 127, 3), (3, 63, 2), (2, 15, 4)]:
+    F = torch.from_numpy(np.random.default_rng(n + ndim).standard_normal((nt, n ** ndim))).cuda()
+    p = stk.HeatPlan.p1_uniform(ndim, n, nt, transform="dst")
+    out[f"u{ndim}_{n}"] = p.solve(F).cpu().numpy()
+    L = torch.from_numpy(np.random.default_rng(n).standard_normal((2, n ** ndim))).cuda()
+    R = torch.from_numpy(np.random.default_rng(nt).standard_normal((2, nt))).cuda()
+    out[f"f{ndim}_{n}"] = p.solve_factored(L, R).cpu().numpy()
+np.savez(sys.argv[2], **out)
+"""
+
+
+def test_padded_layout_equals_unpadded(tmp_path):
+    """The device solve's padded internal layout (fastest axis at pitch N, 16-byte strided
+    kernel in place) computes what the unpadded passes compute.  Not bit for bit: two real
+    vectors share one complex FFT, and the layouts pair different vectors (vector n - 1
+    pairs with the zero pad lane instead of the next line's vector 0), so the partners'
+    rounding differs.  Each layout runs in its own process (STKG_PAD is read once)."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = str(Path(__file__).resolve().parent.parent)
+    res = {}
+    for pad in ("1", "0"):
+        f = tmp_path / f"pad{pad}.npz"
+        env = dict(os.environ, STKG_PAD=pad)
+        subprocess.run([sys.executable, "-c", _PAD_SCRIPT, root, str(f)], check=True, env=env)
+        res[pad] = dict(np.load(f))
+    for k in res["1"]:
+        assert rel(res["1"][k], res["0"][k]) < 1e-13, (k, rel(res["1"][k], res["0"][k]))
