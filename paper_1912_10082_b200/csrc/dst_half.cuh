@@ -578,53 +578,76 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 // inputs (a CTA barrier), the tile space is reused by the pairs' FFT regions; the outputs
 // (OutPair) leave as 16-byte streaming stores.  In place is allowed (src == dst): a tile
 // is read completely before it is written.
+// Default pairs per tile: 4 (64-byte rows) for FFTs of whole warps, else 128 threads.
 template <int N>
+constexpr int half2_pairs() { return N / half_v<N>() >= 32 ? 4 : 128 / (N / half_v<N>()); }
+
+// PF (prefetch): the staged tile gets its own buffer beside the pair regions, and the next
+// tile's copy is issued as soon as every pair has read the current one, so it lands while
+// the FFTs run (more shared memory per CTA, fewer CTAs per SM).
+template <int N, int PP = half2_pairs<N>(), bool PF = false>
 struct HalfStrided2Cfg {
   static constexpr int V = half_v<N>(), T = N / V;
-  static constexpr int P = T >= 32 ? 4 : 128 / T;  // vector pairs per tile
-  static constexpr int G = 2 * P;                  // vectors per tile
+  static constexpr int P = PP;       // vector pairs per tile
+  static constexpr int G = 2 * P;    // vectors per tile
   static constexpr int kThreads = P * T;
   static constexpr int kMinBlocks = 65536 / (kThreads * 128) < 1 ? 1 : 65536 / (kThreads * 128);
   // double2 per pair region (FFT, outputs), rounded to 128 bytes plus a skew: the output
-  // copy interleaves the P regions (q = e % P), so consecutive regions start 8/P (P = 4) or
+  // copy interleaves the P regions (q = e % P), so consecutive regions start 8/P (P <= 4) or
   // 1 (P >= 8) 16-byte bank groups apart and every quarter-warp phase of 8 16-byte reads
   // hits 8 distinct groups
   static constexpr int kRegion = (hpadded_len<N>() + 7) / 8 * 8 + (P >= 8 ? 1 : 8 / P);
-  static constexpr int kTile = (N - 1) * P;  // double2 of the staged tile
-  static constexpr int kSmemD2 = P * kRegion > kTile ? P * kRegion : kTile;
+  static constexpr int kTile = ((N - 1) * P + 7) / 8 * 8;  // double2 of the staged tile
+  static constexpr int kTileOff = PF ? P * kRegion : 0;   // where the tile is staged
+  static constexpr int kSmemD2 = PF ? P * kRegion + kTile
+                                    : (P * kRegion > kTile ? P * kRegion : kTile);
   static constexpr size_t kSmem = size_t(kSmemD2) * sizeof(double2);
   static_assert(T <= 32 || T % 32 == 0, "FFTs are lane segments or whole warps");
-  static_assert(P == 4 || P % 8 == 0, "tile rows of 64 bytes or multiples of 128 bytes");
+  static_assert(P == 2 || P == 4 || P % 8 == 0, "tile rows of 32, 64 or 128k bytes");
   static_assert(N - 1 + (N - 2) / 16 < kRegion, "OutPair staging fits the region");
-  // 16-byte chunk of pair c in tile row r: SWIZZLE_64B (P = 4) / SWIZZLE_128B (P >= 8)
+  // 16-byte chunk of pair c in tile row r, XOR-swizzled so that 8 consecutive rows of one
+  // pair fall in 8 distinct 16-byte bank groups (SWIZZLE_32B/64B/128B-like)
   __device__ __forceinline__ static int chunk(int r, int c) {
-    return P == 4 ? (c ^ ((r >> 1) & 3)) : (c ^ (r & 7));
+    if constexpr (P == 2) return c ^ ((r >> 2) & 1);
+    else if constexpr (P == 4) return c ^ ((r >> 1) & 3);
+    else return c ^ (r & 7);
   }
 };
 
-template <int N>
-__global__ void __launch_bounds__(HalfStrided2Cfg<N>::kThreads, HalfStrided2Cfg<N>::kMinBlocks)
+template <int N, int PP = half2_pairs<N>(), bool PF = false>
+__global__ void __launch_bounds__(HalfStrided2Cfg<N, PP, PF>::kThreads,
+                                  HalfStrided2Cfg<N, PP, PF>::kMinBlocks)
     dst_half_strided2_kernel(const double* src, double* dst, int64_t inner, int64_t nvec,
                              const double2* __restrict__ tw2, double scale) {
-  using C = HalfStrided2Cfg<N>;
+  using C = HalfStrided2Cfg<N, PP, PF>;
   constexpr int V = C::V, T = C::T, P = C::P, G = C::G, n = N - 1, RG = C::kRegion;
   extern __shared__ __align__(128) double2 sreg[];
   __shared__ double red[P][T > 32 ? 2 * (T / 32) : 2];
   const int f = threadIdx.x / T, t = threadIdx.x % T;
   double2* region = sreg + f * RG;
+  double2* stile = sreg + C::kTileOff;
   const int64_t ntiles = nvec / G;  // the host guarantees inner % G == 0
   const double hs = 0.5 * scale;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  auto tile_base = [&](int64_t tile) {
     const int64_t g = tile * G;
-    const int64_t base = (g / inner) * n * inner + g % inner;
-    __syncthreads();  // the previous tile's stores have read the regions
+    return (g / inner) * n * inner + g % inner;
+  };
+  auto load_tile = [&](int64_t base) {
     for (int e = threadIdx.x; e < P * n; e += C::kThreads) {
       const int c = e % P, r = e / P;
-      cp_async16(sreg + r * P + C::chunk(r, c), src + base + int64_t(r) * inner + 2 * c);
+      cp_async16(stile + r * P + C::chunk(r, c), src + base + int64_t(r) * inner + 2 * c);
     }
     cp_async_commit();
+  };
+  if (PF && blockIdx.x < ntiles) load_tile(tile_base(blockIdx.x));
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t base = tile_base(tile);
+    if (!PF) {
+      __syncthreads();  // the previous tile's stores have read the regions
+      load_tile(base);
+    }
     cp_async_wait<0>();
-    __syncthreads();
+    __syncthreads();  // (PF: also orders the previous tile's stores before the FFT writes)
     double2 x[V];
 #pragma unroll
     for (int p = 0; p < V; ++p) {
@@ -633,11 +656,12 @@ __global__ void __launch_bounds__(HalfStrided2Cfg<N>::kThreads, HalfStrided2Cfg<
       if (m > 0) {
         const int r0 = m - 1, r1 = N - m - 1;
         const double s = -__ldg(&tw2[m].y);
-        const double2 u = sreg[r0 * P + C::chunk(r0, f)], w = sreg[r1 * P + C::chunk(r1, f)];
+        const double2 u = stile[r0 * P + C::chunk(r0, f)], w = stile[r1 * P + C::chunk(r1, f)];
         x[p] = half_pre(s, u.x, w.x, u.y, w.y);
       }
     }
-    __syncthreads();  // every pair has read the tile: the regions may overwrite it
+    __syncthreads();  // every pair has read the tile: the regions / the next tile may overwrite it
+    if (PF && tile + gridDim.x < ntiles) load_tile(tile_base(tile + gridDim.x));
     half_fft_post<N, V>(x, region, tw2, t, hs, red[f], OutPair{region}, P > 1 ? 1 + f : 0);
     __syncthreads();
     for (int e = threadIdx.x; e < P * n; e += C::kThreads) {

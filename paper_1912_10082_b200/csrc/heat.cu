@@ -511,6 +511,24 @@ void launch_dst(const stkg_heat& h, int a, const double* src, double* dst, int64
   STKG_CUDA_CHECK(cudaGetLastError());
 }
 
+template <int N, int P, bool PF>
+void launch_dst_half_strided2(const stkg_heat& h, const double* src, double* dst, int64_t inner,
+                              int64_t nvec, const double2* tw2, double scale) {
+  using C = HalfStrided2Cfg<N, P, PF>;
+  static const int per_sm = [] {
+    STKG_CUDA_CHECK(cudaFuncSetAttribute(dst_half_strided2_kernel<N, P, PF>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(C::kSmem)));
+    int b = 0;
+    STKG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &b, dst_half_strided2_kernel<N, P, PF>, C::kThreads, C::kSmem));
+    return std::max(b, 1);
+  }();
+  const int64_t blocks = std::min<int64_t>(nvec / C::G, int64_t(148) * per_sm);
+  dst_half_strided2_kernel<N, P, PF><<<static_cast<unsigned>(blocks), C::kThreads, C::kSmem,
+                                       h.stream>>>(src, dst, inner, nvec, tw2, scale);
+}
+
 // Half-length kernels (dst_half.cuh) for N = n + 1 in [16, 1024].  Contiguous axis
 // (inner == 1): vector g at src + g ld_src -> dst + g ld_dst (ld 0 = n).  Strided axes:
 // dst_half_strided_kernel, or the 16-byte dst_half_strided2_kernel when `wide` (the padded
@@ -533,22 +551,23 @@ void launch_dst_half(const stkg_heat& h, int a, const double* src, double* dst, 
       return std::max(b, 1);
     }();
     const int64_t blocks = std::min<int64_t>(ceil_div(nvec, 2 * C::F), int64_t(148) * per_sm);
+    const int64_t lds = ld_src > 0 ? ld_src : N - 1, ldd = ld_dst > 0 ? ld_dst : N - 1;
     dst_half_kernel<N><<<static_cast<unsigned>(blocks), C::kThreads, C::kSmem, h.stream>>>(
-        src, dst, nvec, tw2, scale, ld_src > 0 ? ld_src : N - 1, ld_dst > 0 ? ld_dst : N - 1);
+        src, dst, nvec, tw2, scale, lds, ldd);
   } else if (wide && inner % HalfStrided2Cfg<N>::G == 0) {
-    using C = HalfStrided2Cfg<N>;
-    static const int per_sm = [] {
-      STKG_CUDA_CHECK(cudaFuncSetAttribute(dst_half_strided2_kernel<N>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           static_cast<int>(C::kSmem)));
-      int b = 0;
-      STKG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-          &b, dst_half_strided2_kernel<N>, C::kThreads, C::kSmem));
-      return std::max(b, 1);
-    }();
-    const int64_t blocks = std::min<int64_t>(nvec / C::G, int64_t(148) * per_sm);
-    dst_half_strided2_kernel<N><<<static_cast<unsigned>(blocks), C::kThreads, C::kSmem, h.stream>>>(
-        src, dst, inner, nvec, tw2, scale);
+    if constexpr (N == 1024) {  // tuning variants: STKG_HALF2 = pairs * 10 + prefetch
+      static const int var = [] {
+        const char* e = std::getenv("STKG_HALF2");
+        return e ? std::atoi(e) : 40;
+      }();
+      switch (var) {
+        case 41: return launch_dst_half_strided2<N, 4, true>(h, src, dst, inner, nvec, tw2, scale);
+        case 20: return launch_dst_half_strided2<N, 2, false>(h, src, dst, inner, nvec, tw2, scale);
+        case 21: return launch_dst_half_strided2<N, 2, true>(h, src, dst, inner, nvec, tw2, scale);
+        default: break;
+      }
+    }
+    launch_dst_half_strided2<N, half2_pairs<N>(), false>(h, src, dst, inner, nvec, tw2, scale);
   } else {
     using C = HalfStridedCfg<N>;
     static const int per_sm = [] {
