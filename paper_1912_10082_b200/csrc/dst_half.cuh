@@ -215,9 +215,8 @@ __device__ __forceinline__ double2 half_pre(double s, double xa, double xam, dou
 
 // Output staging of the n transformed values of both vectors of a pair.
 // OutSplit: two arrays of doubles (one per vector) at opad(e), read back per vector by the
-// contiguous-axis stores.  OutPair: one array of double2 (a_e, b_e) at e + e/16, read back
-// as 16-byte rows by the strided 16-byte kernel; the e/16 pad keeps the post-processing's
-// stride-2 writes and the scan's stride-16 reads conflict-free.
+// contiguous-axis stores.  OutPair: one array of double2 (a_e, b_e) at idx(e), read back
+// as 16-byte rows by the strided 16-byte kernel.
 template <int V>
 struct OutSplit {
   double* oa;
@@ -231,9 +230,22 @@ struct OutSplit {
     b = ob[opad<V>(e)];
   }
 };
+template <int N>
 struct OutPair {
   double2* o;
+#if STKG_OUTPAIR_LINEAR
   __device__ __forceinline__ static int idx(int e) { return e + (e >> 4); }
+#else
+  // Even outputs e = 2k at p(k), odd outputs e = 2k - 1 at N/2 + p(k), p(k) = k XOR-swizzled
+  // by k / 8 within groups of 64: the post-processing's writes of 8 consecutive k, the
+  // scan's reads of k = 8t + i over 8 consecutive t and the tile copy's (even, odd) pairs
+  // fall in distinct 16-byte bank groups (the previous e + e/16 layout made every stride-2
+  // post-processing write phase 2-way conflicted).
+  __device__ __forceinline__ static int idx(int e) {
+    const int k = (e + 1) >> 1;
+    return (e & 1) * (N / 2) + (k ^ ((k >> 3) & 7));
+  }
+#endif
   __device__ __forceinline__ void put(int e, double a, double b) const { o[idx(e)] = make_double2(a, b); }
   __device__ __forceinline__ void get(int e, double& a, double& b) const {
     const double2 v = o[idx(e)];
@@ -604,7 +616,7 @@ struct HalfStrided2Cfg {
   static constexpr size_t kSmem = size_t(kSmemD2) * sizeof(double2);
   static_assert(T <= 32 || T % 32 == 0, "FFTs are lane segments or whole warps");
   static_assert(P == 2 || P == 4 || P % 8 == 0, "tile rows of 32, 64 or 128k bytes");
-  static_assert(N - 1 + (N - 2) / 16 < kRegion, "OutPair staging fits the region");
+  static_assert(N - 1 + (N - 2) / 16 < kRegion && N <= kRegion, "OutPair staging fits the region");
   // 16-byte chunk of pair c in tile row r, XOR-swizzled so that 8 consecutive rows of one
   // pair fall in 8 distinct 16-byte bank groups (SWIZZLE_32B/64B/128B-like)
   __device__ __forceinline__ static int chunk(int r, int c) {
@@ -662,12 +674,12 @@ __global__ void __launch_bounds__(HalfStrided2Cfg<N, PP, PF>::kThreads,
     }
     __syncthreads();  // every pair has read the tile: the regions / the next tile may overwrite it
     if (PF && tile + gridDim.x < ntiles) load_tile(tile_base(tile + gridDim.x));
-    half_fft_post<N, V>(x, region, tw2, t, hs, red[f], OutPair{region}, P > 1 ? 1 + f : 0);
+    half_fft_post<N, V>(x, region, tw2, t, hs, red[f], OutPair<N>{region}, P > 1 ? 1 + f : 0);
     __syncthreads();
     for (int e = threadIdx.x; e < P * n; e += C::kThreads) {
       const int q = e % P, kk = e / P;
       __stcs(reinterpret_cast<double2*>(dst + base + int64_t(kk) * inner + 2 * q),
-             sreg[q * RG + OutPair::idx(kk)]);
+             sreg[q * RG + OutPair<N>::idx(kk)]);
     }
   }
 }
