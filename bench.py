@@ -264,7 +264,7 @@ def _timed_path(stk, inputs, cfg, transform, args, stream, barrier, F, U, with_c
                 and os.environ.get("STKG_DST_HALF", "1") != "0")
         L = (cfg.n + 1) if half else 2 * (cfg.n + 1)  # complex FFT length per vector pair
         fft_flops = 5.0 * L * np.log2(L) / 2.0 / cfg.n  # per element and axis pass
-        kname = ("dst_half_kernel / dst_half_strided_kernel (FP64 half-length DST-I: "
+        kname = ("dst_half_kernel / dst_half_strided2_kernel (FP64 half-length DST-I: "
                  "N-point Stockham FFT per vector pair)") if half else \
             "dst_axis_kernel / dst_strided_kernel (FP64 padded 2N-point FFT DST-I)"
         roof = {"bound": "hbm", "kernel": kname,
