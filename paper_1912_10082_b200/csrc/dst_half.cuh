@@ -103,7 +103,11 @@ constexpr int hpadded_len() { return N + N / (STKG_HALF_V < 16 ? STKG_HALF_V : 1
 // One Stockham stage (radix R; NS = product of the earlier radices) of a length-N FFT
 // whose T = N/V threads hold x[p] = value at position t + T p.  Computes in registers,
 // writes the stage output to buf, and re-reads the thread's values for the next stage.
-template <int N, int V, int R, int NS>
+// LIN: this stage's output goes to buf in linear order (no swizzle) -- used for the stage
+// that feeds the fused last stage (half_fft_post), whose mirrored reads (N - k runs, not
+// 8-aligned) would straddle two swizzle groups and conflict 2-way; with NS >= 8 this
+// stage's writes (8 consecutive j per quarter-warp phase) are conflict-free in linear order.
+template <int N, int V, int R, int NS, bool LIN = false>
 __device__ __forceinline__ void half_stage(double2 (&x)[V], double2* buf,
                                            const double2* __restrict__ tw2, int t, int bar) {
   constexpr int T = N / V;
@@ -137,10 +141,10 @@ __device__ __forceinline__ void half_stage(double2 (&x)[V], double2* buf,
     const int j = t + T * i;
     const int base = (j / NS) * NS * R + j % NS;
 #pragma unroll
-    for (int q = 0; q < R; ++q) buf[hpidx(base + q * NS)] = x[i + q * B];
+    for (int q = 0; q < R; ++q) buf[LIN ? base + q * NS : hpidx(base + q * NS)] = x[i + q * B];
   }
   fft_sync<T>(bar);
-  if constexpr (NS * R < N) {  // the last stage's output is consumed from buf directly
+  if constexpr (NS * R < N && !LIN) {  // the last stage's output is consumed from buf directly
 #pragma unroll
     for (int p = 0; p < V; ++p) x[p] = buf[hpidx(t + T * p)];
   }
@@ -148,14 +152,26 @@ __device__ __forceinline__ void half_stage(double2 (&x)[V], double2* buf,
 
 // All stages: radix V while V divides the remaining length, then the remainder radix.
 // Stops before the stage whose NS reaches STOP (STOP = N: run them all).
-template <int N, int V, int NS, int STOP = N>
+template <int N, int V, int NS, int STOP = N, bool LL = false>
 __device__ __forceinline__ void half_fft_stages(double2 (&x)[V], double2* buf,
                                                 const double2* __restrict__ tw2, int t, int bar) {
   if constexpr (NS < STOP) {
     constexpr int rem = N / NS;
     constexpr int R = rem >= V ? V : rem;
-    half_stage<N, V, R, NS>(x, buf, tw2, t, bar);
-    half_fft_stages<N, V, NS * R, STOP>(x, buf, tw2, t, bar);
+    constexpr bool LIN = LL && STOP < N && NS * R == STOP && NS >= 8;
+    half_stage<N, V, R, NS, LIN>(x, buf, tw2, t, bar);
+    half_fft_stages<N, V, NS * R, STOP, LL>(x, buf, tw2, t, bar);
+  }
+}
+
+// NS of the stage that runs just before the stage with NS = stop.
+template <int N, int V>
+constexpr int stage_before(int stop) {
+  int ns = 1;
+  for (;;) {
+    const int rem = N / ns, r = rem >= V ? V : rem;
+    if (ns * r >= stop) return ns;
+    ns *= r;
   }
 }
 
@@ -291,7 +307,9 @@ __device__ __forceinline__ void half_scan_odd(int t, double* red, const Out& out
 // post-processing: thread t takes the mirrored butterflies j and NS - j (thread 0 the
 // multiples of T), so Z_k and Z_{N-k} meet in its registers and the last stage's output
 // never goes to shared memory.
-template <int N, int V, class Out>
+// LL: the stage feeding the fused last stage writes linearly (half_stage's LIN); measured
+// 1% faster for the contiguous kernel, slower for the strided one (28 bytes of spills).
+template <int N, int V, bool LL = false, class Out>
 __device__ __forceinline__ void half_fft_post(double2 (&x)[V], double2* buf,
                                              const double2* __restrict__ tw2, int t, double hs,
                                              double* red, const Out& out, int bar = 0) {
@@ -300,7 +318,9 @@ __device__ __forceinline__ void half_fft_post(double2 (&x)[V], double2* buf,
   constexpr int RL = N / NSL;   // radix of the last stage
   constexpr int BL = NSL / T;   // its butterflies per thread
   if constexpr (BL >= 2 && NSL > 1) {
-    half_fft_stages<N, V, 1, NSL>(x, buf, tw2, t, bar);  // leaves the stage-(L-1) output in buf
+    // the stage-(L-1) output is left in buf, linear when that stage has NS >= 8
+    constexpr bool LINL = LL && stage_before<N, V>(NSL) >= 8;
+    half_fft_stages<N, V, 1, NSL, LL>(x, buf, tw2, t, bar);
     // butterflies of this thread: jj[0..BL/2) and their mirrors jj[BL/2 + i] = NSL - jj[i]
     int jj[BL];
 #pragma unroll
@@ -313,7 +333,7 @@ __device__ __forceinline__ void half_fft_post(double2 (&x)[V], double2* buf,
     for (int b = 0; b < BL; ++b) {
       const int j = jj[b];
 #pragma unroll
-      for (int q = 0; q < RL; ++q) z[b][q] = buf[hpidx(j + NSL * q)];
+      for (int q = 0; q < RL; ++q) z[b][q] = buf[LINL ? j + NSL * q : hpidx(j + NSL * q)];
       if (j > 0) {
         const double2 w = __ldg(tw2 + 2 * j);  // exp(-2 pi i j / N)
         double2 wr = w;
@@ -463,7 +483,7 @@ __global__ void __launch_bounds__(HalfCfg<N>::kThreads, HalfCfg<N>::kMinBlocks)
     // (half_fft_post's first barrier orders these reads before fbuf is overwritten, and
     // the previous item's stores from fbuf before this item's first write: the trailing
     // __syncthreads below)
-    half_fft_post<N, V>(x, fbuf, tw2, t, hs, red, OutSplit<V>{oa, ob});
+    half_fft_post<N, V, true>(x, fbuf, tw2, t, hs, red, OutSplit<V>{oa, ob});
     __syncthreads();
     if constexpr (F == 1) {
       double* da = dst + g0 * ld_dst;
