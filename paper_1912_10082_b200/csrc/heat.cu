@@ -411,6 +411,185 @@ __global__ void __launch_bounds__(256) heat_apply_kernel(
   }
 }
 
+// 2D K1, marching along x.  A thread owns PT = 4 consecutive points along x at one y
+// (a warp = 32 consecutive y, coalesced), so the y-direction products of a U row
+// (m = M_y u, a = A_y u: 6 FMA) are shared by the up-to-3 points that use that row
+// instead of being recomputed per point: (PT + 2) / PT x 6 + 9 FMA per point for M U and
+// A U instead of 27 (heat_apply_kernel<2>).  The x weights of the thread's 4 points stay
+// in registers as diag[4] / off[5] (the factors are symmetric tridiagonal).  A CTA handles
+// a 32 x 32 tile over a chunk of kChunk time slices, first re-deriving M U, A U of the
+// slice before its chunk, so the grid has tiles x chunks CTAs (no half-empty last wave).
+struct Apply2D {
+  static constexpr int PT = 4, SEG = 8, BY = 32, BX = PT * SEG;
+  static constexpr int HX = BX + 2, HY = BY + 2, TE = HX * HY, TF = BX * BY;
+  static constexpr int kStages = 4, kChunk = 64;
+  static constexpr int kPer = (TE + 255) / 256, kPerF = TF / 256;
+};
+template <bool RESIDUAL>
+constexpr size_t apply2d_smem() {
+  return size_t(Apply2D::kStages) * (Apply2D::TE + (RESIDUAL ? Apply2D::TF : 0)) * sizeof(double);
+}
+
+template <bool RESIDUAL>
+__global__ void __launch_bounds__(256, 2) heat_apply2d_kernel(
+    const double* __restrict__ U, const double* __restrict__ F, double* __restrict__ out,
+    int64_t n0, int64_t n1, int64_t nt, Tri m0, Tri m1, Tri a0, Tri a1,
+    const double* __restrict__ d_diag, const double* __restrict__ d_sup,
+    const double* __restrict__ c_diag, const double* __restrict__ c_sup,
+    double* __restrict__ partials) {
+  using A = Apply2D;
+  constexpr int PT = A::PT, HY = A::HY, TE = A::TE, TF = A::TF, kStages = A::kStages;
+  extern __shared__ __align__(16) double asmem[];
+  double* su = asmem;                  // [kStages][TE]
+  double* sf = asmem + kStages * TE;   // [kStages][TF]
+  const int64_t tiles_y = (n1 + A::BY - 1) / A::BY, tiles_x = (n0 + A::BX - 1) / A::BX;
+  const int64_t tile = blockIdx.x % (tiles_x * tiles_y), ck = blockIdx.x / (tiles_x * tiles_y);
+  const int64_t x0 = (tile / tiles_y) * A::BX, y0 = (tile % tiles_y) * A::BY;
+  const int64_t l_begin = ck * A::kChunk;
+  const int64_t l_end = l_begin + A::kChunk < nt ? l_begin + A::kChunk : nt;
+  const int64_t l_first = l_begin > 0 ? l_begin - 1 : 0;  // warm-up slice for M U_{l-1}
+  const int tid = threadIdx.x, lane = tid & 31, seg = tid >> 5;
+  const int64_t iy = y0 + lane, xs = x0 + seg * PT;
+  const int64_t nx = n0 * n1;
+
+  int64_t hoff[A::kPer];
+  uint32_t hok = 0;
+#pragma unroll
+  for (int k = 0; k < A::kPer; ++k) {
+    const int e = tid + 256 * k;
+    const int64_t gx = x0 + e / HY - 1, gy = y0 + e % HY - 1;
+    const bool ok = e < TE && gx >= 0 && gx < n0 && gy >= 0 && gy < n1;
+    hoff[k] = ok ? gx * n1 + gy : 0;
+    if (ok) hok |= 1u << k;
+  }
+  int64_t foff[A::kPerF];
+  uint32_t fok = 0;
+  if constexpr (RESIDUAL) {
+#pragma unroll
+    for (int k = 0; k < A::kPerF; ++k) {
+      const int e = tid + 256 * k;
+      const int64_t gx = x0 + e / A::BY, gy = y0 + e % A::BY;
+      const bool ok = gx < n0 && gy < n1;
+      foff[k] = ok ? gx * n1 + gy : 0;
+      if (ok) fok |= 1u << k;
+    }
+  }
+  auto load_slice = [&](int stage, int64_t l) {
+    const bool lin = l < l_end;
+    const double* Ul = U + l * nx;
+#pragma unroll
+    for (int k = 0; k < A::kPer; ++k) {
+      const int e = tid + 256 * k;
+      if (e < TE) {
+        const bool ok = lin && ((hok >> k) & 1u);
+        cp_async8(&su[stage * TE + e], ok ? Ul + hoff[k] : U, ok);
+      }
+    }
+    if constexpr (RESIDUAL) {
+      const double* Fl = F + l * nx;
+#pragma unroll
+      for (int k = 0; k < A::kPerF; ++k) {
+        const bool ok = lin && l >= l_begin && ((fok >> k) & 1u);
+        cp_async8(&sf[stage * TF + tid + 256 * k], ok ? Fl + foff[k] : F, ok);
+      }
+    }
+  };
+
+  // y weights of this thread's row; x weights of its PT points (symmetric tridiagonals)
+  const bool y_ok = iy < n1;
+  double wmy[3], way[3];
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    const int64_t j = iy + q - 1;
+    const bool ok = y_ok && j >= 0 && j < n1;
+    wmy[q] = ok ? m1.w(iy, q - 1) : 0.0;
+    way[q] = ok ? a1.w(iy, q - 1) : 0.0;
+  }
+  double md[PT], ad[PT], mo[PT + 1], ao[PT + 1];
+#pragma unroll
+  for (int p = 0; p < PT; ++p) {
+    const bool ok = xs + p < n0;
+    md[p] = ok ? m0.diag[xs + p] : 0.0;
+    ad[p] = ok ? a0.diag[xs + p] : 0.0;
+  }
+#pragma unroll
+  for (int k = 0; k <= PT; ++k) {  // off[xs - 1 + k]: entry (x, x+1) for x = xs - 1 + k
+    const int64_t x = xs - 1 + k;
+    const bool ok = x >= 0 && x + 1 < n0;
+    mo[k] = ok ? m0.off[x] : 0.0;
+    ao[k] = ok ? a0.off[x] : 0.0;
+  }
+
+#pragma unroll
+  for (int st = 0; st < kStages - 1; ++st) {
+    load_slice(st, l_first + st);
+    cp_async_commit();
+  }
+  double rr = 0.0, ff = 0.0;
+  double mu_prev[PT], au_prev[PT];
+#pragma unroll
+  for (int p = 0; p < PT; ++p) mu_prev[p] = au_prev[p] = 0.0;
+  const int hbase = seg * PT * HY + lane;
+  int cur = 0, nxt = kStages - 1;
+  for (int64_t l = l_first; l < l_end; ++l) {
+    cp_async_wait<kStages - 2>();
+    __syncthreads();
+    load_slice(nxt, l + kStages - 1);
+    cp_async_commit();
+    const double* t = su + cur * TE + hbase;
+    double mr[PT + 2], ar[PT + 2];
+#pragma unroll
+    for (int r = 0; r < PT + 2; ++r) {
+      const double v0 = t[r * HY], v1 = t[r * HY + 1], v2 = t[r * HY + 2];
+      mr[r] = fma(wmy[2], v2, fma(wmy[1], v1, wmy[0] * v0));
+      ar[r] = fma(way[2], v2, fma(way[1], v1, way[0] * v0));
+    }
+    double mu[PT], au[PT];
+#pragma unroll
+    for (int p = 0; p < PT; ++p) {
+      mu[p] = fma(mo[p + 1], mr[p + 2], fma(md[p], mr[p + 1], mo[p] * mr[p]));
+      au[p] = fma(ao[p + 1], mr[p + 2], fma(ad[p], mr[p + 1], ao[p] * mr[p])) +
+              fma(mo[p + 1], ar[p + 2], fma(md[p], ar[p + 1], mo[p] * ar[p]));
+    }
+    if (l >= l_begin) {
+      const double dd = d_diag[l], cd = c_diag[l];
+      const double ds = l > 0 ? d_sup[l - 1] : 0.0, cs = l > 0 ? c_sup[l - 1] : 0.0;
+#pragma unroll
+      for (int p = 0; p < PT; ++p) {
+        double acc = dd * mu[p] + cd * au[p];
+        if (l > 0) acc += ds * mu_prev[p] + cs * au_prev[p];
+        if (y_ok && xs + p < n0) {
+          if constexpr (RESIDUAL) {
+            const double f = sf[cur * TF + (seg * PT + p) * A::BY + lane];
+            const double r = f - acc;
+            rr += r * r;
+            ff += f * f;
+          } else {
+            out[l * nx + (xs + p) * n1 + iy] = acc;
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int p = 0; p < PT; ++p) {
+      mu_prev[p] = mu[p];
+      au_prev[p] = au[p];
+    }
+    cur = cur + 1 == kStages ? 0 : cur + 1;
+    nxt = nxt + 1 == kStages ? 0 : nxt + 1;
+  }
+  cp_async_wait<0>();
+  if (RESIDUAL) {
+    __shared__ double red[8];
+    rr = block_sum<256>(rr, red);
+    ff = block_sum<256>(ff, red);
+    if (threadIdx.x == 0) {
+      partials[2 * blockIdx.x] = rr;
+      partials[2 * blockIdx.x + 1] = ff;
+    }
+  }
+}
+
 // Sum interleaved partial pairs in a fixed order (deterministic).
 __global__ void __launch_bounds__(256) sum_pairs_kernel(const double* partials, int64_t count,
                                                         double* result) {
@@ -849,7 +1028,21 @@ int64_t apply_tiles(const stkg_heat& h) {
   return ceil_div(h.n[0], T::BX) * ceil_div(h.n[1], T::BY) * ceil_div(h.n[2], T::BZ);
 }
 
+// 2D: tiles x time chunks of heat_apply2d_kernel (STKG_K1_2D=0: the generic kernel)
+bool use_apply2d() {
+  static const bool on = [] {
+    const char* e = std::getenv("STKG_K1_2D");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+int64_t apply2d_blocks(const stkg_heat& h, int64_t nt) {
+  return ceil_div(h.n[0], Apply2D::BX) * ceil_div(h.n[1], Apply2D::BY) *
+         std::max<int64_t>(1, ceil_div(nt, Apply2D::kChunk));
+}
+
 int64_t apply_blocks(const stkg_heat& h) {
+  if (h.ndim == 2 && use_apply2d()) return apply2d_blocks(h, h.nt);
   return h.ndim == 1 ? apply_tiles<1>(h) : (h.ndim == 2 ? apply_tiles<2>(h) : apply_tiles<3>(h));
 }
 
@@ -861,6 +1054,22 @@ void launch_apply(stkg_heat& h, const double* U, const double* F, double* out, i
   for (int i = 0; i < 3; ++i) {
     m[i] = Tri{h.m_diag[i].p, h.m_off[i].p};
     a[i] = Tri{h.a_diag[i].p, h.a_off[i].p};
+  }
+  if constexpr (NDIM == 2) {
+    if (use_apply2d()) {
+      static const bool configured2 = [] {
+        STKG_CUDA_CHECK(cudaFuncSetAttribute(heat_apply2d_kernel<RES>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(apply2d_smem<RES>())));
+        return true;
+      }();
+      (void)configured2;
+      heat_apply2d_kernel<RES><<<static_cast<unsigned>(apply2d_blocks(h, nt)), 256,
+                                 apply2d_smem<RES>(), h.stream>>>(
+          U, F, out, h.n[0], h.n[1], nt, m[0], m[1], a[0], a[1], dd, ds, cd, cs, h.partials.p);
+      STKG_CUDA_CHECK(cudaGetLastError());
+      return;
+    }
   }
   using SM = ApplySmem<NDIM, RES>;
   static const bool configured = [] {
