@@ -32,6 +32,8 @@
 #define STKG_HALF_V 16
 #endif
 
+#include <cuda.h>  // CUtensorMap (the TMA descriptor type; the encoder is fetched at run time)
+
 #include "dst.cuh"
 
 namespace stkg {
@@ -695,6 +697,124 @@ __global__ void __launch_bounds__(HalfStrided2Cfg<N, PP, PF>::kThreads,
     __syncthreads();  // every pair has read the tile: the regions / the next tile may overwrite it
     if (PF && tile + gridDim.x < ntiles) load_tile(tile_base(tile + gridDim.x));
     half_fft_post<N, V>(x, region, tw2, t, hs, red[f], OutPair<N>{region}, P > 1 ? 1 + f : 0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < P * n; e += C::kThreads) {
+      const int q = e % P, kk = e / P;
+      __stcs(reinterpret_cast<double2*>(dst + base + int64_t(kk) * inner + 2 * q),
+             sreg[q * RG + OutPair<N>::idx(kk)]);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// Strided axis, TMA variant of dst_half_strided2_kernel for tiles of 4 pairs (64-byte rows,
+// N = 512, 1024): one thread arms an mbarrier and issues the tile as ceil(n / 256) 2D TMA
+// boxes of {8 doubles, 256 rows} with SWIZZLE_64B, which lands exactly the swizzled row
+// mirror the pre-processing reads (16-byte chunk c of row r at c ^ ((r >> 1) & 3)).  The
+// copy leaves the LSU pipe: no per-thread cp.async instructions, address arithmetic or
+// shared-memory store wavefronts.  The tensor map views the buffer as [outer * n rows] x
+// [inner columns] (row stride inner * 8 bytes); the last box's extra rows read the next
+// block's first rows (or are zero-filled past the end) and are never used.
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(a), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(a), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(a), "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* smem, const CUtensorMap* map, int c0, int c1,
+                                            uint64_t* bar) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  const unsigned b = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3}], [%4];\n" ::"r"(s),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(b)
+      : "memory");
+}
+
+template <int N>
+struct HalfStridedTmaCfg {
+  using B = HalfStrided2Cfg<N, 4, false>;
+#ifdef STKG_TMA_BOX
+  static constexpr int kBoxRows = STKG_TMA_BOX;
+#else
+  static constexpr int kBoxRows = 256;
+#endif
+  static constexpr int kBoxes = (N - 1 + kBoxRows - 1) / kBoxRows;
+  static constexpr int kTileBytes = kBoxes * kBoxRows * 64;
+  static constexpr size_t kRegionsBytes = size_t(B::P) * B::kRegion * sizeof(double2);
+  // + 512 bytes so the tile can be aligned to the 512-byte SWIZZLE_64B pattern
+  static constexpr size_t kSmem =
+      (kRegionsBytes > size_t(kTileBytes) ? kRegionsBytes : size_t(kTileBytes)) + 512;
+  static_assert(B::T >= 32, "TMA variant: tiles of 4 pairs (whole-warp FFTs)");
+};
+
+template <int N>
+__global__ void __launch_bounds__(HalfStrided2Cfg<N, 4, false>::kThreads,
+                                  HalfStrided2Cfg<N, 4, false>::kMinBlocks)
+    dst_half_strided_tma_kernel(const __grid_constant__ CUtensorMap map, double* dst,
+                                int64_t inner, int64_t nvec, const double2* __restrict__ tw2,
+                                double scale) {
+  using C = HalfStrided2Cfg<N, 4, false>;
+  using TC = HalfStridedTmaCfg<N>;
+  constexpr int V = C::V, T = C::T, P = C::P, G = C::G, n = N - 1, RG = C::kRegion;
+  extern __shared__ __align__(128) unsigned char sraw[];
+  double2* sreg = reinterpret_cast<double2*>(
+      (reinterpret_cast<uintptr_t>(sraw) + 511) & ~uintptr_t(511));
+  __shared__ double red[P][T > 32 ? 2 * (T / 32) : 2];
+  __shared__ __align__(8) uint64_t bar;
+  const int f = threadIdx.x / T, t = threadIdx.x % T;
+  double2* region = sreg + f * RG;
+  const int64_t ntiles = nvec / G;  // the host guarantees inner % G == 0
+  const double hs = 0.5 * scale;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  unsigned phase = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t g = tile * G;
+    const int64_t o = g / inner, i0 = g - o * inner;
+    const int64_t base = o * n * inner + i0;
+    __syncthreads();  // the previous tile's stores have read the regions (and bar is set up)
+    if (threadIdx.x == 0) {
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      mbar_arrive_expect_tx(&bar, TC::kTileBytes);
+#pragma unroll
+      for (int b = 0; b < TC::kBoxes; ++b)
+        tma_load_2d(reinterpret_cast<char*>(sreg) + b * TC::kBoxRows * 64, &map,
+                    static_cast<int>(i0), static_cast<int>(o * n + b * TC::kBoxRows), &bar);
+    }
+    mbar_wait(&bar, phase);
+    phase ^= 1u;
+    double2 x[V];
+#pragma unroll
+    for (int p = 0; p < V; ++p) {
+      const int m = t + T * p;
+      x[p] = make_double2(0.0, 0.0);
+      if (m > 0) {
+        const int r0 = m - 1, r1 = N - m - 1;
+        const double s = -__ldg(&tw2[m].y);
+        const double2 u = sreg[r0 * P + C::chunk(r0, f)], w = sreg[r1 * P + C::chunk(r1, f)];
+        x[p] = half_pre(s, u.x, w.x, u.y, w.y);
+      }
+    }
+    __syncthreads();  // every pair has read the tile: the regions may overwrite it
+    half_fft_post<N, V>(x, region, tw2, t, hs, red[f], OutPair<N>{region}, 1 + f);
     __syncthreads();
     for (int e = threadIdx.x; e < P * n; e += C::kThreads) {
       const int q = e % P, kk = e / P;

@@ -19,6 +19,8 @@
 #include <string>
 #include <vector>
 
+#include <cudaTypedefs.h>  // PFN_cuTensorMapEncodeTiled
+
 #include "common.cuh"
 #include "dst.cuh"
 #include "dst_half.cuh"
@@ -690,6 +692,77 @@ void launch_dst(const stkg_heat& h, int a, const double* src, double* dst, int64
   STKG_CUDA_CHECK(cudaGetLastError());
 }
 
+// TMA descriptors: cuTensorMapEncodeTiled is a driver entry point, fetched through the
+// runtime (the library links only cudart_static).
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    STKG_CUDA_CHECK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    STKG_REQUIRE(p && q == cudaDriverEntryPointSuccess, STKG_CUDA,
+                 "cuTensorMapEncodeTiled entry point not available");
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+
+CUtensorMapL2promotion tma_promotion() {  // STKG_TMA_PROMO = 0 / 64 / 128 / 256 (default 0)
+  static const CUtensorMapL2promotion v = [] {
+    const char* e = std::getenv("STKG_TMA_PROMO");
+    const int b = e ? std::atoi(e) : 0;
+    return b == 256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+                    : b == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                               : b == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                                         : CU_TENSOR_MAP_L2_PROMOTION_NONE;
+  }();
+  return v;
+}
+
+// Opt-in (STKG_TMA=1): measured 5% slower than the cp.async staging on the cfg3 strided
+// passes (355 vs 336 us per 64 slices, same DRAM bytes, any box height or L2 promotion;
+// tools/tma_promo.sh) -- a single thread's TMA boxes of 64-byte rows land later than 256
+// threads' 16-byte cp.async copies of the same tile.
+bool use_tma_strided() {
+  static const bool on = [] {
+    const char* e = std::getenv("STKG_TMA");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
+// Strided pass over [outer * n rows] x [inner columns] (row stride inner * 8 bytes) with
+// the TMA kernel; tiles of 4 vector pairs = 8 columns of 64-byte rows.
+template <int N>
+void launch_dst_half_strided_tma(const stkg_heat& h, const double* src, double* dst,
+                                 int64_t inner, int64_t outer, const double2* tw2,
+                                 double scale) {
+  using C = HalfStrided2Cfg<N, 4, false>;
+  using TC = HalfStridedTmaCfg<N>;
+  const int64_t nvec = outer * inner;
+  CUtensorMap map;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer * (N - 1))};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(inner * sizeof(double))};
+  const cuuint32_t box[2] = {8, TC::kBoxRows};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = tensor_map_encoder()(
+      &map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(src), dims, strides, box,
+      estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+      tma_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  STKG_REQUIRE(r == CUDA_SUCCESS, STKG_CUDA, "cuTensorMapEncodeTiled failed");
+  static const int per_sm = [] {
+    STKG_CUDA_CHECK(cudaFuncSetAttribute(dst_half_strided_tma_kernel<N>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(TC::kSmem)));
+    int b = 0;
+    STKG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &b, dst_half_strided_tma_kernel<N>, C::kThreads, TC::kSmem));
+    return std::max(b, 1);
+  }();
+  const int64_t blocks = std::min<int64_t>(nvec / C::G, int64_t(148) * per_sm);
+  dst_half_strided_tma_kernel<N><<<static_cast<unsigned>(blocks), C::kThreads, TC::kSmem,
+                                   h.stream>>>(map, dst, inner, nvec, tw2, scale);
+}
+
 template <int N, int P, bool PF>
 void launch_dst_half_strided2(const stkg_heat& h, const double* src, double* dst, int64_t inner,
                               int64_t nvec, const double2* tw2, double scale) {
@@ -734,6 +807,14 @@ void launch_dst_half(const stkg_heat& h, int a, const double* src, double* dst, 
     dst_half_kernel<N><<<static_cast<unsigned>(blocks), C::kThreads, C::kSmem, h.stream>>>(
         src, dst, nvec, tw2, scale, lds, ldd);
   } else if (wide && inner % HalfStrided2Cfg<N>::G == 0) {
+    if constexpr (N / half_v<N>() >= 32) {  // tiles of 4 pairs: optional TMA staging
+      if (use_tma_strided() && (reinterpret_cast<uintptr_t>(src) & 15) == 0 &&
+          outer * (N - 1) < (int64_t(1) << 31) && inner < (int64_t(1) << 31)) {
+        launch_dst_half_strided_tma<N>(h, src, dst, inner, outer, tw2, scale);
+        STKG_CUDA_CHECK(cudaGetLastError());
+        return;
+      }
+    }
     if constexpr (N == 1024) {  // tuning variants: STKG_HALF2 = pairs * 10 + prefetch
       static const int var = [] {
         const char* e = std::getenv("STKG_HALF2");

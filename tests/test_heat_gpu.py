@@ -453,3 +453,21 @@ def test_padded_layout_equals_unpadded(tmp_path):
         res[pad] = dict(np.load(f))
     for k in res["1"]:
         assert rel(res["1"][k], res["0"][k]) < 1e-13, (k, rel(res["1"][k], res["0"][k]))
+
+
+def test_tma_strided_variant_matches(tmp_path):
+    """The opt-in TMA staging of the strided DST pass (STKG_TMA=1: SWIZZLE_64B boxes into the
+    same swizzled row mirror) computes bit for bit what the cp.async staging computes."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = str(Path(__file__).resolve().parent.parent)
+    res = {}
+    for tma in ("1", "0"):
+        f = tmp_path / f"tma{tma}.npz"
+        env = dict(os.environ, STKG_TMA=tma)
+        subprocess.run([sys.executable, "-c", _PAD_SCRIPT, root, str(f)], check=True, env=env)
+        res[tma] = dict(np.load(f))
+    for k in res["1"]:
+        assert np.array_equal(res["1"][k], res["0"][k]), k
