@@ -1303,11 +1303,11 @@ int64_t apply_tiles(const stkg_heat& h) {
   return ceil_div(h.n[0], T::BX) * ceil_div(h.n[1], T::BY) * ceil_div(h.n[2], T::BZ);
 }
 
-// 2D / 3D: tiles x time chunks of heat_apply2d_kernel / heat_apply3d_kernel (STKG_K1_2D=0:
+// 2D / 3D: tiles x time chunks of heat_apply2d_kernel / heat_apply3d_kernel (STKG_K1_XMARCH=0:
 // the generic kernel)
-bool use_apply2d() {
+bool use_apply_xmarch() {
   static const bool on = [] {
-    const char* e = std::getenv("STKG_K1_2D");
+    const char* e = std::getenv("STKG_K1_XMARCH");
     return !(e && e[0] == '0');
   }();
   return on;
@@ -1323,8 +1323,8 @@ int64_t apply3d_blocks(const stkg_heat& h, int64_t nt) {
 }
 
 int64_t apply_blocks(const stkg_heat& h) {
-  if (h.ndim == 2 && use_apply2d()) return apply2d_blocks(h, h.nt);
-  if (h.ndim == 3 && use_apply2d()) return apply3d_blocks(h, h.nt);
+  if (h.ndim == 2 && use_apply_xmarch()) return apply2d_blocks(h, h.nt);
+  if (h.ndim == 3 && use_apply_xmarch()) return apply3d_blocks(h, h.nt);
   return h.ndim == 1 ? apply_tiles<1>(h) : (h.ndim == 2 ? apply_tiles<2>(h) : apply_tiles<3>(h));
 }
 
@@ -1338,7 +1338,7 @@ void launch_apply(stkg_heat& h, const double* U, const double* F, double* out, i
     a[i] = Tri{h.a_diag[i].p, h.a_off[i].p};
   }
   if constexpr (NDIM == 2) {
-    if (use_apply2d()) {
+    if (use_apply_xmarch()) {
       static const bool configured2 = [] {
         STKG_CUDA_CHECK(cudaFuncSetAttribute(heat_apply2d_kernel<RES>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1354,7 +1354,7 @@ void launch_apply(stkg_heat& h, const double* U, const double* F, double* out, i
     }
   }
   if constexpr (NDIM == 3) {
-    if (use_apply2d()) {
+    if (use_apply_xmarch()) {
       static const bool configured3 = [] {
         STKG_CUDA_CHECK(cudaFuncSetAttribute(heat_apply3d_kernel<RES>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
