@@ -471,3 +471,40 @@ def test_tma_strided_variant_matches(tmp_path):
         res[tma] = dict(np.load(f))
     for k in res["1"]:
         assert np.array_equal(res["1"][k], res["0"][k]), k
+
+
+_K1_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_1912_10082_b200 as stk
+out = {}
+for ndim, n, nt in [(2, 1023, 70), (2, 45, 9), (3, 127, 5), (3, 21, 66)]:
+    rng = np.random.default_rng(n + nt)
+    U = torch.from_numpy(rng.standard_normal((nt, n ** ndim))).cuda()
+    F = torch.from_numpy(rng.standard_normal((nt, n ** ndim))).cuda()
+    p = stk.HeatPlan.p1_uniform(ndim, n, nt, transform="dense")  # K1 is backend-independent
+    out[f"a{ndim}_{n}"] = p.apply(U).cpu().numpy()
+    out[f"r{ndim}_{n}"] = np.array(p.residual(U, F))
+np.savez(sys.argv[2], **out)
+"""
+
+
+def test_k1_xmarch_matches_generic(tmp_path):
+    """The x-marching K1 kernels (2D and 3D; time-chunked grids, including chunk starts that
+    re-derive the previous slice) against the generic kernel: operator to 1e-14, residual
+    and ||F|| to 1e-12 (different summation order)."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = str(Path(__file__).resolve().parent.parent)
+    res = {}
+    for v in ("1", "0"):
+        f = tmp_path / f"k1{v}.npz"
+        env = dict(os.environ, STKG_K1_XMARCH=v)
+        subprocess.run([sys.executable, "-c", _K1_SCRIPT, root, str(f)], check=True, env=env)
+        res[v] = dict(np.load(f))
+    for k in res["1"]:
+        a, b = res["1"][k], res["0"][k]
+        tol = 1e-14 if k.startswith("a") else 1e-12
+        assert rel(a, b) < tol, (k, rel(a, b))
