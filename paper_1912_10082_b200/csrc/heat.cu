@@ -107,8 +107,19 @@ __global__ void __launch_bounds__(256) heat_scan_kernel(
 // g~_j[i] = sum_r Lt[i, r] R[j, r] is formed in registers (Lt = X^T L, n_x x rank), and the
 // recurrence writes Y~ (n_x x n_t) -- 8 B/unknown of HBM traffic instead of 16.
 constexpr int kMaxFactorRank = 16;
+//
+// UNI (uniform time grid: every d_j, c_j, d^s_j, c^s_j equal): the pivot and coupling of a
+// mode are the same at every step, so the step is y = (g - b y) * (1 / piv) with the
+// reciprocal formed once per mode.  Without a transformed load to stream this kernel is
+// bound by the per-step FP64 division (a ~25-instruction Newton sequence), not by its
+// 8 B/unknown of stores; the reciprocal differs from the reference's division by at most
+// an ulp per step.
+// RP: the rank rounded up to 2/4/8/16; Rt holds R transposed and zero-padded, Rt[l RP + r]
+// (factor_transpose_kernel), so a step's RP coefficients are RP/2 broadcast 16-byte loads
+// (indexing R[r nt + l] under a runtime rank cost ~190 instructions per warp and step).
+template <bool UNI, int RP>
 __global__ void __launch_bounds__(256) heat_scan_factored_kernel(
-    const double* __restrict__ Lt, const double* __restrict__ R, int rank, double* __restrict__ Y,
+    const double* __restrict__ Lt, const double* __restrict__ Rt, int rank, double* __restrict__ Y,
     int64_t nx, int64_t nt, ModeLambda lam, ModeWeight wgt, const double* __restrict__ d_diag,
     const double* __restrict__ d_sup, const double* __restrict__ c_diag,
     const double* __restrict__ c_sup, int64_t pitch, int64_t nl) {
@@ -126,21 +137,66 @@ __global__ void __launch_bounds__(256) heat_scan_factored_kernel(
     nxu = nx / pitch * nl;
     pad = rr >= nl;
   }
-  double lt[kMaxFactorRank];
+  double lt[RP];
 #pragma unroll
-  for (int r = 0; r < kMaxFactorRank; ++r)
+  for (int r = 0; r < RP; ++r)
     lt[r] = (r < rank && !pad) ? Lt[int64_t(r) * nxu + iu] : 0.0;
-  double y = 0.0;
-  for (int64_t l = 0; l < nt; ++l) {
+  auto load_g = [&](int64_t l) {
+    const double2* rl = reinterpret_cast<const double2*>(Rt + l * RP);
     double g = 0.0;
 #pragma unroll
-    for (int r = 0; r < kMaxFactorRank; ++r)
-      if (r < rank) g += lt[r] * __ldg(R + int64_t(r) * nt + l);
-    const double piv = d_diag[l] + li * c_diag[l];
-    if (l > 0) g -= (d_sup[l - 1] + li * c_sup[l - 1]) * y;
-    y = g / piv;
-    __stcs(Y + l * nx + i, wi * y);
+    for (int k = 0; k < RP / 2; ++k) {
+      const double2 v = __ldg(rl + k);
+      g = fma(lt[2 * k], v.x, g);
+      g = fma(lt[2 * k + 1], v.y, g);
+    }
+    return g;
+  };
+  double y = 0.0;
+  if constexpr (UNI) {
+    const double rpiv = 1.0 / (d_diag[0] + li * c_diag[0]);
+    const double b = nt > 1 ? d_sup[0] + li * c_sup[0] : 0.0;
+    for (int64_t l = 0; l < nt; ++l) {
+      const double g = load_g(l);
+      y = fma(-b, y, g) * rpiv;  // y_{-1} = 0
+      __stcs(Y + l * nx + i, wi * y);
+    }
+  } else {
+    for (int64_t l = 0; l < nt; ++l) {
+      double g = load_g(l);
+      const double piv = d_diag[l] + li * c_diag[l];
+      if (l > 0) g -= (d_sup[l - 1] + li * c_sup[l - 1]) * y;
+      y = g / piv;
+      __stcs(Y + l * nx + i, wi * y);
+    }
   }
+}
+
+using FactoredScanFn = void (*)(const double*, const double*, int, double*, int64_t, int64_t,
+                               ModeLambda, ModeWeight, const double*, const double*,
+                               const double*, const double*, int64_t, int64_t);
+int factor_rp(int64_t rank) { return rank <= 2 ? 2 : rank <= 4 ? 4 : rank <= 8 ? 8 : 16; }
+template <bool UNI>
+FactoredScanFn factored_fn(int rp) {
+  switch (rp) {
+    case 2: return heat_scan_factored_kernel<UNI, 2>;
+    case 4: return heat_scan_factored_kernel<UNI, 4>;
+    case 8: return heat_scan_factored_kernel<UNI, 8>;
+    default: return heat_scan_factored_kernel<UNI, 16>;
+  }
+}
+FactoredScanFn launch_factored(bool uniform, int rp) {
+  static const bool on = !(std::getenv("STKG_SCAN_RECIP") && std::getenv("STKG_SCAN_RECIP")[0] == '0');
+  return uniform && on ? factored_fn<true>(rp) : factored_fn<false>(rp);
+}
+
+// Rt[l rp + r] = R[r nt + l] for r < rank, 0 for rank <= r < rp.
+__global__ void factor_transpose_kernel(const double* __restrict__ R, int64_t rank, int64_t nt,
+                                        int rp, double* __restrict__ Rt) {
+  const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= nt * rp) return;
+  const int64_t l = e / rp, r = e % rp;
+  Rt[e] = r < rank ? R[r * nt + l] : 0.0;
 }
 
 // Singularity check of stk/sylvester.hpp:133-135, done once per plan: min over modes and
@@ -1507,6 +1563,14 @@ int stkg_heat_create(stkg_heat** out, const stkg_heat_desc* desc, void* cuda_str
       STKG_CUDA_CHECK(cudaStreamSynchronize(s));  // host temporaries die here
     }
     const int64_t nt = h->nt;
+    {  // uniform time grid: every step has the same bidiagonal coefficients
+      bool u = true;
+      for (int64_t l = 1; l < nt; ++l)
+        u = u && desc->d_diag[l] == desc->d_diag[0] && desc->c_diag[l] == desc->c_diag[0];
+      for (int64_t l = 1; l + 1 < nt; ++l)
+        u = u && desc->d_sup[l] == desc->d_sup[0] && desc->c_sup[l] == desc->c_sup[0];
+      h->uniform_time = u;
+    }
     h->d_diag_h.assign(desc->d_diag, desc->d_diag + nt);
     h->c_diag_h.assign(desc->c_diag, desc->c_diag + nt);
     if (nt > 1) {
@@ -1673,14 +1737,20 @@ int stkg_heat_solve_factored(stkg_heat* h, int64_t rank, const double* L, const 
       axis_pass(*h, a, true, src, dst, rank);
       src = dst;
     }
+    const int rp = factor_rp(rank);
+    if (h->rt.n < static_cast<size_t>(h->nt * rp)) h->rt.alloc(h->nt * rp);
+    factor_transpose_kernel<<<static_cast<unsigned>(ceil_div(h->nt * rp, 256)), 256, 0, h->stream>>>(
+        R, rank, h->nt, rp, h->rt.p);
+    STKG_CUDA_CHECK(cudaGetLastError());
+    const double* Rt = h->rt.p;
     if (h->pitch > 0) {  // padded layout: Y~ in the scratch, inverse passes as run_chunk_padded
       const int64_t nxp = padded_nx(*h), last = h->ndim - 1;
       if (h->scratch.n < static_cast<size_t>(nxp * h->nt)) h->scratch.alloc(nxp * h->nt);
       double* S = h->scratch.p;
       {
         ProfScope ps(*h, 1);
-        heat_scan_factored_kernel<<<static_cast<unsigned>(ceil_div(nxp, 256)), 256, 0, h->stream>>>(
-            src, R, static_cast<int>(rank), S, nxp, h->nt, mode_lambda_padded(*h),
+        launch_factored(h->uniform_time, rp)<<<static_cast<unsigned>(ceil_div(nxp, 256)), 256, 0, h->stream>>>(
+            src, Rt, static_cast<int>(rank), S, nxp, h->nt, mode_lambda_padded(*h),
             mode_weight_padded(*h), h->d_diag.p, h->d_sup.p, h->c_diag.p, h->c_sup.p, h->pitch,
             h->n[last]);
         STKG_CUDA_CHECK(cudaGetLastError());
@@ -1692,8 +1762,8 @@ int stkg_heat_solve_factored(stkg_heat* h, int64_t rank, const double* L, const 
     double* Y = (h->ndim % 2 == 0) ? U : h->scratch.p;
     {
       ProfScope ps(*h, 1);
-      heat_scan_factored_kernel<<<static_cast<unsigned>(ceil_div(h->nx, 256)), 256, 0, h->stream>>>(
-          src, R, static_cast<int>(rank), Y, h->nx, h->nt, mode_lambda(*h), mode_weight(*h), h->d_diag.p,
+      launch_factored(h->uniform_time, rp)<<<static_cast<unsigned>(ceil_div(h->nx, 256)), 256, 0, h->stream>>>(
+          src, Rt, static_cast<int>(rank), Y, h->nx, h->nt, mode_lambda(*h), mode_weight(*h), h->d_diag.p,
           h->d_sup.p, h->c_diag.p, h->c_sup.p, 0, 0);
       STKG_CUDA_CHECK(cudaGetLastError());
     }

@@ -51,6 +51,7 @@ struct stkg_heat {
   // N = n + 1 (0: unpadded); lam/inv_mu of that axis extended by a 0 for the pad lane
   int64_t pitch = 0;
   DevBuf lam_pad, inv_mu_pad;
+  bool uniform_time = false;  // all temporal bidiagonal coefficients equal (factored scan)
   DevBuf d_diag, d_sup, c_diag, c_sup;
   // host copies used by the host-side parts of the rational Krylov solver
   std::vector<double> lam_h[3], d_diag_h, d_sup_h, c_diag_h, c_sup_h;
@@ -65,6 +66,7 @@ struct stkg_heat {
   DevBuf m_diag[3], m_off[3], a_diag[3], a_off[3];
   DevBuf scratch;   // nx * nt, device solve
   DevBuf lfac;      // 2 * nx * rank, transformed load factors (factored solve)
+  DevBuf rt;        // nt * rp, the temporal factor transposed and zero-padded (factored solve)
   DevBuf carry;     // nx, modal state y_{l0-1} carried across time chunks
   DevBuf partials;  // reduction partials
   DevBuf scalars;   // device results of reductions
