@@ -103,6 +103,128 @@ __global__ void __launch_bounds__(256) heat_scan_kernel(
   carry[i] = y;
 }
 
+// Parallel-in-time K3 for plans with few modes (the north_star's "parallel scans batched
+// over modes"): with n_x <= 2^17 one thread per mode leaves most of the GPU idle and the
+// solve is bound by the n_t-step dependency chain.  A CTA of 32 x 32 threads takes 32
+// consecutive modes (lane = mode, coalesced) and cuts time into 32 chunks (warp w = chunk
+// w).  Phase 1: every thread composes its chunk's affine steps y -> a y + g/piv into
+// (A, B); phase 2: warp 0 chains the 32 composites into each chunk's carry-in; phase 3:
+// every thread reruns its chunk from its carry-in with the reference's step
+// y = (g - sub y) / piv.  The dependency chain drops from n_t to about 2 n_t/32 + 32 steps;
+// the carries differ from the sequential ones in rounding only (P1_DST plans, whose
+// host-buffer path is not bitwise-equal to the device path anyway), and g is read twice.
+// LREG > 0: chunks of at most LREG steps keep their g in registers between phases 1 and
+// 3 (g read once, 16 B/unknown as in heat_scan_kernel); LREG = 0: g is re-read in phase 3.
+constexpr int64_t kChunkedScanMaxModes = int64_t(1) << 17;
+template <int LREG>
+__global__ void __launch_bounds__(1024) heat_scan_chunked_kernel(
+    double* __restrict__ Y, int64_t nx, int64_t ntc, int64_t l0, ModeLambda lam, ModeWeight wgt,
+    const double* __restrict__ d_diag, const double* __restrict__ d_sup,
+    const double* __restrict__ c_diag, const double* __restrict__ c_sup,
+    double* __restrict__ carry) {
+  __shared__ double sA[32][33], sB[32][33];  // [chunk][mode]
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t i = int64_t(blockIdx.x) * 32 + lane;
+  const bool ok = i < nx;
+  const int64_t L = (ntc + 31) / 32, lb = w * L, le = lb + L < ntc ? lb + L : ntc;
+  const double li = ok ? lam(i) : 0.0, wi = ok ? wgt(i) : 0.0;
+  double A = 1.0, B = 0.0;
+  double gr[LREG > 0 ? LREG : 1];
+  // LREG > 0 (uniform grids): y = (g - sub y) / piv with the mode's constant piv, sub
+  const double upiv = d_diag[0] + li * c_diag[0];
+  const double usub = ntc + l0 > 1 ? d_sup[0] + li * c_sup[0] : 0.0;
+  const double urp = LREG > 0 ? 1.0 / upiv : 0.0, ua = -usub * urp;
+  if constexpr (LREG > 0) {
+#pragma unroll
+    for (int k = 0; k < LREG; ++k) gr[k] = (ok && lb + k < le) ? __ldcs(Y + (lb + k) * nx + i) : 0.0;
+  }
+  if (ok) {
+    if constexpr (LREG > 0) {  // uniform time grid: one pivot and coupling per mode
+#pragma unroll
+      for (int k = 0; k < LREG; ++k) {
+        if (lb + k < le) {
+          const double a = l0 + lb + k > 0 ? ua : 0.0;
+          A *= a;
+          B = fma(a, B, gr[k] * urp);
+        }
+      }
+    } else {
+      for (int64_t l = lb; l < le; ++l) {
+        const int64_t gl = l0 + l;
+        const double piv = d_diag[gl] + li * c_diag[gl];
+        const double sub = gl > 0 ? d_sup[gl - 1] + li * c_sup[gl - 1] : 0.0;
+        const double a = -sub / piv;
+        A *= a;
+        B = fma(a, B, __ldcs(Y + l * nx + i) / piv);
+      }
+    }
+  }
+  sA[w][lane] = A;
+  sB[w][lane] = B;
+  __syncthreads();
+  if (w == 0) {
+    double c = (ok && l0 > 0) ? carry[i] : 0.0;
+    for (int k = 0; k < 32; ++k) {
+      const double a = sA[k][lane], b = sB[k][lane];
+      sA[k][lane] = c;  // carry-in y_{lb - 1} of chunk k
+      c = fma(a, c, b);
+    }
+  }
+  __syncthreads();
+  double y = sA[w][lane];
+  if (ok && lb < le) {
+    if constexpr (LREG > 0) {
+#pragma unroll
+      for (int k = 0; k < LREG; ++k) {
+        if (lb + k < le) {
+          double rhs = gr[k];
+          if (l0 + lb + k > 0) rhs -= usub * y;
+          y = rhs * urp;
+          __stcs(Y + (lb + k) * nx + i, wi * y);
+        }
+      }
+    } else {
+      for (int64_t l = lb; l < le; ++l) {
+        const int64_t gl = l0 + l;
+        const double piv = d_diag[gl] + li * c_diag[gl];
+        double rhs = Y[l * nx + i];
+        if (gl > 0) rhs -= (d_sup[gl - 1] + li * c_sup[gl - 1]) * y;
+        y = rhs / piv;
+        __stcs(Y + l * nx + i, wi * y);
+      }
+    }
+    if (le == ntc) carry[i] = y;
+  }
+}
+
+// Which K3 kernel a scan over nm modes and ntc steps uses: 0 = heat_scan_kernel (one
+// chain per mode), 1 = chunked with g in registers (ntc <= 32 * 16), 2 = chunked with g
+// re-read (only for very few modes, where the chain latency dwarfs the second read).
+// Measured (cfg1 1D 255 x 256): 53.5 -> 14.6 us with the re-read form; the re-read form
+// lost at cfg2 (65,280 modes x 512: 215 -> 267 us, it moves 24 B/unknown).
+int scan_variant(const stkg_heat& h, int64_t nm, int64_t ntc) {
+  static const bool on = !(std::getenv("STKG_SCAN_CHUNKED") && std::getenv("STKG_SCAN_CHUNKED")[0] == '0');
+  if (!on || h.transform != STKG_TRANSFORM_P1_DST || nm > kChunkedScanMaxModes) return 0;
+  if (h.uniform_time && ntc <= 32 * 16) return 1;
+  return nm <= 8192 ? 2 : 0;
+}
+
+template <class LAM, class WGT>
+void launch_scan(const stkg_heat& h, double* Y, int64_t nm, int64_t ntc, int64_t l0, LAM lam,
+                 WGT wgt) {
+  const int v = scan_variant(h, nm, ntc);
+  if (v == 1)
+    heat_scan_chunked_kernel<16><<<static_cast<unsigned>(ceil_div(nm, 32)), 1024, 0, h.stream>>>(
+        Y, nm, ntc, l0, lam, wgt, h.d_diag.p, h.d_sup.p, h.c_diag.p, h.c_sup.p, h.carry.p);
+  else if (v == 2)
+    heat_scan_chunked_kernel<0><<<static_cast<unsigned>(ceil_div(nm, 32)), 1024, 0, h.stream>>>(
+        Y, nm, ntc, l0, lam, wgt, h.d_diag.p, h.d_sup.p, h.c_diag.p, h.c_sup.p, h.carry.p);
+  else
+    heat_scan_kernel<<<static_cast<unsigned>(ceil_div(nm, 256)), 256, 0, h.stream>>>(
+        Y, nm, ntc, l0, lam, wgt, h.d_diag.p, h.d_sup.p, h.c_diag.p, h.c_sup.p, h.carry.p);
+  STKG_CUDA_CHECK(cudaGetLastError());
+}
+
 // Factored load F = L R^T: the transformed load is never stored;
 // g~_j[i] = sum_r Lt[i, r] R[j, r] is formed in registers (Lt = X^T L, n_x x rank), and the
 // recurrence writes Y~ (n_x x n_t) -- 8 B/unknown of HBM traffic instead of 16.
@@ -1244,9 +1366,7 @@ void run_chunk_padded(stkg_heat& h, const double* F, double* U, double* S, int64
   {
     const int64_t nxp = padded_nx(h);
     ProfScope ps(h, 1);
-    heat_scan_kernel<<<static_cast<unsigned>(ceil_div(nxp, 256)), 256, 0, h.stream>>>(
-        S, nxp, ntc, l0, mode_lambda_padded(h), mode_weight_padded(h), h.d_diag.p, h.d_sup.p,
-        h.c_diag.p, h.c_sup.p, h.carry.p);
+    launch_scan(h, S, nxp, ntc, l0, mode_lambda_padded(h), mode_weight_padded(h));
     STKG_CUDA_CHECK(cudaGetLastError());
   }
   for (int a = 0; a < last; ++a) strided(a);
@@ -1289,9 +1409,8 @@ void run_chunk(stkg_heat& h, const double* F, double* U, double* S, int64_t l0, 
     double* Y = const_cast<double*>(src);
     const int64_t blocks = ceil_div(h.nx, 256);
     ProfScope ps(h, 1);
-    heat_scan_kernel<<<static_cast<unsigned>(blocks), 256, 0, h.stream>>>(
-        Y, h.nx, ntc, l0, mode_lambda(h), mode_weight(h), h.d_diag.p, h.d_sup.p, h.c_diag.p,
-        h.c_sup.p, h.carry.p);
+    (void)blocks;
+    launch_scan(h, Y, h.nx, ntc, l0, mode_lambda(h), mode_weight(h));
     STKG_CUDA_CHECK(cudaGetLastError());
   }
   for (int a = 0; a < d; ++a) {  // inverse, slowest axis first
