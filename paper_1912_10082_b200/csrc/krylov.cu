@@ -139,18 +139,14 @@ void fetch(Krylov& k, int count, double* out) {
   for (int i = 0; i < count; ++i) out[i] = k.pinned[i];
 }
 
-// h = V(:, 0:m)^T x, left on the device in k.hvec and copied to host_h
-void gemv_t(Krylov& k, int m, const double* x, double* host_h) {
+// h = V(:, 0:m)^T x into the device vector out (no host round trip)
+void gemv_t_dev(Krylov& k, int m, const double* x, double* out) {
   dim3 grid(kReduceBlocks, static_cast<unsigned>(ceil_div(m, kGemvCols)));
   gemv_t_kernel<<<grid, kReduceThreads, 0, k.stream>>>(k.V.p, k.N, m, x, k.partials.p);
-  sum_partials_kernel<<<m, kReduceThreads, 0, k.stream>>>(k.partials.p, kReduceBlocks, k.hvec.p);
+  sum_partials_kernel<<<m, kReduceThreads, 0, k.stream>>>(k.partials.p, kReduceBlocks, out);
   STKG_CUDA_CHECK(cudaGetLastError());
-  k.pin(m);
-  STKG_CUDA_CHECK(cudaMemcpyAsync(k.pinned, k.hvec.p, sizeof(double) * m, cudaMemcpyDeviceToHost,
-                                  k.stream));
-  STKG_CUDA_CHECK(cudaStreamSynchronize(k.stream));
-  for (int i = 0; i < m; ++i) host_h[i] = k.pinned[i];
 }
+
 
 }  // namespace
 
@@ -182,8 +178,8 @@ void Krylov::ensure(int64_t cols, int64_t hcap) {
   const int64_t h = std::max<int64_t>(hcap, 8);
   if (partials.n < static_cast<size_t>(h * kReduceBlocks)) partials.alloc(h * kReduceBlocks);
   if (scalars.n < static_cast<size_t>(h)) scalars.alloc(h);
-  if (hvec.n < static_cast<size_t>(h)) hvec.alloc(h);
-  pin(static_cast<int>(h));  // once: cudaMallocHost synchronises the device
+  if (hvec.n < static_cast<size_t>(2 * h)) hvec.alloc(2 * h);  // two Gram-Schmidt passes
+  pin(static_cast<int>(2 * h + 1));  // once: cudaMallocHost synchronises the device
 }
 
 double kdot(Krylov& k, const double* x, const double* y) {
@@ -251,16 +247,31 @@ void gmres_run(Krylov& k, const DevOp& apply, const DevOp* precond, const double
         apply(vcol(j), k.w.p);
       }
       const int m = j + 1;
-      gemv_t(k, m, k.w.p, h.data());  // (:111-115)
-      gemv_n_update_kernel<<<kReduceBlocks, kReduceThreads, 0, s>>>(k.V.p, N, m, k.hvec.p, k.w.p,
+      // both Gram-Schmidt passes stay on the device (h1 in hvec[0:m), h2 in hvec[hoff:hoff+m));
+      // one host round trip per iteration fetches h1, h2 and ||w||^2 together
+      const int64_t hoff = k.hvec.n / 2;
+      double* h1d = k.hvec.p;
+      double* h2d = k.hvec.p + hoff;
+      gemv_t_dev(k, m, k.w.p, h1d);  // (:111-115)
+      gemv_n_update_kernel<<<kReduceBlocks, kReduceThreads, 0, s>>>(k.V.p, N, m, h1d, k.w.p,
                                                                    nullptr);
-      gemv_t(k, m, k.w.p, corr.data());  // re-orthogonalisation (:116-120)
-      gemv_n_update_kernel<<<kReduceBlocks, kReduceThreads, 0, s>>>(k.V.p, N, m, k.hvec.p, k.w.p,
+      gemv_t_dev(k, m, k.w.p, h2d);  // re-orthogonalisation (:116-120)
+      gemv_n_update_kernel<<<kReduceBlocks, kReduceThreads, 0, s>>>(k.V.p, N, m, h2d, k.w.p,
                                                                    k.partials.p);
       sum_partials_kernel<<<1, kReduceThreads, 0, s>>>(k.partials.p, kReduceBlocks, k.scalars.p);
       STKG_CUDA_CHECK(cudaGetLastError());
-      double h2;
-      fetch(k, 1, &h2);
+      k.pin(2 * m + 1);
+      STKG_CUDA_CHECK(cudaMemcpyAsync(k.pinned, h1d, sizeof(double) * m, cudaMemcpyDeviceToHost, s));
+      STKG_CUDA_CHECK(cudaMemcpyAsync(k.pinned + m, h2d, sizeof(double) * m,
+                                      cudaMemcpyDeviceToHost, s));
+      STKG_CUDA_CHECK(cudaMemcpyAsync(k.pinned + 2 * m, k.scalars.p, sizeof(double),
+                                      cudaMemcpyDeviceToHost, s));
+      STKG_CUDA_CHECK(cudaStreamSynchronize(s));
+      for (int i = 0; i < m; ++i) {
+        h[i] = k.pinned[i];
+        corr[i] = k.pinned[m + i];
+      }
+      const double h2 = k.pinned[2 * m];
       const double hlast = std::sqrt(h2);
       std::vector<double> col(m + 1, 0.0);
       for (int i = 0; i < m; ++i) col[i] = h[i] + corr[i];
