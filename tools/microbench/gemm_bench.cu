@@ -19,6 +19,9 @@ using C15 = GemmCfg<32, 64, 32, 32, 32, 2, 4>;
 using C16 = GemmCfg<64, 32, 32, 32, 32, 2, 4>;
 using C17 = GemmCfg<32, 32, 32, 32, 32, 2, 8>;
 using C18 = GemmCfg<64, 64, 16, 32, 32, 3, 3>;
+using C19 = GemmCfg<64, 64, 32, 32, 16, 2, 2>;  // 8 warps of 32x16
+using C20 = GemmCfg<64, 64, 32, 16, 32, 2, 2>;  // 8 warps of 16x32
+using C21 = GemmCfg<64, 64, 32, 32, 16, 3, 2>;  // 8 warps, 3 stages
 template <class Cfg>
 float run(const GemmProblem& p, int reps) {
   cudaEvent_t a, b;
@@ -105,6 +108,9 @@ int main() {
     report("C16 64x32x32 s2 x4 2w", run<C16>(s.p, reps));
     report("C17 32x32x32 s2 x8 1w", run<C17>(s.p, reps));
     report("C18 64x64x16 s3 x3", run<C18>(s.p, reps));
+    report("C19 64x64x32 s2 8w 32x16", run<C19>(s.p, reps));
+    report("C20 64x64x32 s2 8w 16x32", run<C20>(s.p, reps));
+    report("C21 64x64x32 s3 8w 32x16", run<C21>(s.p, reps));
   }
   cudaError_t e = cudaGetLastError();
   printf("status %s\n", cudaGetErrorString(e));
