@@ -635,19 +635,30 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 // (OutPair) leave as 16-byte streaming stores.  In place is allowed (src == dst): a tile
 // is read completely before it is written.
 // Default pairs per tile: 4 (64-byte rows) for FFTs of whole warps, else 128 threads.
+#ifndef STKG_HALF2_V
+#define STKG_HALF2_V STKG_HALF_V
+#endif
+// Values per thread of the strided kernel's FFTs (tuning knob STKG_HALF2_V; falls back to
+// half_v when the FFT would not span whole warps).
 template <int N>
-constexpr int half2_pairs() { return N / half_v<N>() >= 32 ? 4 : 128 / (N / half_v<N>()); }
+constexpr int half2_v() { return N / STKG_HALF2_V >= 32 ? STKG_HALF2_V : half_v<N>(); }
+template <int N>
+constexpr int half2_pairs() { return N / half2_v<N>() >= 32 ? 4 : 128 / (N / half2_v<N>()); }
 
 // PF (prefetch): the staged tile gets its own buffer beside the pair regions, and the next
 // tile's copy is issued as soon as every pair has read the current one, so it lands while
 // the FFTs run (more shared memory per CTA, fewer CTAs per SM).
 template <int N, int PP = half2_pairs<N>(), bool PF = false>
 struct HalfStrided2Cfg {
-  static constexpr int V = half_v<N>(), T = N / V;
+  static constexpr int V = half2_v<N>(), T = N / V;
   static constexpr int P = PP;       // vector pairs per tile
   static constexpr int G = 2 * P;    // vectors per tile
   static constexpr int kThreads = P * T;
+#ifdef STKG_HALF2_MINB
+  static constexpr int kMinBlocks = STKG_HALF2_MINB;
+#else
   static constexpr int kMinBlocks = 65536 / (kThreads * 128) < 1 ? 1 : 65536 / (kThreads * 128);
+#endif
   // double2 per pair region (FFT, outputs), rounded to 128 bytes plus a skew: the output
   // copy interleaves the P regions (q = e % P), so consecutive regions start 8/P (P <= 4) or
   // 1 (P >= 8) 16-byte bank groups apart and every quarter-warp phase of 8 16-byte reads
