@@ -218,7 +218,10 @@ def test_factored_load_equals_dense_load(stk, orc, cuda, ndim, n, nt, rank):
                                        (2, 127, 4), (3, 15, 6), (3, 31, 3), (1, 2047, 3),
                                        (2, 1023, 2), (1, 511, 9), (2, 511, 3), (3, 511, 1),
                                        (2, 2047, 1), (1, 1023, 5), (2, 255, 4), (3, 127, 2),
-                                       (2, 31, 3), (3, 63, 1)])
+                                       (2, 31, 3), (3, 63, 1),
+                                       # few modes, long time axes: the chunked parallel-in-time
+                                       # scan (registers for n_t <= 512, re-read beyond)
+                                       (1, 127, 1100), (2, 31, 700), (2, 63, 333), (1, 15, 31)])
 def test_dst_backend_equals_dense_backend(stk, cuda, ndim, n, nt):
     """The P1 fast-sine-transform backend computes the same solve_projected_heat_with as the
     dense DMMA backend on the closed-form eigenbasis (X = S diag(mu^-1/2))."""
