@@ -511,3 +511,18 @@ def test_k1_xmarch_matches_generic(tmp_path):
         a, b = res["1"][k], res["0"][k]
         tol = 1e-14 if k.startswith("a") else 1e-12
         assert rel(a, b) < tol, (k, rel(a, b))
+
+
+@pytest.mark.parametrize("ndim,n,nt", [(2, 1023, 4), (3, 127, 3), (2, 255, 40)])
+def test_dst_padded_solve_deterministic(stk, cuda, ndim, n, nt):
+    """Repeated solves of the padded-layout DST path (16-byte strided kernel with its shared
+    tile/region reuse and per-pair named barriers, L2-prefetching contiguous kernel, scans)
+    and repeated residuals are bit-identical -- a shared-memory race would show here."""
+    rng = np.random.default_rng(n + nt)
+    F = dev(rng.standard_normal((nt, n ** ndim)))
+    p = stk.HeatPlan.p1_uniform(ndim, n, nt, transform="dst")
+    U1 = host(p.solve(F))
+    for _ in range(3):
+        assert np.array_equal(host(p.solve(F)), U1)
+    r1 = p.residual(dev(U1), F)
+    assert p.residual(dev(U1), F) == r1 and r1[0] < 1e-10
