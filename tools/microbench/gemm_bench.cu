@@ -22,6 +22,7 @@ using C18 = GemmCfg<64, 64, 16, 32, 32, 3, 3>;
 using C19 = GemmCfg<64, 64, 32, 32, 16, 2, 2>;  // 8 warps of 32x16
 using C20 = GemmCfg<64, 64, 32, 16, 32, 2, 2>;  // 8 warps of 16x32
 using C21 = GemmCfg<64, 64, 32, 32, 16, 3, 2>;  // 8 warps, 3 stages
+using C22 = GemmCfg<48, 64, 48, 16, 32, 2, 3>;  // 48-row tiles: 374 tiles at the 1k shape
 template <class Cfg>
 float run(const GemmProblem& p, int reps) {
   cudaEvent_t a, b;
@@ -111,6 +112,7 @@ int main() {
     report("C19 64x64x32 s2 8w 32x16", run<C19>(s.p, reps));
     report("C20 64x64x32 s2 8w 16x32", run<C20>(s.p, reps));
     report("C21 64x64x32 s3 8w 32x16", run<C21>(s.p, reps));
+    report("C22 48x64x48 s2 6w", run<C22>(s.p, reps));
   }
   cudaError_t e = cudaGetLastError();
   printf("status %s\n", cudaGetErrorString(e));
