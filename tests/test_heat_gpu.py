@@ -526,3 +526,24 @@ def test_dst_padded_solve_deterministic(stk, cuda, ndim, n, nt):
         assert np.array_equal(host(p.solve(F)), U1)
     r1 = p.residual(dev(U1), F)
     assert p.residual(dev(U1), F) == r1 and r1[0] < 1e-10
+
+
+@pytest.mark.parametrize("env", [{"STKG_HALF2": "20"}, {"STKG_HALF2": "21"}, {"STKG_HALF2": "41"},
+                                 {"STKG_SCAN_CHUNKED": "0"}, {"STKG_SCAN_RECIP": "0"}])
+def test_tuning_variants_match_default(tmp_path, env):
+    """The opt-in tuning variants (strided-tile shapes with and without next-tile prefetch,
+    the one-chain scan for small plans, per-step division in the factored scan) compute the
+    default path's solve to rounding."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = str(Path(__file__).resolve().parent.parent)
+    res = {}
+    for tag, extra in (("v", env), ("d", {})):
+        f = tmp_path / f"{tag}.npz"
+        subprocess.run([sys.executable, "-c", _PAD_SCRIPT, root, str(f)], check=True,
+                       env=dict(os.environ, **extra))
+        res[tag] = dict(np.load(f))
+    for k in res["v"]:
+        assert rel(res["v"][k], res["d"][k]) < 1e-13, (k, rel(res["v"][k], res["d"][k]))
