@@ -44,8 +44,53 @@ UNIT = "unknowns/s"
 # Measured on this pool's B200 (profiles/r01_fp64_peak.txt): DMMA m16n8k16 sustained.
 FP64_PEAK_TFLOPS = 37.11
 FP64_PEAK_SOURCE = "measured DMMA (mma.sync f64) sustained, profiles/r01_fp64_peak.txt"
-HBM_GBS = 6557.4  # MEASURED_PEAKS.json hbm_gbs (driver-measured copy bandwidth)
-CPU_SAMPLE_STEPS = 96  # causal prefix of cfg3 time slices for the CPU leg
+
+
+def _hbm_peak():
+    """MEASURED_PEAKS.json hbm_gbs (driver-measured copy bandwidth on this pool's B200s)."""
+    try:
+        v = float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"])
+        return v, "MEASURED_PEAKS.json hbm_gbs"
+    except Exception:
+        return 6553.9, "fallback: MEASURED_PEAKS.json hbm_gbs of round 1 (file unreadable)"
+
+
+HBM_GBS, HBM_SOURCE = _hbm_peak()
+CPU_SAMPLE_STEPS = 320  # causal prefix of cfg3 time slices for the CPU leg (~10 s)
+REF_MAX_CHUNK = 64  # time slices per oracle call in the streamed reference arm
+# precond = 4 GEMMs of 2 n_h n_h n_t' flop (TwoTermPrecond::solve) + WaveOperator ~84 flop/unknown
+WAVE_FLOP_PER_PCG_ITER = lambda nh, ntb: 4 * 2.0 * nh * nh * ntb + 84.0 * nh * ntb  # noqa: E731
+
+
+def loaded_native_libs():
+    """Shared objects of this repository (and any torch extension) mapped into this process:
+    the evidence that the reference arm runs without the product library."""
+    libs = set()
+    try:
+        for ln in Path("/proc/self/maps").read_text().splitlines():
+            parts = ln.split()
+            if parts and parts[-1].endswith(".so") or ".so." in (parts[-1] if parts else ""):
+                path = parts[-1]
+                if path.startswith(str(ROOT)) or "torch_extensions" in path:
+                    libs.add(os.path.relpath(path, ROOT) if path.startswith(str(ROOT)) else path)
+    except Exception:
+        pass
+    return sorted(libs)
+
+
+def fft_flop_per_unknown(n: int, half: bool) -> float:
+    """Executed flops of one DST-I axis pass per unknown (complex FFT of length L per vector
+    pair, 5 L log2 L / 2 per vector, spread over n entries)."""
+    L = (n + 1) if half else 2 * (n + 1)
+    return 5.0 * L * np.log2(L) / 2.0 / n
+
+
+def workload_config(cfg):
+    """The `config` object both arms print for a heat workload (identical keys and values)."""
+    return {"workload": cfg.name, "unknowns_per_solve": cfg.unknowns, "ndim": cfg.ndim,
+            "n": cfg.n, "nt": cfg.nt, "load_rank": cfg.rank or "full", "seed": 0,
+            "l2_flush": "inputs larger than L2 (F, U 8.6 GB each)" if cfg.unknowns * 8 > 2**30
+            else "none"}
 
 
 def dist_env():
@@ -146,16 +191,20 @@ def build_plan(stk, cfg, stream=None, time_chunk=0, transform="dst"):
 
 
 def cpu_reference_run(cfg, steps: int, seed: int = 0):
-    """The oracle port of solve_projected_heat_with on a causal prefix (steps slices)."""
+    """The oracle port of solve_projected_heat_with on a causal prefix (steps slices),
+    streamed in chunks with the modal recurrence carried; F generation is not timed."""
     from oracle import oracle as O
     from paper_1912_10082_b200 import inputs
-    F = inputs.heat_rhs_host(cfg, seed, nsteps=steps)
     m, a = O.fem1d_matrices(0.0, 1.0, cfg.n)
     d, c = O.heat_time_matrices(cfg.nt)
-    eig = O.p1_pencil_eig(m, a)
-    t0 = time.perf_counter()
-    O.heat_decoupled([eig] * cfg.ndim, d, c, F, nsteps=steps)
-    return time.perf_counter() - t0
+    st = O.DecoupledStream([O.p1_pencil_eig(m, a)] * cfg.ndim, d, c)
+    t = 0.0
+    for j0 in range(0, steps, REF_MAX_CHUNK):
+        F = inputs.heat_rhs_host_slices(cfg, j0, min(j0 + REF_MAX_CHUNK, steps), seed)
+        t0 = time.perf_counter()
+        st.step(F)
+        t += time.perf_counter() - t0
+    return t
 
 
 def cpu_cn_run(cfg, steps: int = 16, seed: int = 0):
@@ -206,29 +255,54 @@ def traffic_from_profiles(kind: str = "gemm"):
 
 
 def run_reference(args):
+    """The reference's CPU path on the SAME workload as the GPU arm: the oracle port of
+    solve_projected_heat_with in tensor form (oracle.DecoupledStream, numpy + all-core BLAS)
+    solving the full n_t time axis, split into args.steps consecutive chunks with the
+    per-mode recurrence carried between them -- so the timed steps together are exactly one
+    full solve of the configuration.  F is generated outside the timed region.  Only the
+    host-only input generator of the package is imported; the product library is not mapped
+    (the line lists what was)."""
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
-    from paper_1912_10082_b200 import inputs
+    from oracle import oracle as O
+    from paper_1912_10082_b200 import inputs  # host-only module: does not load _stk_gpu.so
     cfg = inputs.CONFIGS[args.config]
     cores = os.cpu_count()
-    steps_per = args.ref_sample
-    for _ in range(args.warmup):
-        cpu_reference_run(cfg, max(2, steps_per // 8))
-    times = [cpu_reference_run(cfg, steps_per) for _ in range(args.steps)]
-    t = sum(times)
-    value = cfg.nx * steps_per * args.steps / t
+    m, a = O.fem1d_matrices(0.0, 1.0, cfg.n)
+    d, c = O.heat_time_matrices(cfg.nt)
+    eigs = [O.p1_pencil_eig(m, a)] * cfg.ndim
+    warm = O.DecoupledStream(eigs, d, c)
+    for w in range(args.warmup):  # warms BLAS threads and page-faults the work arrays
+        warm.step(inputs.heat_rhs_host_slices(cfg, w, w + 1))
+    steps = max(1, min(args.steps, cfg.nt))
+    bounds = np.linspace(0, cfg.nt, steps + 1).astype(int)
+    st = O.DecoupledStream(eigs, d, c)
+    t_solve = 0.0
+    t_wall0 = time.perf_counter()
+    for k in range(steps):
+        for j0 in range(bounds[k], bounds[k + 1], REF_MAX_CHUNK):
+            j1 = min(j0 + REF_MAX_CHUNK, bounds[k + 1])
+            F = inputs.heat_rhs_host_slices(cfg, j0, j1)
+            t0 = time.perf_counter()
+            st.step(F)
+            t_solve += time.perf_counter() - t0
+    wall = time.perf_counter() - t_wall0
+    assert st.j == cfg.nt
+    value = cfg.unknowns / t_solve
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
+        "steps": steps, "unknowns_per_step": cfg.unknowns / steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_solve / steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic",
-        "config": {"workload": cfg.name, "parallelism": "cpu",
-                   "sample": f"causal prefix of {steps_per} of {cfg.nt} time slices"},
+        "data": "synthetic", "config": workload_config(cfg),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"oracle heat_decoupled (numpy+BLAS, {cores} threads), "
-                                   f"{steps_per}-slice causal prefix of {args.config}"},
+                         "sample": f"the full {args.config} solve (all {cfg.nt} time slices), "
+                                   f"streamed as {steps} steps of consecutive time chunks "
+                                   f"with the modal recurrence carried; oracle heat_decoupled "
+                                   f"(numpy + {cores}-thread BLAS)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "wall_s_incl_input_generation": wall,
+        "native_so_loaded": loaded_native_libs(),
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -278,20 +352,27 @@ def _timed_path(stk, inputs, cfg, transform, args, stream, barrier, F, U, with_c
         # which sine-transform kernels the plan runs (heat.cu::dst_pass)
         half = (cfg.ndim >= 2 and cfg.n + 1 in (512, 1024)
                 and os.environ.get("STKG_DST_HALF", "1") != "0")
-        L = (cfg.n + 1) if half else 2 * (cfg.n + 1)  # complex FFT length per vector pair
-        fft_flops = 5.0 * L * np.log2(L) / 2.0 / cfg.n  # per element and axis pass
+        fft_flops = fft_flop_per_unknown(cfg.n, half)  # per element and axis pass
         kname = ("dst_half_kernel / dst_half_strided2_kernel (FP64 half-length DST-I: "
                  "N-point Stockham FFT per vector pair)") if half else \
             "dst_axis_kernel / dst_strided_kernel (FP64 padded 2N-point FFT DST-I)"
+        passes = (t_n + s_n) / (args.steps)  # HBM passes of the executed schedule per solve
+        sec = ms / 1e3 / args.steps
+        t_hbm = 16.0 * N / (HBM_GBS * 1e9)  # read F + write U once
+        t_fp64 = (2 * cfg.ndim * fft_flops + 3.0) * N / (FP64_PEAK_TFLOPS * 1e12)
         roof = {"bound": "hbm", "kernel": kname,
                 "achieved": achieved, "peak": HBM_GBS, "unit": "GB/s",
                 "frac": achieved / HBM_GBS,
                 "traffic": traffic_from_profiles("dst_half" if half else "dst"),
                 "binding_resource": binding_from_profiles() if half else None,
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+                "peak_source": HBM_SOURCE,
                 "flop_per_unknown_per_pass": fft_flops,
-                "whole_solve_frac": ((2 * cfg.ndim + 1) * 16.0 * N * args.steps / (ms / 1e3) / 1e9)
-                / HBM_GBS}
+                "whole_solve_frac": max(t_hbm, t_fp64) / sec,
+                "whole_solve_basis": "SURVEY 8(d): T_roof = max(16 B/unknown / HBM, executed "
+                                     "DST + scan flops / FP64 peak) over the measured solve",
+                "whole_solve_roof_ms": 1e3 * max(t_hbm, t_fp64),
+                "hbm_passes_per_solve": passes,
+                "whole_solve_frac_executed_passes": passes * t_hbm / sec}
     roof["share_of_step"] = t_ms / ms
     roof["scan_share_of_step"] = s_ms / ms
     out = {"transform": transform, "ms_per_step": ms / args.steps, "ms": ms,
@@ -300,6 +381,84 @@ def _timed_path(stk, inputs, cfg, transform, args, stream, barrier, F, U, with_c
            "k3_scan": {"ms_per_launch": s_ms / s_n, "gbs": 16.0 * N / (s_ms / s_n / 1e3) / 1e9,
                        "frac_hbm": 16.0 * N / (s_ms / s_n / 1e3) / 1e9 / HBM_GBS}}
     return plan, out, clk
+
+
+def heat_config_leg(stk, inputs, name, stream, steps=10, warmup=3, with_cpu=True,
+                    cpu_slices=None):
+    """One named heat shape: the device solve with dense F resident in
+    HBM (P1_DST backend, CUDA events on the plan stream), the factored-load solve of the same
+    low-rank F, the GPU K1 relres, the whole-solve roofline fraction (T_roof = max(16
+    B/unknown / HBM, executed flops / FP64) over the measured time), and the oracle port of
+    the reference's CPU path on this host (full n_t, or a causal prefix when stated)."""
+    import torch
+    cfg = inputs.CONFIGS[name]
+    N = cfg.unknowns
+    with torch.cuda.stream(stream):
+        plan = stk.HeatPlan.p1_uniform(cfg.ndim, cfg.n, cfg.nt, transform="dst",
+                                       stream=stream.cuda_stream)
+        F = inputs.heat_rhs_device(cfg)
+        U = torch.empty_like(F)
+        for _ in range(warmup):
+            plan.solve(F, out=U)
+        stream.synchronize()
+        plan.profile_begin()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            plan.solve(F, out=U)
+        e1.record(stream)
+        stream.synchronize()
+        prof = plan.profile_end()
+        ms = e0.elapsed_time(e1) / steps
+        relres, _ = plan.residual(U, F)
+        out = {"workload": cfg.name, "unknowns": N, "ms": ms, "value": N / (ms / 1e3),
+               "relres_gpu_k1": relres,
+               "launches_per_solve": (prof["transform"][1] + prof["scan"][1]) / steps}
+        half = cfg.ndim >= 2 and cfg.n + 1 in (512, 1024)
+        fl = (2 * cfg.ndim * fft_flop_per_unknown(cfg.n, half) + 3.0) * N
+        t_roof = max(16.0 * N / (HBM_GBS * 1e9), fl / (FP64_PEAK_TFLOPS * 1e12))
+        out["roofline"] = {"bound": "hbm" if 16.0 * N / HBM_GBS / 1e9 >= fl / FP64_PEAK_TFLOPS
+                           / 1e12 else "fp64", "roof_ms": 1e3 * t_roof,
+                           "frac": t_roof / (ms / 1e3), "flops_executed": fl,
+                           "bytes_alg": 16.0 * N}
+        if cfg.rank:
+            left, right = inputs.heat_factors(cfg)
+            L = torch.tensor(left.T.copy(), device="cuda")
+            R = torch.tensor(right.T.copy(), device="cuda")
+            for _ in range(warmup):
+                plan.solve_factored(L, R, out=U)
+            e0.record(stream)
+            for _ in range(steps):
+                plan.solve_factored(L, R, out=U)
+            e1.record(stream)
+            stream.synchronize()
+            msf = e0.elapsed_time(e1) / steps
+            out["factored"] = {"ms": msf, "value": N / (msf / 1e3),
+                               "bytes_alg": 8.0 * N,
+                               "frac_hbm": 8.0 * N / (HBM_GBS * 1e9) / (msf / 1e3)}
+        plan.close()
+        del F, U
+    if with_cpu:
+        from oracle import oracle as O
+        m, a = O.fem1d_matrices(0.0, 1.0, cfg.n)
+        d, c = O.heat_time_matrices(cfg.nt)
+        st = O.DecoupledStream([O.p1_pencil_eig(m, a)] * cfg.ndim, d, c)
+        nts = cfg.nt if cpu_slices is None else cpu_slices
+        tc = 0.0
+        for j0 in range(0, nts, REF_MAX_CHUNK):
+            j1 = min(j0 + REF_MAX_CHUNK, nts)
+            Fh = inputs.heat_rhs_host_slices(cfg, j0, j1)
+            t0 = time.perf_counter()
+            st.step(Fh)
+            tc += time.perf_counter() - t0
+        vc = cfg.nx * nts / tc
+        out["cpu_baseline"] = {"value": vc, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+                               "s": tc, "sample": (f"full solve ({nts} slices)" if nts == cfg.nt
+                                                   else f"causal prefix of {nts} of {cfg.nt} "
+                                                        "slices") +
+                               ", oracle heat_decoupled (numpy + all-core BLAS)"}
+        out["gpu_over_cpu"] = out["value"] / vc
+    return out
 
 
 def rksm_leg(stk, inputs, with_cpu=True, name="cfg1"):
@@ -384,6 +543,15 @@ def wave_leg(stk, inputs, with_cpu=True, cpu_iters=10):
            "pcg": {"iterations": rp.iterations, "final_relres": rp.final_relres, "tol": 1e-7,
                    "s": tp, "ms_per_iteration": 1e3 * tp / max(rp.iterations, 1),
                    "unknowns_per_s": N / tp}}
+    fl = WAVE_FLOP_PER_PCG_ITER(cfg.nh, cfg.nt + 1)
+    roof_ms = 1e3 * fl / (FP64_PEAK_TFLOPS * 1e12)
+    out["pcg"]["roofline"] = {"bound": "tensor", "flop_per_iteration": fl,
+                              "roof_ms_per_iteration": roof_ms, "peak": FP64_PEAK_TFLOPS,
+                              "peak_source": FP64_PEAK_SOURCE,
+                              "frac": roof_ms / out["pcg"]["ms_per_iteration"],
+                              "basis": "4 DMMA GEMMs of TwoTermPrecond::solve + the banded "
+                                       "WaveOperator per iteration (wall clock incl. the "
+                                       "per-chunk host convergence checks)"}
     if with_cpu:
         sys.path.insert(0, str(ROOT))
         from oracle import oracle as orc
@@ -478,11 +646,9 @@ def run_ours(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg.name, "unknowns_per_step": N, "n": cfg.n, "nt": cfg.nt,
-                   "transform": main,
-                   "parallelism": "replicas" if world > 1 else "single",
-                   "l2_flush": "inputs larger than L2 (F, U 8.6 GB each)",
-                   "relres_gpu_k1": res["relres_gpu_k1"]},
+        "config": workload_config(cfg),
+        "backend": {"transform": main, "parallelism": "replicas" if world > 1 else "single"},
+        "relres_gpu_k1": res["relres_gpu_k1"],
         "roofline": res["roofline"],
         "e2e": e2e,
         "gpu_launches": res["launches"],
@@ -506,6 +672,27 @@ def run_ours(args):
         line["rksm"] = rksm_leg(stk, inputs, with_cpu=(world == 1 and not args.no_cpu))
     if rank == 0 and not args.no_wave:
         line["wave"] = wave_leg(stk, inputs, with_cpu=(world == 1 and not args.no_cpu))
+    if rank == 0 and not args.no_configs:
+        cfgs = {}
+        for nm, slices in (("cfg1", None), ("cfg2", None), ("cfg5", 32)):
+            cfgs[nm] = heat_config_leg(stk, inputs, nm, stream,
+                                       with_cpu=(world == 1 and not args.no_cpu),
+                                       cpu_slices=slices)
+        cfgs[args.config] = {"workload": cfg.name, "unknowns": N, "ms": ms_max / args.steps,
+                             "value": value / world, "relres_gpu_k1": res["relres_gpu_k1"],
+                             "roofline": {"frac": res["roofline"].get("whole_solve_frac"),
+                                          "roof_ms": res["roofline"].get("whole_solve_roof_ms"),
+                                          "note": "the headline line (roofline.whole_solve_*)"}}
+        if "wave" in line:
+            wv = line["wave"]
+            cfgs["cfg4"] = {"workload": wv["workload"], "unknowns": wv["unknowns"],
+                            "pcg_ms_per_iteration": wv["pcg"]["ms_per_iteration"],
+                            "pcg_iterations_1e-7": wv["pcg"]["iterations"],
+                            "roofline": wv["pcg"]["roofline"],
+                            "refined_dd_relres": wv["refined_dd"]["final_relres_dd"],
+                            "refined_s": wv["refined_dd"]["s"],
+                            "cpu_baseline": wv.get("cpu_oracle_gmres")}
+        line["configs"] = dict(sorted(cfgs.items()))
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu_t = cpu_reference_run(cfg, args.ref_sample)
         cpu_v = cfg.nx * args.ref_sample / cpu_t
@@ -540,6 +727,8 @@ def main():
     ap.add_argument("--no-cn", action="store_true",
                     help="skip the single-thread Crank-Nicolson CPU reference timing")
     ap.add_argument("--no-alt", action="store_true", help="skip timing the other transform backend")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the per-config legs (cfg1, cfg2, cfg5 heat; cfg4 from the wave leg)")
     ap.add_argument("--transform", choices=["dst", "dense"], default="dst",
                     help="headline backend: P1 fast sine transforms (dst) or dense DMMA GEMMs")
     args = ap.parse_args()

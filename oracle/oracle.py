@@ -219,6 +219,45 @@ def heat_decoupled(eigs, d, c, F, nsteps=None):
     return Y.reshape(nt, -1)
 
 
+class DecoupledStream:
+    """heat_decoupled over consecutive time chunks: the same tensor-form
+    solve_projected_heat_with (stk/sylvester.hpp:117-142), with the per-mode recurrence
+    state y_{j0-1} carried from one chunk to the next, so a full n_t solve can be run (and
+    compared, or timed) a bounded number of time slices at a time.  step(F_chunk) takes the
+    next (k, n_x) C-order rows of F and returns the same rows of U."""
+
+    def __init__(self, eigs, d, c):
+        self.eigs = eigs
+        self.d, self.c = d, c
+        self.ns = [e[0].size for e in eigs]
+        lam_t = np.zeros(self.ns)
+        for ax, (lam, X) in enumerate(eigs):
+            shape = [1] * len(self.ns)
+            shape[ax] = self.ns[ax]
+            lam_t = lam_t + lam.reshape(shape)
+        self.lam_t = lam_t
+        self.j = 0
+        self.y = np.zeros(self.ns)
+
+    def step(self, F):
+        k = F.shape[0]
+        G = np.asarray(F, dtype=np.float64).reshape(k, *self.ns)
+        for ax, (lam, X) in enumerate(self.eigs):
+            G = np.moveaxis(np.tensordot(G, X, axes=([ax + 1], [0])), -1, ax + 1)
+        d, c, lam_t, y = self.d, self.c, self.lam_t, self.y
+        for i in range(k):
+            j = self.j + i
+            rhs = G[i]
+            if j > 0:
+                rhs = rhs - (d[1][j - 1] + lam_t * c[1][j - 1]) * y
+            y = rhs / (d[0][j] + lam_t * c[0][j])
+            G[i] = y
+        self.y, self.j = y, self.j + k
+        for ax, (lam, X) in enumerate(self.eigs):
+            G = np.moveaxis(np.tensordot(G, X, axes=([ax + 1], [1])), -1, ax + 1)
+        return G.reshape(k, -1)
+
+
 def crank_nicolson_splu(ms, as_, dt, F, nsteps=None):
     """CN (stk/cn_baseline.hpp:26-48) with scipy SuperLU in place of SimplicialLLT."""
     import scipy.sparse.linalg as spl
@@ -396,6 +435,73 @@ class WaveSystemNP:
         import scipy.sparse.linalg as spl
         B = (sp.kron(self.Qt, self.Mh) + sp.kron(self.E.T, self.Ah) + sp.kron(self.Mt.T, self.Qh))
         return spl.splu(B.tocsc()).solve(b)
+
+
+# ----------------------------------------------------------------- load projection --
+def gauss_legendre01(npoints: int):
+    """gauss_legendre(npoints, 0, 1) (stk/quadrature.hpp:17-64): the reference's own rule
+    (compiled from the reference by oracle/_ref, committed as tests/golden/wave_bands_ref.npz
+    by tests/golden/make_golden.py) when the fixture holds it, else numpy's Golub-Welsch rule
+    (agrees to a few ulps; tests/test_host_cpu.py pins both)."""
+    fx = HERE.parent / "tests" / "golden" / "wave_bands_ref.npz"
+    if fx.exists():
+        z = np.load(fx)
+        if f"gauss_{npoints}_x" in z:
+            return z[f"gauss_{npoints}_x"], z[f"gauss_{npoints}_w"]
+    x, w = np.polynomial.legendre.leggauss(npoints)
+    return (x + 1.0) / 2.0, w / 2.0
+
+
+def project_rhs_heat(theta, f, nt: int, T: float, a: float, b: float, nh: int,
+                     trapezoidal_time: bool = False, npoints: int = 6, rule=None):
+    """project_rhs_heat (stk/rhs_sep.hpp:111-151) for one separable term theta(t) f(x),
+    with the reference's summation order: H[l] = sum_i dt w_i theta(t_l + dt x_i) (or the
+    trapezoid dt/2 (theta(t_l) + theta(t_l+1))), and G[j] accumulates the rising-hat part of
+    element j and then the falling-hat part of element j+1.  Returns (G (nh,), H (nt,))."""
+    xs, ws = rule if rule is not None else gauss_legendre01(npoints)
+    dt = T / nt  # TimeGrid::dt (stk/discretize.hpp:13-24), node(l) = l * dt
+    t0 = np.arange(nt) * dt
+    t1 = np.arange(1, nt + 1) * dt
+    H = np.zeros(nt)
+    if trapezoidal_time:
+        H = dt / 2.0 * (theta(t0) + theta(t1))
+    else:
+        for xi, wi in zip(xs, ws):
+            H = H + dt * wi * theta(t0 + dt * xi)
+    h = (b - a) / (nh + 1)  # SpaceGrid1D::fem_h
+    x0 = a + np.arange(nh + 1) * h  # element e = [x0[e], x0[e] + h]
+    G = np.zeros(nh)
+    for xi, wi in zip(xs, ws):  # rising part of element e -> node e+1 -> G[e], e < nh
+        x = x0[:nh] + h * xi
+        G = G + (h * wi) * f(x) * ((x - x0[:nh]) / h)
+    for xi, wi in zip(xs, ws):  # falling part of element e -> node e -> G[e-1], e >= 1
+        x = x0[1:] + h * xi
+        G = G + (h * wi) * f(x) * (1.0 - (x - x0[1:]) / h)
+    return G, H
+
+
+def heat_ex1_theta(t):
+    """heat_ex1_rhs theta (stk/bench.hpp:300-306): 10 sin(t) t."""
+    return 10.0 * np.sin(t) * t
+
+
+def heat_ex1_f(x):
+    """heat_ex1_rhs f_x = f_y: cos(pi x / 2) (stk/bench.hpp:300-306)."""
+    return np.cos(np.pi / 2.0 * x)
+
+
+def heat_ex1_load(ndim: int, nh: int, nt: int, T: float = 10.0,
+                  trapezoidal_time: bool = False):
+    """assemble_heat's built-in heat-ex1 load (stk/bench.hpp:361-406) on Omega = (-1,1)^ndim:
+    F = L H^T with L = kron_cols(G_x, G_y) (index ix*ny + iy, :378-384), H the temporal
+    factor of the x-term (trapezoidal when requested; the y-term is projected with the
+    quadrature mode and contributes only its spatial factor, :375-385).  3D (no reference
+    function) extends the same product.  Returns (L (n_x,), H (nt,))."""
+    G, H = project_rhs_heat(heat_ex1_theta, heat_ex1_f, nt, T, -1.0, 1.0, nh, trapezoidal_time)
+    L = G
+    for _ in range(ndim - 1):
+        L = np.kron(L, G)
+    return L, H
 
 
 # ----------------------------------------------------------------------- generator --

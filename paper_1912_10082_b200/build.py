@@ -44,25 +44,24 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         return LIB
     objdir = PKG / "build"
     objdir.mkdir(exist_ok=True)
-    objs = []
-    log = []
-    for src in CUDA_SOURCES:
-        obj = objdir / (src + ".o")
-        extra = os.environ.get("STKG_NVCC_EXTRA", "").split()  # variant builds (tools/ab.sh)
-        cmd = [NVCC, *NVCC_FLAGS, *extra, "-c", str(CSRC / src), "-o", str(obj)]
-        r = subprocess.run(cmd, capture_output=True, text=True)
-        log.append(r.stdout + r.stderr)
-        if r.returncode != 0:
-            raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
-        objs.append(obj)
+    extra = os.environ.get("STKG_NVCC_EXTRA", "").split()  # variant builds (tools/ab.sh)
     cxx = shutil.which("g++") or "g++"
-    for src in HOST_SOURCES:
-        obj = objdir / (src + ".o")
-        cmd = [cxx, *CXX_FLAGS, "-c", str(CSRC / src), "-o", str(obj)]
+    jobs = [(src, [NVCC, *NVCC_FLAGS, *extra, "-c", str(CSRC / src), "-o",
+                   str(objdir / (src + ".o"))]) for src in CUDA_SOURCES]
+    jobs += [(src, [cxx, *CXX_FLAGS, "-c", str(CSRC / src), "-o", str(objdir / (src + ".o"))])
+             for src in HOST_SOURCES]
+
+    def run(job):
+        src, cmd = job
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
-            raise RuntimeError(f"g++ failed for {src}:\n{r.stderr}")
-        objs.append(obj)
+            raise RuntimeError(f"compile failed for {src}:\n{r.stderr}")
+        return r.stdout + r.stderr
+
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=len(jobs)) as pool:  # nvcc is single-threaded
+        log = list(pool.map(run, jobs))
+    objs = [objdir / (src + ".o") for src, _ in jobs]
     tmp = LIB.with_suffix(".so.tmp")
     cmd = [NVCC, *ARCH, "-shared", "-Xcompiler", "-fopenmp", "-o", str(tmp), *map(str, objs),
            "-lcudart_static", "-lrt", "-lpthread", "-ldl"]

@@ -80,7 +80,9 @@ struct DevBuf {
 // Deterministic two-level sum: a fixed grid of kReduceBlocks partial sums, each block a
 // fixed-order tree; the partials are then summed in index order by one block.  Same
 // inputs + same sizes => bit-identical result.
-constexpr int kReduceBlocks = 592;  // 4 x 148 SMs
+// The grid is a fixed constant (not derived from the SM count) so that results do not
+// depend on the device the reduction runs on.
+constexpr int kReduceBlocks = 592;
 constexpr int kReduceThreads = 256;
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -121,5 +123,17 @@ __host__ __device__ __forceinline__ double uniform_pm1(uint64_t seed, uint64_t s
 }
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Multiprocessor count of the current device (148 on B200), queried once per device.
+inline int num_sms() {
+  static thread_local int cached_dev = -1, cached_sms = 0;
+  int dev = 0;
+  STKG_CUDA_CHECK(cudaGetDevice(&dev));
+  if (dev != cached_dev) {
+    STKG_CUDA_CHECK(cudaDeviceGetAttribute(&cached_sms, cudaDevAttrMultiProcessorCount, dev));
+    cached_dev = dev;
+  }
+  return cached_sms;
+}
 
 }  // namespace stkg

@@ -104,7 +104,7 @@ void launch_dst_strided(const stkg_heat& h, int a, const double* src, double* ds
                                                                 C::kThreads, C::kSmem));
   const int64_t nvec = outer * inner;
   const int64_t tiles = ceil_div(nvec, C::kG);
-  const int64_t blocks = std::min<int64_t>(tiles, int64_t(148) * std::max(per_sm, 1));
+  const int64_t blocks = std::min<int64_t>(tiles, int64_t(num_sms()) * std::max(per_sm, 1));
   const double scale = std::sqrt(2.0 / static_cast<double>(h.n[a] + 1));
   dst_strided_kernel<L><<<static_cast<unsigned>(blocks), C::kThreads, C::kSmem, h.stream>>>(
       src, dst, h.n[a], inner, nvec, reinterpret_cast<const double2*>(h.twiddle[a].p), scale);
@@ -128,7 +128,7 @@ void launch_dst(const stkg_heat& h, int a, const double* src, double* dst, int64
                                                                 C::kThreads, C::kSmem));
   const int64_t nvec = outer * inner;
   const int64_t items = ceil_div(nvec, 2);
-  const int64_t blocks = std::min<int64_t>(items, int64_t(148) * std::max(per_sm, 1));
+  const int64_t blocks = std::min<int64_t>(items, int64_t(num_sms()) * std::max(per_sm, 1));
   const double scale = std::sqrt(2.0 / static_cast<double>(h.n[a] + 1));
   dst_axis_kernel<L><<<static_cast<unsigned>(blocks), C::kThreads, C::kSmem, h.stream>>>(
       src, dst, h.n[a], inner, nvec, reinterpret_cast<const double2*>(h.twiddle[a].p), scale);
@@ -201,7 +201,7 @@ void launch_dst_half_strided_tma(const stkg_heat& h, const double* src, double* 
         &b, dst_half_strided_tma_kernel<N>, C::kThreads, TC::kSmem));
     return std::max(b, 1);
   }();
-  const int64_t blocks = std::min<int64_t>(nvec / C::G, int64_t(148) * per_sm);
+  const int64_t blocks = std::min<int64_t>(nvec / C::G, int64_t(num_sms()) * per_sm);
   dst_half_strided_tma_kernel<N><<<static_cast<unsigned>(blocks), C::kThreads, TC::kSmem,
                                    h.stream>>>(map, dst, inner, nvec, tw2, scale);
 }
@@ -219,7 +219,7 @@ void launch_dst_half_strided2(const stkg_heat& h, const double* src, double* dst
         &b, dst_half_strided2_kernel<N, P, PF>, C::kThreads, C::kSmem));
     return std::max(b, 1);
   }();
-  const int64_t blocks = std::min<int64_t>(nvec / C::G, int64_t(148) * per_sm);
+  const int64_t blocks = std::min<int64_t>(nvec / C::G, int64_t(num_sms()) * per_sm);
   dst_half_strided2_kernel<N, P, PF><<<static_cast<unsigned>(blocks), C::kThreads, C::kSmem,
                                        h.stream>>>(src, dst, inner, nvec, tw2, scale);
 }
@@ -245,7 +245,7 @@ void launch_dst_half(const stkg_heat& h, int a, const double* src, double* dst, 
                                                                     C::kThreads, C::kSmem));
       return std::max(b, 1);
     }();
-    const int64_t blocks = std::min<int64_t>(ceil_div(nvec, 2 * C::F), int64_t(148) * per_sm);
+    const int64_t blocks = std::min<int64_t>(ceil_div(nvec, 2 * C::F), int64_t(num_sms()) * per_sm);
     const int64_t lds = ld_src > 0 ? ld_src : N - 1, ldd = ld_dst > 0 ? ld_dst : N - 1;
     dst_half_kernel<N><<<static_cast<unsigned>(blocks), C::kThreads, C::kSmem, h.stream>>>(
         src, dst, nvec, tw2, scale, lds, ldd);
@@ -282,7 +282,7 @@ void launch_dst_half(const stkg_heat& h, int a, const double* src, double* dst, 
           &b, dst_half_strided_kernel<N>, C::kThreads, C::kSmem));
       return std::max(b, 1);
     }();
-    const int64_t blocks = std::min<int64_t>(ceil_div(nvec, C::G), int64_t(148) * per_sm);
+    const int64_t blocks = std::min<int64_t>(ceil_div(nvec, C::G), int64_t(num_sms()) * per_sm);
     dst_half_strided_kernel<N><<<static_cast<unsigned>(blocks), C::kThreads, C::kSmem, h.stream>>>(
         src, dst, inner, nvec, tw2, scale);
   }
@@ -685,7 +685,7 @@ int stkg_fill_uniform(double* dst, int64_t count, uint64_t seed, uint64_t stream
   return guarded([&] {
     STKG_REQUIRE(count >= 0 && (dst || count == 0), STKG_ARGUMENT, "fill_uniform: bad args");
     if (count == 0) return;
-    fill_uniform_kernel<<<148 * 8, 256, 0, static_cast<cudaStream_t>(cuda_stream)>>>(
+    fill_uniform_kernel<<<num_sms() * 8, 256, 0, static_cast<cudaStream_t>(cuda_stream)>>>(
         dst, count, seed, stream, index_offset);
     STKG_CUDA_CHECK(cudaGetLastError());
   });

@@ -44,7 +44,8 @@ int run(F&& body) {
 // gauss_legendre (stk/quadrature.hpp:17-64): Newton iteration on the three-term Legendre
 // recurrence from the Chebyshev-like initial guess, symmetric fill, affine map to (a,b).
 // The operation sequence is kept identical so the spline Gram bands are bit-identical to
-// the reference's (checked against oracle/_ref in tests/test_wave_assembly.py).
+// the reference's (checked against oracle/_ref by
+// tests/test_host_cpu.py::test_wave_bands_bit_identical_to_reference).
 struct Rule {
   std::vector<double> x, w;
 };

@@ -11,7 +11,7 @@
 namespace stkg {
 namespace {
 
-constexpr unsigned kEwBlocks = 148 * 8;
+inline unsigned ew_blocks() { return static_cast<unsigned>(num_sms()) * 8; }
 
 __global__ void __launch_bounds__(kReduceThreads) dot_partials_kernel(
     const double* __restrict__ x, const double* __restrict__ y, int64_t n,
@@ -226,14 +226,14 @@ void gmres_run(Krylov& k, const DevOp& apply, const DevOp* precond, const double
       STKG_CUDA_CHECK(cudaMemcpyAsync(r, b, sizeof(double) * N, cudaMemcpyDeviceToDevice, s));
     } else {
       apply(x, r);
-      sub_from_kernel<<<kEwBlocks, 256, 0, s>>>(b, r, N);
+      sub_from_kernel<<<ew_blocks(), 256, 0, s>>>(b, r, N);
     }
     const double beta = knorm(k, r);
     if (beta <= cfg.tol * norm_b) {
       converged = true;
       break;
     }
-    scale_copy_kernel<<<kEwBlocks, 256, 0, s>>>(r, 1.0 / beta, vcol(0), N);
+    scale_copy_kernel<<<ew_blocks(), 256, 0, s>>>(r, 1.0 / beta, vcol(0), N);
     std::vector<std::vector<double>> hcols;
     std::vector<double> g(cycle + 1, 0.0), cs, sn;
     g[0] = beta;
@@ -308,7 +308,7 @@ void gmres_run(Krylov& k, const DevOp& apply, const DevOp* precond, const double
         ++total;
         break;
       }
-      scale_copy_kernel<<<kEwBlocks, 256, 0, s>>>(k.w.p, 1.0 / hlast, vcol(j + 1), N);
+      scale_copy_kernel<<<ew_blocks(), 256, 0, s>>>(k.w.p, 1.0 / hlast, vcol(j + 1), N);
       ++nbasis;
     }
     if (kdim > 0) {
@@ -327,16 +327,16 @@ void gmres_run(Krylov& k, const DevOp& apply, const DevOp* precond, const double
                                                                    k.xk.p, nullptr);
       if (precond) {
         (*precond)(k.xk.p, k.z.p);
-        add_kernel<<<kEwBlocks, 256, 0, s>>>(k.z.p, x, N);
+        add_kernel<<<ew_blocks(), 256, 0, s>>>(k.z.p, x, N);
       } else {
-        add_kernel<<<kEwBlocks, 256, 0, s>>>(k.xk.p, x, N);
+        add_kernel<<<ew_blocks(), 256, 0, s>>>(k.xk.p, x, N);
       }
       STKG_CUDA_CHECK(cudaStreamSynchronize(s));  // y dies here
     }
     if (done || total >= cfg.maxit) break;
   }
   apply(x, k.r.p);  // final true residual (:159)
-  sub_from_kernel<<<kEwBlocks, 256, 0, s>>>(b, k.r.p, N);
+  sub_from_kernel<<<ew_blocks(), 256, 0, s>>>(b, k.r.p, N);
   const double fr = knorm(k, k.r.p) / norm_b;
   if (fr <= cfg.tol) converged = true;
   if (rep) {
@@ -501,6 +501,10 @@ void pcg_run(Krylov& k, const DevOp& apply, const DevOp& precond, const double* 
   pcg_init_kernel<<<1, kReduceThreads, 0, s>>>(k.partials.p, st, norm_b, tol, maxit);
   STKG_CUDA_CHECK(cudaGetLastError());
   k.skip = &st->done;  // library operators turn into no-ops once the device test fires
+  struct SkipReset {  // cleared on every exit path, including a throw inside the loop
+    const int*& ref;
+    ~SkipReset() { ref = nullptr; }
+  } skip_reset{k.skip};
   PcgState hs{};
   k.pin(sizeof(PcgState) / 8 + 1);
   int enqueued = 0;
@@ -514,7 +518,7 @@ void pcg_run(Krylov& k, const DevOp& apply, const DevOp& precond, const double* 
       precond(r, z);
       pcg_dot_kernel<<<kReduceBlocks, kReduceThreads, 0, s>>>(st, r, z, N, k.partials.p);
       pcg_beta_kernel<<<1, kReduceThreads, 0, s>>>(k.partials.p, st);
-      pcg_xpby_kernel<<<kEwBlocks, 256, 0, s>>>(st, z, p, N);
+      pcg_xpby_kernel<<<ew_blocks(), 256, 0, s>>>(st, z, p, N);
     }
     STKG_CUDA_CHECK(cudaGetLastError());
     STKG_CUDA_CHECK(cudaMemcpyAsync(k.pinned, st, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
@@ -522,7 +526,7 @@ void pcg_run(Krylov& k, const DevOp& apply, const DevOp& precond, const double* 
     std::memcpy(&hs, k.pinned, sizeof(PcgState));
     if (hs.done || enqueued >= maxit) break;
   }
-  k.skip = nullptr;
+  k.skip = nullptr;  // the true-residual apply below must run
   if (hs.error == 1)
     throw Error(STKG_NUMERIC, "pcg: non-positive curvature at iteration " + std::to_string(hs.iters + 1));
   if (hs.error == 2)
@@ -534,7 +538,7 @@ void pcg_run(Krylov& k, const DevOp& apply, const DevOp& precond, const double* 
   for (int i = 0; i < it; ++i) report_history(rep, h[i]);
   const bool converged = it > 0 && h[it - 1] <= tol;
   apply(x, k.r.p);  // true final residual
-  sub_from_kernel<<<kEwBlocks, 256, 0, s>>>(b, k.r.p, N);
+  sub_from_kernel<<<ew_blocks(), 256, 0, s>>>(b, k.r.p, N);
   const double fr = knorm(k, k.r.p) / norm_b;
   if (rep) {
     rep->iterations = it;

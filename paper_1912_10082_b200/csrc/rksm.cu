@@ -36,7 +36,7 @@ namespace {
 
 constexpr int kTsCols = 4;   // V columns per block in the tall-skinny Gram
 constexpr int kTsRhs = 8;    // W columns per pass
-constexpr unsigned kEw = 148 * 8;
+inline unsigned ew_blocks() { return static_cast<unsigned>(num_sms()) * 8; }
 
 // Tall-skinny Gram V(:, c0 + 0..k)^T W(:, 0..b): CTA (g, cb) covers rows of slab g (of
 // gridDim.x slabs) and the 32 V columns of block cb, each warp 4 columns; lanes stride the
@@ -293,7 +293,7 @@ class Rksm {
     STKG_REQUIRE(smem <= 200 * 1024, STKG_ARGUMENT, "rksm: Krylov basis too large");
     for (int64_t j0 = 0; j0 < b; j0 += kTsRhs) {
       const int bb = static_cast<int>(std::min<int64_t>(kTsRhs, b - j0));
-      ts_update_kernel<kTsRhs><<<kEw, 256, smem, s_>>>(W + j0 * n_, n_, bb, V, static_cast<int>(k),
+      ts_update_kernel<kTsRhs><<<ew_blocks(), 256, smem, s_>>>(W + j0 * n_, n_, bb, V, static_cast<int>(k),
                                                        Hd + j0 * k);
       STKG_CUDA_CHECK(cudaGetLastError());
     }
@@ -369,7 +369,7 @@ class Rksm {
       axis_pass(h_, a, true, src, dstp, b);
       src = dstp;
     }
-    scale_modes_kernel<<<kEw, 256, 0, s_>>>(const_cast<double*>(src), n_, static_cast<int>(b),
+    scale_modes_kernel<<<ew_blocks(), 256, 0, s_>>>(const_cast<double*>(src), n_, static_cast<int>(b),
                                             mode_lambda(h_), sigma);
     STKG_CUDA_CHECK(cudaGetLastError());
     for (int a = 0; a < h_.ndim; ++a) {  // inverse transforms
@@ -445,7 +445,7 @@ class Rksm {
   }
 
   void scale(double* x, double alpha) {
-    scale_kernel<<<kEw, 256, 0, s_>>>(x, n_, alpha);
+    scale_kernel<<<ew_blocks(), 256, 0, s_>>>(x, n_, alpha);
     STKG_CUDA_CHECK(cudaGetLastError());
   }
 
@@ -889,6 +889,11 @@ extern "C" int stkg_heat_rksm(stkg_heat* plan, int64_t rank, const double* L, co
     stkg_rksm_options o = opts ? *opts : stkg_rksm_options{1e-8, 100, 0, 1e-10};
     STKG_REQUIRE(o.fixed_iters >= 0, STKG_ARGUMENT, "rksm_solve: fixed_iters must be >= 1");
     STKG_REQUIRE(o.maxit >= 1, STKG_ARGUMENT, "rksm_solve: maxit must be >= 1");
+    // lowrank_truncate's argument check (stk/la_core.hpp:135) on the tolerance the final
+    // truncation uses (stk/rksm.hpp:226-227), made before any work is done
+    const double final_tol = o.fixed_iters > 0 ? o.trunc_tol : o.tol;
+    STKG_REQUIRE(final_tol > 0.0 && final_tol < 1.0, STKG_ARGUMENT,
+                 "lowrank_truncate: tol must be in (0,1)");
     Rksm solver(*plan, o);
     solver.run(rank, L, R, U_left, U_right, cap, rank_out, report);
   });

@@ -414,7 +414,7 @@ int stkg_wave_solve_refined(stkg_wave* wv, const double* b, double* x_hi, double
       stkg_report inner{};
       pcg_run(w.krylov, apply, precond, r.p, d.p, inner_tol, inner_maxit, &inner);
       total += inner.iterations;
-      dd_accumulate_kernel<<<148 * 8, 256, 0, w.stream>>>(x_hi, x_lo, d.p, w.N);
+      dd_accumulate_kernel<<<num_sms() * 8, 256, 0, w.stream>>>(x_hi, x_lo, d.p, w.N);
       STKG_CUDA_CHECK(cudaGetLastError());
     }
     STKG_CUDA_CHECK(cudaStreamSynchronize(w.stream));

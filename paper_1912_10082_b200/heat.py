@@ -14,6 +14,7 @@ go through ``stkg_heat_solve_host`` (H2D / solve / D2H pipelined over time chunk
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 from dataclasses import dataclass
 from typing import Sequence
@@ -38,6 +39,30 @@ def _dev_ptr(t) -> int:
     if not t.is_contiguous():
         raise ArgumentError("expected a contiguous tensor")
     return t.data_ptr()
+
+
+@contextlib.contextmanager
+def on_plan_stream(handle):
+    """Order a plan call with the caller's current torch stream: the plan's stream waits
+    for work already queued on the caller's stream (inputs written there), and the caller's
+    stream waits for the plan's work (outputs used there).  A no-op when they are the same
+    stream.  Plans bind their stream at creation; this keeps later calls made under another
+    torch stream correct."""
+    import torch
+    if not torch.cuda.is_available():
+        yield
+        return
+    cur = torch.cuda.current_stream()
+    ph = int(handle.value or 0) if isinstance(handle, C.c_void_p) else int(handle or 0)
+    if cur.cuda_stream == ph:
+        yield
+        return
+    plan_stream = torch.cuda.ExternalStream(ph) if ph else torch.cuda.default_stream()
+    plan_stream.wait_stream(cur)
+    try:
+        yield
+    finally:
+        cur.wait_stream(plan_stream)
 
 
 def _stream_handle(stream):
@@ -167,7 +192,8 @@ class HeatPlan:
         self._check_size(F)
         U = torch.empty_like(F) if out is None else out
         self._check_size(U)
-        check(lib.stkg_heat_solve(self._h, C.c_void_p(_dev_ptr(F)), C.c_void_p(_dev_ptr(U))))
+        with on_plan_stream(self._stream):
+            check(lib.stkg_heat_solve(self._h, C.c_void_p(_dev_ptr(F)), C.c_void_p(_dev_ptr(U))))
         return U
 
     def solve_factored(self, L, R, out=None):
@@ -179,8 +205,9 @@ class HeatPlan:
             raise ArgumentError("solve_factored: factor shape mismatch")
         U = torch.empty((self.nt, self.nx), dtype=torch.float64, device=L.device) if out is None else out
         self._check_size(U)
-        check(lib.stkg_heat_solve_factored(self._h, rank, C.c_void_p(_dev_ptr(L)),
-                                           C.c_void_p(_dev_ptr(R)), C.c_void_p(_dev_ptr(U))))
+        with on_plan_stream(self._stream):
+            check(lib.stkg_heat_solve_factored(self._h, rank, C.c_void_p(_dev_ptr(L)),
+                                               C.c_void_p(_dev_ptr(R)), C.c_void_p(_dev_ptr(U))))
         return U
 
     def rksm(self, L, R, tol: float = 1e-8, maxit: int = 100, fixed_iters: int = 0,
@@ -203,9 +230,11 @@ class HeatPlan:
         rep.rel_res_history = _np_ptr(hist)
         rep.history_capacity = hist.size
         rk = C.c_int64()
-        check(lib.stkg_heat_rksm(self._h, rank, C.c_void_p(_dev_ptr(L)), C.c_void_p(_dev_ptr(R)),
-                                 C.byref(opts), C.c_void_p(_dev_ptr(UL)), C.c_void_p(_dev_ptr(UR)),
-                                 cap, C.byref(rk), C.byref(rep)))
+        with on_plan_stream(self._stream):
+            check(lib.stkg_heat_rksm(self._h, rank, C.c_void_p(_dev_ptr(L)),
+                                     C.c_void_p(_dev_ptr(R)), C.byref(opts),
+                                     C.c_void_p(_dev_ptr(UL)), C.c_void_p(_dev_ptr(UR)), cap,
+                                     C.byref(rk), C.byref(rep)))
         out = _report(rep, hist)
         out.rank = int(rk.value)
         return UL[: rk.value], UR[: rk.value], out
@@ -215,7 +244,9 @@ class HeatPlan:
         import torch
         self._check_size(U)
         Y = torch.empty_like(U) if out is None else out
-        check(lib.stkg_heat_apply(self._h, C.c_void_p(_dev_ptr(U)), C.c_void_p(_dev_ptr(Y))))
+        self._check_size(Y)
+        with on_plan_stream(self._stream):
+            check(lib.stkg_heat_apply(self._h, C.c_void_p(_dev_ptr(U)), C.c_void_p(_dev_ptr(Y))))
         return Y
 
     def residual(self, U, F):
@@ -223,8 +254,9 @@ class HeatPlan:
         self._check_size(U)
         self._check_size(F)
         rel, fn = C.c_double(), C.c_double()
-        check(lib.stkg_heat_residual(self._h, C.c_void_p(_dev_ptr(U)), C.c_void_p(_dev_ptr(F)),
-                                     C.byref(rel), C.byref(fn)))
+        with on_plan_stream(self._stream):
+            check(lib.stkg_heat_residual(self._h, C.c_void_p(_dev_ptr(U)),
+                                         C.c_void_p(_dev_ptr(F)), C.byref(rel), C.byref(fn)))
         return rel.value, fn.value
 
     # -- profiling ------------------------------------------------------------------
@@ -244,8 +276,10 @@ class HeatPlan:
         F = np.ascontiguousarray(F, dtype=np.float64)
         self._check_size(F)
         U = np.empty_like(F) if out is None else out
-        if not (U.flags.c_contiguous and U.dtype == np.float64):
-            raise ArgumentError("solve_host: out must be a contiguous float64 array")
+        if not (isinstance(U, np.ndarray) and U.flags.c_contiguous and U.dtype == np.float64
+                and U.flags.writeable):
+            raise ArgumentError("solve_host: out must be a writable contiguous float64 array")
+        self._check_size(U)  # the D2H copy writes n_x * n_t doubles
         check(lib.stkg_heat_solve_host(self._h, C.c_void_p(F.ctypes.data),
                                        C.c_void_p(U.ctypes.data)))
         return U

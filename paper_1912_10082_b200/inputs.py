@@ -99,6 +99,16 @@ def heat_rhs_host(cfg: HeatConfig, seed: int = 0, nsteps: int | None = None) -> 
     return np.ascontiguousarray(right[:nt] @ left.T)
 
 
+def heat_rhs_host_slices(cfg: HeatConfig, j0: int, j1: int, seed: int = 0) -> np.ndarray:
+    """Time slices j0..j1-1 of F (rows of the (n_t, n_x) C-order array), generated directly
+    (the counter generator is random-access), for streaming a full-size solve on the host."""
+    if cfg.rank == 0:
+        return uniform_pm1(cfg.nx * (j1 - j0), seed, cfg.cid * 16,
+                           offset=cfg.nx * j0).reshape(j1 - j0, cfg.nx)
+    left, right = heat_factors(cfg, seed)
+    return np.ascontiguousarray(right[j0:j1] @ left.T)
+
+
 def wave_rhs_host(cfg: WaveConfig, seed: int = 0) -> np.ndarray:
     ntb = cfg.nt + 1
     return normal(cfg.nh * ntb, seed, cfg.cid * 16).reshape(ntb, cfg.nh)

@@ -22,7 +22,7 @@ import numpy as np
 from ._lib import VEC_OP, GmresCfg, Report, WaveDesc, lib
 from .assembly import EigPair, WaveSpaceMatrices, WaveTimeMatrices, sym_gen_eig
 from .errors import ArgumentError, check
-from .heat import _dev_ptr, _np_ptr, _stream_handle
+from .heat import _dev_ptr, _np_ptr, _stream_handle, on_plan_stream
 
 
 @dataclass
@@ -88,7 +88,8 @@ class WavePlan:
             desc.lambdas = arr(self.space_eig.lambdas)
             desc.thetas = arr(self.time_eig.lambdas)
         h = C.c_void_p()
-        check(lib.stkg_wave_create(C.byref(h), C.byref(desc), _stream_handle(stream)))
+        self._stream = _stream_handle(stream)
+        check(lib.stkg_wave_create(C.byref(h), C.byref(desc), self._stream))
         self._h = h
 
     def close(self):
@@ -114,14 +115,19 @@ class WavePlan:
         import torch
         self._chk(x)
         y = torch.empty_like(x) if out is None else out
-        check(lib.stkg_wave_apply(self._h, C.c_void_p(_dev_ptr(x)), C.c_void_p(_dev_ptr(y))))
+        self._chk(y)
+        with on_plan_stream(self._stream):
+            check(lib.stkg_wave_apply(self._h, C.c_void_p(_dev_ptr(x)), C.c_void_p(_dev_ptr(y))))
         return y
 
     def two_term_solve(self, v, out=None):
         import torch
         self._chk(v)
         w = torch.empty_like(v) if out is None else out
-        check(lib.stkg_two_term_solve(self._h, C.c_void_p(_dev_ptr(v)), C.c_void_p(_dev_ptr(w))))
+        self._chk(w)
+        with on_plan_stream(self._stream):
+            check(lib.stkg_two_term_solve(self._h, C.c_void_p(_dev_ptr(v)),
+                                          C.c_void_p(_dev_ptr(w))))
         return w
 
     def gmres(self, b, cfg: GmresConfig | None = None, precond: bool = True, x=None):
@@ -130,25 +136,29 @@ class WavePlan:
         cfg.validate()
         self._chk(b)
         x = torch.empty_like(b) if x is None else x
+        self._chk(x)
         c = GmresCfg(cfg.tol, cfg.maxit, cfg.restart, 1 if precond else 0)
         hist = np.zeros(cfg.maxit + 1)
         rep = Report()
         rep.rel_res_history = _np_ptr(hist)
         rep.history_capacity = hist.size
-        check(lib.stkg_gmres(self._h, C.c_void_p(_dev_ptr(b)), C.c_void_p(_dev_ptr(x)),
-                             C.byref(c), C.byref(rep)))
+        with on_plan_stream(self._stream):
+            check(lib.stkg_gmres(self._h, C.c_void_p(_dev_ptr(b)), C.c_void_p(_dev_ptr(x)),
+                                 C.byref(c), C.byref(rep)))
         return x, _report(rep, hist)
 
     def pcg(self, b, tol: float = 1e-8, maxit: int = 1000, x=None):
         import torch
         self._chk(b)
         x = torch.empty_like(b) if x is None else x
+        self._chk(x)
         hist = np.zeros(maxit + 1)
         rep = Report()
         rep.rel_res_history = _np_ptr(hist)
         rep.history_capacity = hist.size
-        check(lib.stkg_pcg(self._h, C.c_void_p(_dev_ptr(b)), C.c_void_p(_dev_ptr(x)), tol, maxit,
-                           C.byref(rep)))
+        with on_plan_stream(self._stream):
+            check(lib.stkg_pcg(self._h, C.c_void_p(_dev_ptr(b)), C.c_void_p(_dev_ptr(x)), tol,
+                               maxit, C.byref(rep)))
         return x, _report(rep, hist)
 
     def residual_dd(self, b, x_hi, x_lo=None, out=None) -> float:
@@ -156,11 +166,15 @@ class WavePlan:
         (stkg_wave_residual_dd); the FP64-rounded residual vector lands in out if given."""
         self._chk(b)
         self._chk(x_hi)
+        for t in (x_lo, out):
+            if t is not None:
+                self._chk(t)
         rel = C.c_double()
-        check(lib.stkg_wave_residual_dd(
-            self._h, C.c_void_p(_dev_ptr(b)), C.c_void_p(_dev_ptr(x_hi)),
-            C.c_void_p(_dev_ptr(x_lo) if x_lo is not None else None),
-            C.c_void_p(_dev_ptr(out) if out is not None else None), C.byref(rel)))
+        with on_plan_stream(self._stream):
+            check(lib.stkg_wave_residual_dd(
+                self._h, C.c_void_p(_dev_ptr(b)), C.c_void_p(_dev_ptr(x_hi)),
+                C.c_void_p(_dev_ptr(x_lo) if x_lo is not None else None),
+                C.c_void_p(_dev_ptr(out) if out is not None else None), C.byref(rel)))
         return rel.value
 
     def solve_refined(self, b, tol: float = 1e-10, max_refine: int = 6,
@@ -176,9 +190,11 @@ class WavePlan:
         rep = Report()
         rep.rel_res_history = _np_ptr(hist)
         rep.history_capacity = hist.size
-        check(lib.stkg_wave_solve_refined(self._h, C.c_void_p(_dev_ptr(b)), C.c_void_p(_dev_ptr(xh)),
-                                          C.c_void_p(_dev_ptr(xl)), tol, max_refine, inner_tol,
-                                          inner_maxit, C.byref(rep)))
+        with on_plan_stream(self._stream):
+            check(lib.stkg_wave_solve_refined(self._h, C.c_void_p(_dev_ptr(b)),
+                                              C.c_void_p(_dev_ptr(xh)), C.c_void_p(_dev_ptr(xl)),
+                                              tol, max_refine, inner_tol, inner_maxit,
+                                              C.byref(rep)))
         return xh, xl, _report(rep, hist)
 
 

@@ -73,7 +73,7 @@ def main():
         out[f"time_{nt}_{deg}"] = tb
     lib = O.ref_lib()
     import ctypes as C
-    for npts in (3, 4):
+    for npts in (3, 4, 6):  # 6: project_rhs_heat's default rule (stk/rhs_sep.hpp:113)
         x, w = np.zeros(npts), np.zeros(npts)
         lib.ref_gauss_legendre(npts, 0.0, 1.0, x.ctypes.data_as(C.POINTER(C.c_double)),
                                w.ctypes.data_as(C.POINTER(C.c_double)))

@@ -10,7 +10,7 @@ BIN = ROOT / "tests" / "cpp" / "test_stk_gpu"
 
 
 def build_cpp_test():
-    import paper_1912_10082_b200  # noqa: F401  (ensures the .so is built)
+    import paper_1912_10082_b200._lib  # noqa: F401  (ensures the .so is built)
     pkg = ROOT / "paper_1912_10082_b200"
     cmd = ["g++", "-std=c++17", "-O1", "-Wall", "-Wextra", f"-I{ROOT / 'include'}",
            str(ROOT / "tests" / "cpp" / "test_stk_gpu.cpp"), "-o", str(BIN), f"-L{pkg}",

@@ -257,3 +257,51 @@ def test_oracle_adaptive_shift_spec_example(orc):
     assert cands[int(np.argmax(vals))] == -4.0
     s1 = orc.adaptive_next_shift([-1.0], [2.0], 1.0, 10.0)
     assert s1 == orc.adaptive_next_shift([-1.0], [2.0], 1.0, 10.0) and s1 < 0
+
+
+# ------------------------------------------- heat-ex1 (the reference's desk problem) --
+def test_oracle_gauss_rule_and_load_projection(orc, ref_bands):
+    """The oracle's project_rhs_heat (stk/rhs_sep.hpp:111-151) uses the reference's own
+    6-point Gauss-Legendre rule (fixture from oracle/_ref); numpy's rule agrees to ulps.
+    Known answers: a constant load projects onto h per interior hat and dt per interval."""
+    x6, w6 = orc.gauss_legendre01(6)
+    np.testing.assert_array_equal(x6, ref_bands["gauss_6_x"])
+    xn, wn = np.polynomial.legendre.leggauss(6)
+    assert np.abs((xn + 1) / 2 - x6).max() < 1e-15 and np.abs(wn / 2 - w6).max() < 1e-15
+    G, H = orc.project_rhs_heat(lambda t: np.ones_like(t), lambda x: np.ones_like(x),
+                                8, 2.0, -1.0, 1.0, 9)
+    np.testing.assert_allclose(G, 0.2, rtol=1e-14)
+    np.testing.assert_allclose(H, 0.25, rtol=1e-14)
+    Gt, Ht = orc.project_rhs_heat(orc.heat_ex1_theta, orc.heat_ex1_f, 5, 10.0, -1.0, 1.0, 9,
+                                  trapezoidal_time=True)
+    t = np.arange(6) * 2.0
+    np.testing.assert_allclose(Ht, 1.0 * (orc.heat_ex1_theta(t[:-1]) + orc.heat_ex1_theta(t[1:])))
+    # cos(pi x/2) on (-1,1) is the first Dirichlet eigenfunction: its P1 load vector is the
+    # first discrete eigenvector (to quadrature accuracy)
+    xi = -1.0 + 0.2 * np.arange(1, 10)
+    v = np.cos(np.pi / 2 * xi)
+    assert np.linalg.norm(Gt / np.linalg.norm(Gt) - v / np.linalg.norm(v)) < 1e-6
+
+
+@pytest.mark.parametrize("ndim,nh", [(1, 199), (2, 60)])
+def test_oracle_rksm_heat_ex1_acceptance(orc, ndim, nh):
+    """SPEC.md:612-615 on the reference's own heat-ex1 problem (stk/bench.hpp:300-306,
+    361-406: Omega=(-1,1)^d, T=10, load 10 sin(t) t prod cos(pi x_i/2)), N_t in
+    {100, 300, 500}: iterations <= 30 with spread <= 3, rank <= 20, mu_mem <= 40 (2D desk
+    problem); in 1D (N_h=199, trapezoidal-time RHS) the RKSM solution equals the CN
+    trajectory column by column to <= 1e-6 (criterion 2)."""
+    its_all = []
+    for nt in (100, 300, 500):
+        L, H = orc.heat_ex1_load(ndim, nh, nt, T=10.0, trapezoidal_time=(ndim == 1))
+        m, a = orc.fem1d_matrices(-1.0, 1.0, nh)
+        d, c = orc.heat_time_matrices(nt, 10.0)
+        left, right, its, hist = orc.rksm_solve([m] * ndim, [a] * ndim, d, c, L[:, None],
+                                                H[:, None], tol=1e-8, maxit=60)
+        assert hist[-1] <= 1e-8 and its <= 30 and left.shape[1] <= 20
+        its_all.append(its)
+        if ndim == 1:
+            U = (left @ right.T).T  # (nt, nx)
+            Ucn = orc.crank_nicolson_splu([m], [a], 10.0 / nt, np.outer(H, L))
+            col = np.linalg.norm(U - Ucn, axis=1) / np.linalg.norm(Ucn, axis=1)
+            assert col.max() <= 1e-6, col.max()
+    assert max(its_all) - min(its_all) <= 3
