@@ -85,6 +85,14 @@ def fft_flop_per_unknown(n: int, half: bool) -> float:
     return 5.0 * L * np.log2(L) / 2.0 / n
 
 
+def half_kernels(cfg) -> bool:
+    """Whether the plan runs the half-length DST kernels (heat.cu::dst_pass: 2D/3D plans
+    with N = n + 1 a power of two in [16, 1024])."""
+    N = cfg.n + 1
+    return (cfg.ndim >= 2 and 16 <= N <= 1024 and N & (N - 1) == 0
+            and os.environ.get("STKG_DST_HALF", "1") != "0")
+
+
 def workload_config(cfg):
     """The `config` object both arms print for a heat workload (identical keys and values)."""
     return {"workload": cfg.name, "unknowns_per_solve": cfg.unknowns, "ndim": cfg.ndim,
@@ -350,8 +358,7 @@ def _timed_path(stk, inputs, cfg, transform, args, stream, barrier, F, U, with_c
         bytes_launch = 16.0 * N  # read + write each unknown once per axis pass
         achieved = bytes_launch / (t_ms / t_n / 1e3) / 1e9
         # which sine-transform kernels the plan runs (heat.cu::dst_pass)
-        half = (cfg.ndim >= 2 and cfg.n + 1 in (512, 1024)
-                and os.environ.get("STKG_DST_HALF", "1") != "0")
+        half = half_kernels(cfg)
         fft_flops = fft_flop_per_unknown(cfg.n, half)  # per element and axis pass
         kname = ("dst_half_kernel / dst_half_strided2_kernel (FP64 half-length DST-I: "
                  "N-point Stockham FFT per vector pair)") if half else \
@@ -414,7 +421,7 @@ def heat_config_leg(stk, inputs, name, stream, steps=10, warmup=3, with_cpu=True
         out = {"workload": cfg.name, "unknowns": N, "ms": ms, "value": N / (ms / 1e3),
                "relres_gpu_k1": relres,
                "launches_per_solve": (prof["transform"][1] + prof["scan"][1]) / steps}
-        half = cfg.ndim >= 2 and cfg.n + 1 in (512, 1024)
+        half = half_kernels(cfg)
         fl = (2 * cfg.ndim * fft_flop_per_unknown(cfg.n, half) + 3.0) * N
         t_roof = max(16.0 * N / (HBM_GBS * 1e9), fl / (FP64_PEAK_TFLOPS * 1e12))
         out["roofline"] = {"bound": "hbm" if 16.0 * N / HBM_GBS / 1e9 >= fl / FP64_PEAK_TFLOPS
