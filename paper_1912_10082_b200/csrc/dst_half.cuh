@@ -670,12 +670,13 @@ struct HalfStrided2Cfg {
                                     : (P * kRegion > kTile ? P * kRegion : kTile);
   static constexpr size_t kSmem = size_t(kSmemD2) * sizeof(double2);
   static_assert(T <= 32 || T % 32 == 0, "FFTs are lane segments or whole warps");
-  static_assert(P == 2 || P == 4 || P % 8 == 0, "tile rows of 32, 64 or 128k bytes");
+  static_assert(P == 1 || P == 2 || P == 4 || P % 8 == 0, "tile rows of 16, 32, 64 or 128k bytes");
   static_assert(N - 1 + (N - 2) / 16 < kRegion && N <= kRegion, "OutPair staging fits the region");
   // 16-byte chunk of pair c in tile row r, XOR-swizzled so that 8 consecutive rows of one
   // pair fall in 8 distinct 16-byte bank groups (SWIZZLE_32B/64B/128B-like)
   __device__ __forceinline__ static int chunk(int r, int c) {
-    if constexpr (P == 2) return c ^ ((r >> 2) & 1);
+    if constexpr (P == 1) return c;  // 16-byte rows: consecutive rows are distinct groups
+    else if constexpr (P == 2) return c ^ ((r >> 2) & 1);
     else if constexpr (P == 4) return c ^ ((r >> 1) & 3);
     else return c ^ (r & 7);
   }

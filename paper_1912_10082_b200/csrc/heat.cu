@@ -26,6 +26,7 @@
 #include "common.cuh"
 #include "dst.cuh"
 #include "dst_half.cuh"
+#include "heat_fused.cuh"  // K2b + K3: time-marching fused axis-0 pass
 #include "gemm_f64.cuh"
 #include "heat_plan.cuh"
 #include "heat_scan.cuh"   // K3: modal recurrences
@@ -323,6 +324,86 @@ bool dst_half_pass(const stkg_heat& h, int a, const double* src, double* dst, in
   }
 }
 
+// Time-marching fused pass over axis 0 of the padded layout (heat_fused.cuh): forward
+// transform, recurrence and inverse transform of every slice of S in one kernel.
+template <int N, int P = fused_pairs<N>()>
+void launch_fused_axis0(const stkg_heat& h, double* S, int64_t inner, int64_t ntc, int64_t l0) {
+  using C = FusedCfg<N, P>;
+  static const bool configured = [] {
+    STKG_CUDA_CHECK(cudaFuncSetAttribute(heat_fused_axis0_kernel<N, P>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(C::kSmem)));
+    return true;
+  }();
+  (void)configured;
+  const int64_t tiles = inner / C::G;
+  const double scale = std::sqrt(2.0 / static_cast<double>(N));
+  heat_fused_axis0_kernel<N, P><<<static_cast<unsigned>(tiles), C::kThreads, C::kSmem, h.stream>>>(
+      S, inner, h.n[0] * inner, ntc, l0, reinterpret_cast<const double2*>(h.twiddle[0].p), scale,
+      h.lam[0].p, h.inv_mu[0].p, h.lam_col.p, h.w_col.p, h.d_diag.p, h.d_sup.p, h.c_diag.p,
+      h.c_sup.p, h.carry.p);
+  STKG_CUDA_CHECK(cudaGetLastError());
+}
+
+// Columns per fused tile for axis-0 length n0 (0: no fused kernel for that length).
+int64_t fused_tile_cols(int64_t n0) {
+  switch (n0 + 1) {
+    case 16: return FusedCfg<16, fused_pairs<16>()>::G;
+    case 32: return FusedCfg<32, fused_pairs<32>()>::G;
+    case 64: return FusedCfg<64, fused_pairs<64>()>::G;
+    case 128: return FusedCfg<128, fused_pairs<128>()>::G;
+    case 256: return FusedCfg<256, fused_pairs<256>()>::G;
+    case 512: return FusedCfg<512, fused_pairs<512>()>::G;
+    case 1024: {
+      const char* e = std::getenv("STKG_FUSED_P");
+      return e ? 2 * std::atoi(e) : FusedCfg<1024, fused_pairs<1024>()>::G;
+    }
+    default: return 0;
+  }
+}
+
+// STKG_FUSED=0: the separate strided passes + scan kernel; 1: the fused pass whenever the
+// tile geometry allows; unset: the fused pass when it has at least half a CTA per SM.
+int fused_mode() {
+  static const int m = [] {
+    const char* e = std::getenv("STKG_FUSED");
+    return e ? std::atoi(e) : -1;
+  }();
+  return m;
+}
+
+bool use_fused_axis0(const stkg_heat& h, int64_t inner) {
+  if (h.pitch <= 0 || h.lam_col.p == nullptr) return false;
+  const int64_t G = fused_tile_cols(h.n[0]);
+  if (G == 0 || inner % G != 0) return false;
+  const int m = fused_mode();
+  if (m == 0) return false;
+  if (m > 0) return true;
+  return inner / G >= num_sms() / 2;
+}
+
+void fused_axis0(const stkg_heat& h, double* S, int64_t inner, int64_t ntc, int64_t l0) {
+  switch (h.n[0] + 1) {
+    case 16: return launch_fused_axis0<16>(h, S, inner, ntc, l0);
+    case 32: return launch_fused_axis0<32>(h, S, inner, ntc, l0);
+    case 64: return launch_fused_axis0<64>(h, S, inner, ntc, l0);
+    case 128: return launch_fused_axis0<128>(h, S, inner, ntc, l0);
+    case 256: return launch_fused_axis0<256>(h, S, inner, ntc, l0);
+    case 512: return launch_fused_axis0<512>(h, S, inner, ntc, l0);
+    case 1024: {
+      // tuning knob STKG_FUSED_P: vector pairs per tile (1, 2 or 4)
+      static const int pp = [] {
+        const char* e = std::getenv("STKG_FUSED_P");
+        return e ? std::atoi(e) : fused_pairs<1024>();
+      }();
+      if (pp == 1) return launch_fused_axis0<1024, 1>(h, S, inner, ntc, l0);
+      if (pp == 2) return launch_fused_axis0<1024, 2>(h, S, inner, ntc, l0);
+      return launch_fused_axis0<1024>(h, S, inner, ntc, l0);
+    }
+    default: throw Error(STKG_ARGUMENT, "fused pass: unsupported axis length");
+  }
+}
+
 void dst_pass(const stkg_heat& h, int a, const double* src, double* dst, int64_t inner,
               int64_t outer) {
   // The half-length kernels trade accuracy for speed (their odd outputs are a prefix sum):
@@ -433,14 +514,26 @@ void run_chunk_padded(stkg_heat& h, const double* F, double* U, double* S, int64
     ProfScope ps(h, 0);
     dst_half_pass(h, last, F, S, 1, lines, nl, P);
   }
-  for (int a = last - 1; a >= 0; --a) strided(a);
-  {
-    const int64_t nxp = padded_nx(h);
-    ProfScope ps(h, 1);
-    launch_scan(h, S, nxp, ntc, l0, mode_lambda_padded(h), mode_weight_padded(h));
-    STKG_CUDA_CHECK(cudaGetLastError());
+  int64_t inner0 = P;  // columns of axis 0
+  for (int b = 1; b < last; ++b) inner0 *= h.n[b];
+  if (use_fused_axis0(h, inner0)) {
+    // axes last-1 .. 1 forward, then axis 0 forward + recurrence + inverse marching in time
+    for (int a = last - 1; a >= 1; --a) strided(a);
+    {
+      ProfScope ps(h, 0);
+      fused_axis0(h, S, inner0, ntc, l0);
+    }
+    for (int a = 1; a < last; ++a) strided(a);
+  } else {
+    for (int a = last - 1; a >= 0; --a) strided(a);
+    {
+      const int64_t nxp = padded_nx(h);
+      ProfScope ps(h, 1);
+      launch_scan(h, S, nxp, ntc, l0, mode_lambda_padded(h), mode_weight_padded(h));
+      STKG_CUDA_CHECK(cudaGetLastError());
+    }
+    for (int a = 0; a < last; ++a) strided(a);
   }
-  for (int a = 0; a < last; ++a) strided(a);
   {
     ProfScope ps(h, 0);
     dst_half_pass(h, last, S, U, 1, lines, P, nl);
@@ -831,6 +924,30 @@ int stkg_heat_create(stkg_heat** out, const stkg_heat_desc* desc, void* cuda_str
         STKG_CUDA_CHECK(cudaStreamSynchronize(s));
         h->inv_mu_pad.alloc(nl + 1);
         h->inv_mu_pad.upload(wp.data(), nl + 1, s);
+        // per-column eigenvalue sums and weight products of the axes faster than axis 0
+        // (the fused axis-0 pass, heat_fused.cuh)
+        if (h->ndim == 2) {
+          h->lam_col.alloc(nl + 1);
+          h->lam_col.upload(lp.data(), nl + 1, s);
+          h->w_col.alloc(nl + 1);
+          h->w_col.upload(wp.data(), nl + 1, s);
+        } else {
+          const int64_t n1 = h->n[1];
+          std::vector<double> w1(n1);
+          STKG_CUDA_CHECK(cudaMemcpyAsync(w1.data(), h->inv_mu[1].p, n1 * sizeof(double),
+                                          cudaMemcpyDeviceToHost, s));
+          STKG_CUDA_CHECK(cudaStreamSynchronize(s));
+          std::vector<double> lc(n1 * (nl + 1)), wc(n1 * (nl + 1));
+          for (int64_t iy = 0; iy < n1; ++iy)
+            for (int64_t iz = 0; iz <= nl; ++iz) {
+              lc[iy * (nl + 1) + iz] = desc->lambdas[1][iy] + lp[iz];
+              wc[iy * (nl + 1) + iz] = w1[iy] * wp[iz];
+            }
+          h->lam_col.alloc(lc.size());
+          h->lam_col.upload(lc.data(), lc.size(), s);
+          h->w_col.alloc(wc.size());
+          h->w_col.upload(wc.data(), wc.size(), s);
+        }
         STKG_CUDA_CHECK(cudaStreamSynchronize(s));
       }
     }

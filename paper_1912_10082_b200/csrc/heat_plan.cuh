@@ -51,6 +51,7 @@ struct stkg_heat {
   // N = n + 1 (0: unpadded); lam/inv_mu of that axis extended by a 0 for the pad lane
   int64_t pitch = 0;
   DevBuf lam_pad, inv_mu_pad;
+  DevBuf lam_col, w_col;  // fused axis-0 pass: per-column lambda sum / weight product
   bool uniform_time = false;  // all temporal bidiagonal coefficients equal (factored scan)
   DevBuf d_diag, d_sup, c_diag, c_sup;
   // host copies used by the host-side parts of the rational Krylov solver
