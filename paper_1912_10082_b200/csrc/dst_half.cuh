@@ -259,7 +259,9 @@ struct OutSplit {
     b = ob[opad<V>(e)];
   }
 };
-template <int N>
+// OFF: the odd half starts at N/2 + OFF (OFF = 4 puts the odd outputs of a k in the other
+// half of the bank groups, for readers of 8 consecutive outputs -- heat_fused.cuh).
+template <int N, int OFF = 0>
 struct OutPair {
   double2* o;
 #if STKG_OUTPAIR_LINEAR
@@ -272,7 +274,7 @@ struct OutPair {
   // post-processing write phase 2-way conflicted).
   __device__ __forceinline__ static int idx(int e) {
     const int k = (e + 1) >> 1;
-    return (e & 1) * (N / 2) + (k ^ ((k >> 3) & 7));
+    return (e & 1) * (N / 2 + OFF) + (k ^ ((k >> 3) & 7));
   }
 #endif
   __device__ __forceinline__ void put(int e, double a, double b) const { o[idx(e)] = make_double2(a, b); }

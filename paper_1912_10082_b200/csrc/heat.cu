@@ -326,22 +326,37 @@ bool dst_half_pass(const stkg_heat& h, int a, const double* src, double* dst, in
 
 // Time-marching fused pass over axis 0 of the padded layout (heat_fused.cuh): forward
 // transform, recurrence and inverse transform of every slice of S in one kernel.
-template <int N, int P = fused_pairs<N>()>
+template <int N, int P = fused_pairs<N>(), bool CS = false, bool TMA = false>
 void launch_fused_axis0(const stkg_heat& h, double* S, int64_t inner, int64_t ntc, int64_t l0) {
-  using C = FusedCfg<N, P>;
+  using C = FusedCfg<N, P, CS, TMA>;
   static const bool configured = [] {
-    STKG_CUDA_CHECK(cudaFuncSetAttribute(heat_fused_axis0_kernel<N, P>,
+    STKG_CUDA_CHECK(cudaFuncSetAttribute(heat_fused_axis0_kernel<N, P, CS, TMA>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(C::kSmem)));
     return true;
   }();
   (void)configured;
+  CUtensorMap map;
+  std::memset(&map, 0, sizeof map);
+  if constexpr (TMA) {
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner),
+                                static_cast<cuuint64_t>(ntc * h.n[0])};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(inner * sizeof(double))};
+    const cuuint32_t box[2] = {8, C::kBoxRows};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = tensor_map_encoder()(
+        &map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, S, dims, strides, box, estr,
+        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, tma_promotion(),
+        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    STKG_REQUIRE(r == CUDA_SUCCESS, STKG_CUDA, "cuTensorMapEncodeTiled failed");
+  }
   const int64_t tiles = inner / C::G;
   const double scale = std::sqrt(2.0 / static_cast<double>(N));
-  heat_fused_axis0_kernel<N, P><<<static_cast<unsigned>(tiles), C::kThreads, C::kSmem, h.stream>>>(
-      S, inner, h.n[0] * inner, ntc, l0, reinterpret_cast<const double2*>(h.twiddle[0].p), scale,
-      h.lam[0].p, h.inv_mu[0].p, h.lam_col.p, h.w_col.p, h.d_diag.p, h.d_sup.p, h.c_diag.p,
-      h.c_sup.p, h.carry.p);
+  heat_fused_axis0_kernel<N, P, CS, TMA><<<static_cast<unsigned>(tiles), C::kThreads, C::kSmem,
+                                           h.stream>>>(
+      map, S, inner, h.n[0] * inner, ntc, l0, reinterpret_cast<const double2*>(h.twiddle[0].p),
+      scale, h.lam[0].p, h.inv_mu[0].p, h.lam_col.p, h.w_col.p, h.d_diag.p, h.d_sup.p,
+      h.c_diag.p, h.c_sup.p, h.carry.p);
   STKG_CUDA_CHECK(cudaGetLastError());
 }
 
@@ -396,9 +411,21 @@ void fused_axis0(const stkg_heat& h, double* S, int64_t inner, int64_t ntc, int6
         const char* e = std::getenv("STKG_FUSED_P");
         return e ? std::atoi(e) : fused_pairs<1024>();
       }();
+      // STKG_FUSED_V: 1 = carries in shared memory, 2 = TMA tile staging (tiles of 4 pairs)
+      static const int fv = [] {
+        const char* e = std::getenv("STKG_FUSED_V");
+        return e ? std::atoi(e) : 0;
+      }();
       if (pp == 1) return launch_fused_axis0<1024, 1>(h, S, inner, ntc, l0);
       if (pp == 2) return launch_fused_axis0<1024, 2>(h, S, inner, ntc, l0);
-      return launch_fused_axis0<1024>(h, S, inner, ntc, l0);
+      const bool tma_ok = (reinterpret_cast<uintptr_t>(S) & 15) == 0 &&
+                          ntc * h.n[0] < (int64_t(1) << 31) && inner < (int64_t(1) << 31);
+      switch (tma_ok ? fv : fv & 1) {
+        case 1: return launch_fused_axis0<1024, 4, true, false>(h, S, inner, ntc, l0);
+        case 2: return launch_fused_axis0<1024, 4, false, true>(h, S, inner, ntc, l0);
+        case 3: return launch_fused_axis0<1024, 4, true, true>(h, S, inner, ntc, l0);
+        default: return launch_fused_axis0<1024>(h, S, inner, ntc, l0);
+      }
     }
     default: throw Error(STKG_ARGUMENT, "fused pass: unsupported axis length");
   }

@@ -12,13 +12,13 @@
 //
 // The modal data never leaves the CTA between the three steps, so the scan's HBM pass and
 // the second strided pass disappear: 3 HBM passes per 2D solve (5 in 3D) instead of 5 (7),
-// 48 instead of 80 B/unknown.  The carries y_{l-1} of the tile's G n_0 modes live in
-// registers: thread t of pair f owns the OutPair staging slots s = t + T i (i < V), which
-// cover the tile's two columns' n_0 modes exactly once (the even half of OutPair holds
-// k < N/2 for e = 2k, the odd half e = 2k - 1), and the quarter-warp reads of consecutive
-// slots are bank-conflict free.  The next slice's tile is staged by 16-byte cp.async into
-// its own buffer while the current slice computes (the layout of dst_half_strided2_kernel:
-// a swizzled mirror of the 16P-byte global rows).
+// 48 instead of 80 B/unknown.  The carries y_{l-1} of the tile's G n_0 modes stay on the
+// SM (registers, or shared memory with CS): thread t of pair f owns the outputs
+// e = t + T i - 1 (i < V) of its pair's two columns, reads g~ from the forward pass's
+// OutPair staging and writes w y at the linear position e + 1 that the inverse
+// pre-processing reads (tools/banksim: both conflict-free).  The next slice's tile is staged
+// into its own buffer while the current slice computes (cp.async, or TMA boxes with TMA;
+// the layout of dst_half_strided2_kernel: a swizzled mirror of the 16P-byte global rows).
 //
 // The per-step pivot is applied as y = (g - sub y) * r with r a Newton-refined reciprocal of
 // piv = d_l + lambda c_l (two steps from rcp.approx: within an ulp of 1/piv; the reference
@@ -30,12 +30,25 @@
 
 namespace stkg {
 
-template <int N, int PP>
+// CS: carries in shared memory (one double2 per slot) instead of registers; TMA: the tile is
+// staged by SWIZZLE_64B TMA boxes (one elected thread, mbarrier) instead of per-thread
+// cp.async (P = 4 only: 64-byte rows).
+template <int N, int PP, bool CS = false, bool TMA = false>
 struct FusedCfg {
   using B = HalfStrided2Cfg<N, PP, true>;  // pair regions + separate staged tile
   static constexpr int V = B::V, T = B::T, P = B::P, G = B::G, kThreads = B::kThreads;
-  static constexpr int kRegion = B::kRegion, kTileOff = B::kTileOff;
-  static constexpr size_t kSmem = B::kSmem;
+  static constexpr int kRegion = B::kRegion;
+  static constexpr int kBoxRows = 256;
+  static constexpr int kBoxes = (N - 1 + kBoxRows - 1) / kBoxRows;
+  // bytes: regions | (512-byte aligned) tile | carries
+  static constexpr size_t kRegionBytes = size_t(P) * kRegion * sizeof(double2);
+  static constexpr size_t kTileBytes =
+      TMA ? size_t(kBoxes) * kBoxRows * 64 : size_t(B::kTile) * sizeof(double2);
+  static constexpr size_t kTileOff = TMA ? (kRegionBytes + 511) / 512 * 512 : kRegionBytes;
+  static constexpr size_t kCarryOff = kTileOff + kTileBytes;
+  static constexpr size_t kSmem = kCarryOff + (CS ? size_t(P) * N * sizeof(double2) : 0) +
+                                  (TMA ? 512 : 0);  // slack: the base is aligned at run time
+  static_assert(!TMA || P == 4, "TMA staging: tiles of 4 pairs (64-byte rows)");
 };
 
 template <int N>
@@ -55,68 +68,96 @@ __device__ __forceinline__ double nr_recip(double p) {
 // eigenvalues and 1/mu weights (n_0 entries); lam_col / w_col: the summed eigenvalue and the
 // weight product of the faster axes for each column (inner entries; pad lane 0 / 0).
 // carry (slice entries, indexed like one slice): y_{l0-1} in, y_{l0+ntc-1} out.
-template <int N, int PP>
-__global__ void __launch_bounds__(FusedCfg<N, PP>::kThreads,
-                                  FusedCfg<N, PP>::kThreads >= 256 ? 1 : 256 / FusedCfg<N, PP>::kThreads)
-    heat_fused_axis0_kernel(double* S, int64_t inner, int64_t slice, int64_t ntc, int64_t l0,
+// map (TMA only): S viewed as [ntc n_0 rows] x [inner columns], boxes of {8, 256}.
+template <int N, int PP, bool CS, bool TMA>
+__global__ void __launch_bounds__(FusedCfg<N, PP, CS, TMA>::kThreads,
+                                  FusedCfg<N, PP, CS, TMA>::kThreads >= 256
+                                      ? 1 : 256 / FusedCfg<N, PP, CS, TMA>::kThreads)
+    heat_fused_axis0_kernel(const __grid_constant__ CUtensorMap map, double* S, int64_t inner,
+                            int64_t slice, int64_t ntc, int64_t l0,
                             const double2* __restrict__ tw2, double scale,
                             const double* __restrict__ lam_ax, const double* __restrict__ w_ax,
                             const double* __restrict__ lam_col, const double* __restrict__ w_col,
                             const double* __restrict__ d_diag, const double* __restrict__ d_sup,
                             const double* __restrict__ c_diag, const double* __restrict__ c_sup,
                             double* __restrict__ carry) {
-  using C = FusedCfg<N, PP>;
+  using C = FusedCfg<N, PP, CS, TMA>;
   using SC = typename C::B;
-  constexpr int V = C::V, T = C::T, P = C::P, n = N - 1, RG = C::kRegion, H2 = N / 2;
-  extern __shared__ __align__(128) double2 sreg[];
+  using OP = OutPair<N, 4>;
+  constexpr int V = C::V, T = C::T, P = C::P, n = N - 1, RG = C::kRegion;
+  extern __shared__ __align__(128) unsigned char sraw[];
+  unsigned char* sbase = TMA ? reinterpret_cast<unsigned char*>(
+                                   (reinterpret_cast<uintptr_t>(sraw) + 511) & ~uintptr_t(511))
+                             : sraw;
+  double2* sreg = reinterpret_cast<double2*>(sbase);
+  double2* stile = reinterpret_cast<double2*>(sbase + C::kTileOff);
   __shared__ double red[P][T > 32 ? 2 * (T / 32) : 2];
+  __shared__ __align__(8) uint64_t mbar;
   const int f = threadIdx.x / T, t = threadIdx.x % T;
   const int bar = P > 1 ? 1 + f : 0;
   double2* region = sreg + f * RG;
-  double2* stile = sreg + C::kTileOff;
+  double2* creg = reinterpret_cast<double2*>(sbase + C::kCarryOff) + f * N;  // CS only
   const int64_t i0 = int64_t(blockIdx.x) * C::G;
   const int64_t ca = i0 + 2 * f;  // this pair's columns ca, ca + 1
   const double hs = 0.5 * scale;
   const double lca = lam_col[ca], lcb = lam_col[ca + 1];
   const double wca = w_col[ca], wcb = w_col[ca + 1];
 
-  auto load_tile = [&](int64_t l) {
-    const double* src = S + l * slice + i0;
-    for (int e = threadIdx.x; e < P * n; e += C::kThreads) {
-      const int c = e % P, r = e / P;
-      cp_async16(stile + r * P + SC::chunk(r, c), src + int64_t(r) * inner + 2 * c);
-    }
-    cp_async_commit();
-  };
-  // slot s = t + T i of this pair's OutPair staging -> output index e (-1: the unused odd
-  // slot k = 0).  With T a multiple of 64 the swizzle of kk = t + T i' depends on t only,
-  // so e is 2 k0 + 2 T i' (- 1): constant offsets from one base (fewer live registers).
-  const int k0 = t ^ ((t >> 3) & 7);
-  auto slot_e = [&](int i) {
-    const int ih = i % (V / 2);
-    int k;
-    if constexpr (T % 64 == 0) {
-      k = k0 + T * ih;
+  auto load_tile = [&](int64_t j) {  // local slice j of this launch
+    if constexpr (TMA) {
+      if (threadIdx.x == 0) {
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        mbar_arrive_expect_tx(&mbar, static_cast<unsigned>(C::kTileBytes));
+#pragma unroll
+        for (int b = 0; b < C::kBoxes; ++b)
+          tma_load_2d(reinterpret_cast<char*>(stile) + b * C::kBoxRows * 64, &map,
+                      static_cast<int>(i0), static_cast<int>(j * n + b * C::kBoxRows), &mbar);
+      }
     } else {
-      const int kk = t + T * ih;
-      k = kk ^ ((kk >> 3) & 7);
+      const double* src = S + j * slice + i0;
+      for (int e = threadIdx.x; e < P * n; e += C::kThreads) {
+        const int c = e % P, r = e / P;
+        cp_async16(stile + r * P + SC::chunk(r, c), src + int64_t(r) * inner + 2 * c);
+      }
+      cp_async_commit();
     }
-    return i >= V / 2 ? (k == 0 ? -1 : 2 * k - 1) : 2 * k;
   };
-  static_assert(T * V / 2 == H2, "slots i < V/2 are the even half of OutPair");
 
-  double ya[V], yb[V];
+  // The recurrence's slots: thread t handles the outputs e = t + T i - 1 (i < V; e = -1 is
+  // no output): read from OutPair<N, 4> (8 consecutive e of a quarter-warp fall in 8
+  // distinct bank groups), written as y at the linear position e + 1 that the inverse
+  // pre-processing reads (x_m at m, x_{N-m} at N - m: consecutive, conflict-free).
+  double ya[CS ? 1 : V], yb[CS ? 1 : V];
 #pragma unroll
   for (int i = 0; i < V; ++i) {
-    const int e = slot_e(i);
-    ya[i] = (l0 > 0 && e >= 0) ? carry[int64_t(e) * inner + ca] : 0.0;
-    yb[i] = (l0 > 0 && e >= 0) ? carry[int64_t(e) * inner + ca + 1] : 0.0;
+    const int e = t + T * i - 1;
+    const double a = (l0 > 0 && e >= 0) ? carry[int64_t(e) * inner + ca] : 0.0;
+    const double b = (l0 > 0 && e >= 0) ? carry[int64_t(e) * inner + ca + 1] : 0.0;
+    if constexpr (CS) {
+      creg[t + T * i] = make_double2(a, b);
+    } else {
+      ya[i] = a;
+      yb[i] = b;
+    }
   }
+  if constexpr (TMA) {
+    if (threadIdx.x == 0) {
+      mbar_init(&mbar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+  }
+  unsigned phase = 0;
 
   if (ntc > 0) load_tile(0);
   for (int64_t j = 0; j < ntc; ++j) {
     const int64_t l = l0 + j;
-    cp_async_wait<0>();
+    if constexpr (TMA) {
+      mbar_wait(&mbar, phase);
+      phase ^= 1u;
+    } else {
+      cp_async_wait<0>();
+    }
     __syncthreads();  // tile j landed; the previous slice's stores have read the regions
     double2 x[V];
 #pragma unroll
@@ -134,59 +175,85 @@ __global__ void __launch_bounds__(FusedCfg<N, PP>::kThreads,
     if (j + 1 < ntc) load_tile(j + 1);
 
     // forward transform along axis 0 -> OutPair (g~ of both columns, unweighted)
-    half_fft_post<N, V>(x, region, tw2, t, hs, red[f], OutPair<N>{region}, bar);
+    half_fft_post<N, V>(x, region, tw2, t, hs, red[f], OP{region}, bar);
     fft_sync<T>(bar);
 
-    // recurrence (stk/sylvester.hpp:131-139) on this thread's slots, in place
+    // recurrence (stk/sylvester.hpp:131-139): y = (g~ - sub y) / piv per mode
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      const int e = t + T * i - 1;
+      x[i] = e >= 0 ? region[OP::idx(e)] : make_double2(0.0, 0.0);
+    }
+    fft_sync<T>(bar);  // every slot was read: the linear y may overwrite the region
     const double dd = __ldg(d_diag + l), cd = __ldg(c_diag + l);
     const double ds = l > 0 ? __ldg(d_sup + l - 1) : 0.0, cs = l > 0 ? __ldg(c_sup + l - 1) : 0.0;
 #pragma unroll
     for (int i = 0; i < V; ++i) {
-      const int s = t + T * i;
-      const int e = slot_e(i);
+      const int e = t + T * i - 1;
       if (e >= 0) {
         const double le = __ldg(lam_ax + e), we = __ldg(w_ax + e);
         const double la = le + lca, lb = le + lcb;
-        const double2 g = region[s];
         const double ra = nr_recip(dd + la * cd), rb = nr_recip(dd + lb * cd);
-        ya[i] = (g.x - (ds + la * cs) * ya[i]) * ra;
-        yb[i] = (g.y - (ds + lb * cs) * yb[i]) * rb;
-        region[s] = make_double2(we * wca * ya[i], we * wcb * yb[i]);
+        double pa, pb;
+        if constexpr (CS) {
+          const double2 c2 = creg[t + T * i];
+          pa = c2.x;
+          pb = c2.y;
+        } else {
+          pa = ya[i];
+          pb = yb[i];
+        }
+        const double na = (x[i].x - (ds + la * cs) * pa) * ra;
+        const double nb = (x[i].y - (ds + lb * cs) * pb) * rb;
+        if constexpr (CS) {
+          creg[t + T * i] = make_double2(na, nb);
+        } else {
+          ya[i] = na;
+          yb[i] = nb;
+        }
+        region[t + T * i] = make_double2(we * wca * na, we * wcb * nb);
       }
     }
     fft_sync<T>(bar);
 
-    // inverse transform along axis 0 (DST-I is its own inverse) from OutPair
-    const OutPair<N> op{region};
+    // inverse transform along axis 0 (DST-I is its own inverse) from the linear y
 #pragma unroll
     for (int p = 0; p < V; ++p) {
       const int m = t + T * p;
       x[p] = make_double2(0.0, 0.0);
       if (m > 0) {
         const double s = -__ldg(&tw2[m].y);
-        double ua, ub, wa, wb;
-        op.get(m - 1, ua, ub);
-        op.get(N - m - 1, wa, wb);
-        x[p] = half_pre(s, ua, wa, ub, wb);
+        const double2 u = region[m], w = region[N - m];
+        x[p] = half_pre(s, u.x, w.x, u.y, w.y);
       }
     }
-    half_fft_post<N, V>(x, region, tw2, t, hs, red[f], OutPair<N>{region}, bar);
+    half_fft_post<N, V>(x, region, tw2, t, hs, red[f], OP{region}, bar);
     __syncthreads();
     double* dst = S + j * slice + i0;
     for (int e = threadIdx.x; e < P * n; e += C::kThreads) {
       const int q = e % P, kk = e / P;
       __stcs(reinterpret_cast<double2*>(dst + int64_t(kk) * inner + 2 * q),
-             sreg[q * RG + OutPair<N>::idx(kk)]);
+             sreg[q * RG + OP::idx(kk)]);
     }
   }
 #pragma unroll
   for (int i = 0; i < V; ++i) {
-    const int e = slot_e(i);
+    const int e = t + T * i - 1;
     if (e >= 0) {
-      carry[int64_t(e) * inner + ca] = ya[i];
-      carry[int64_t(e) * inner + ca + 1] = yb[i];
+      double a, b;
+      if constexpr (CS) {
+        const double2 c2 = creg[t + T * i];
+        a = c2.x;
+        b = c2.y;
+      } else {
+        a = ya[i];
+        b = yb[i];
+      }
+      carry[int64_t(e) * inner + ca] = a;
+      carry[int64_t(e) * inner + ca + 1] = b;
     }
   }
 }
+
 
 }  // namespace stkg

@@ -618,11 +618,15 @@ def test_dst_padded_solve_deterministic(stk, cuda, ndim, n, nt):
 
 
 @pytest.mark.parametrize("env", [{"STKG_HALF2": "20"}, {"STKG_HALF2": "21"}, {"STKG_HALF2": "41"},
-                                 {"STKG_SCAN_CHUNKED": "0"}, {"STKG_SCAN_RECIP": "0"}])
+                                 {"STKG_SCAN_CHUNKED": "0"}, {"STKG_SCAN_RECIP": "0"},
+                                 {"STKG_FUSED": "0"}, {"STKG_FUSED_P": "2"},
+                                 {"STKG_FUSED_V": "1"}, {"STKG_FUSED_V": "2"},
+                                 {"STKG_FUSED_V": "3"}])
 def test_tuning_variants_match_default(tmp_path, env):
     """The opt-in tuning variants (strided-tile shapes with and without next-tile prefetch,
-    the one-chain scan for small plans, per-step division in the factored scan) compute the
-    default path's solve to rounding."""
+    the one-chain scan for small plans, per-step division in the factored scan; the separate
+    strided passes + scan instead of the fused axis-0 pass, its 2-pair tiles, carries in
+    shared memory, TMA tile staging) compute the default path's solve to rounding."""
     import os
     import subprocess
     import sys

@@ -25,7 +25,7 @@ cfg = inputs.CONFIGS[a.cfg] if hasattr(inputs, "CONFIGS") else None
 if cfg is None:
     raise SystemExit("inputs.CONFIGS missing")
 if a.nt:
-    cfg = inputs.HeatConfig(cfg.name, cfg.ndim, cfg.n, a.nt, cfg.rank, cfg.seed)
+    cfg = inputs.HeatConfig(cfg.name, cfg.ndim, cfg.n, a.nt, cfg.rank, cfg.cid)
 plan = stk.HeatPlan.p1_uniform(cfg.ndim, cfg.n, cfg.nt, transform=a.transform)
 F = inputs.heat_rhs_device(cfg)
 U = torch.empty_like(F)
