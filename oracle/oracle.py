@@ -344,6 +344,118 @@ def wave_apply(sb, tb, U):
     return out
 
 
+def band_transpose(band):
+    """Band of A^T from the 7-band storage of A (band[d, i] = A(i, i + d - 3))."""
+    n = band.shape[1]
+    out = np.zeros_like(band)
+    for d in range(7):
+        o = d - 3
+        i0, i1 = max(0, -o), min(n, n - o)
+        out[d, i0:i1] = band[3 - o, i0 + o:i1 + o]
+    return out
+
+
+def band_rows(band, U):
+    """A U for a 7-band A, every product and sum in U's dtype (rows of U = columns of A)."""
+    n = band.shape[1]
+    out = np.zeros_like(U)
+    for d in range(7):
+        o = d - 3
+        i0, i1 = max(0, -o), min(n, n - o)
+        out[i0:i1] += band[d, i0:i1, None].astype(U.dtype) * U[i0 + o:i1 + o]
+    return out
+
+
+def wave_residual_banded(sb, tb, b, xh, xl=None, dtype=np.longdouble):
+    """b - B (x_h + x_l) with WaveOperator::apply (stk/outer_krylov.hpp:178-186:
+    vec(M_h U Q_t^T + A_h U (D_t + D_t^T) + Q_h U M_t), U = x as n_h x n_t column-major)
+    evaluated band by band in `dtype` (numpy longdouble: 64-bit mantissa), O(49 N) -- the
+    extended-precision check of the GPU's double-double residual at full config-4 size.
+    Returns the residual vector (dtype)."""
+    nh, nt = sb.shape[2], tb.shape[2]
+    x = xh.astype(dtype) + (0 if xl is None else xl.astype(dtype))
+    U = x.reshape(nt, nh).T
+    Mh, Ah, Qh = sb
+    Qt, Dt, Mt = tb
+    E = Dt + band_transpose(Dt)  # formed in FP64, as the reference's sparse sum is
+    out = band_rows(Qt, band_rows(Mh, U).T).T
+    out += band_rows(E, band_rows(Ah, U).T).T  # U E = (E^T U^T)^T, E = E^T
+    out += band_rows(band_transpose(Mt), band_rows(Qh, U).T).T
+    return b.astype(dtype) - out.T.ravel()
+
+
+def wave_residual_floor(sb, tb, b, xh, xl=None, unit=2.0 ** -63):
+    """Rounding floor of wave_residual_banded: unit x || |S_p| |U| |T_p|^T || / ||b|| -- the
+    size of the terms the extended-precision evaluation cancels, times its unit roundoff."""
+    ab = lambda a: np.abs(a)  # noqa: E731
+    x = np.abs(xh) + (0 if xl is None else np.abs(xl))
+    r = wave_residual_banded(ab(sb), ab(tb), np.zeros_like(b), x, dtype=np.float64)
+    return unit * float(np.linalg.norm(r)) / float(np.linalg.norm(b))
+
+
+def wave_residual_exact_entries(sb, tb, b, xh, xl, idx):
+    """b_i - (B x)_i for the listed vec indices i, exactly (Python Fractions: every band
+    product and sum exact, x = x_hi + x_lo exact), with E = D_t + D_t^T rounded in FP64 as the
+    reference forms it.  Returns (r_i rounded to double, sum of |terms|) per index."""
+    from fractions import Fraction as Fr
+    nh, nt = sb.shape[2], tb.shape[2]
+    Mh, Ah, Qh = sb
+    Qt, Dt, Mt = tb
+    E = Dt + band_transpose(Dt)
+
+    def S(k, i, a):  # S_k(i, a)
+        o = a - i
+        return float(sb[k][o + 3][i]) if -3 <= o <= 3 and 0 <= a < nh else 0.0
+
+    def band(m, i, j):  # m(i, j) for a time band
+        o = j - i
+        return float(m[o + 3][i]) if -3 <= o <= 3 and 0 <= j < nt else 0.0
+
+    out = []
+    for g in idx:
+        ih, it = g % nh, g // nh
+        acc = Fr(float(b[g]))
+        mag = abs(float(b[g]))
+        for a in range(max(0, ih - 3), min(nh, ih + 4)):
+            for bb in range(max(0, it - 3), min(nt, it + 4)):
+                u = Fr(float(xh[a + nh * bb])) + Fr(float(xl[a + nh * bb]))
+                # M_h U Q_t^T: Mh(ih,a) Qt(it,bb); A_h U E: Ah(ih,a) E(bb,it); Q_h U M_t: Qh(ih,a) Mt(bb,it)
+                for sv, tv in ((S(0, ih, a), band(Qt, it, bb)), (S(1, ih, a), band(E, bb, it)),
+                               (S(2, ih, a), band(Mt, bb, it))):
+                    if sv != 0.0 and tv != 0.0:
+                        term = Fr(sv) * Fr(tv) * u
+                        acc -= term
+                        mag += abs(float(term))
+        out.append((float(acc), mag))
+    return out
+
+
+def wave_refined_direct(sb, tb, b, steps=3):
+    """kron_direct_solve (stk/bench.hpp:414-429, SuperLU) followed by `steps` rounds of
+    iterative refinement with the longdouble banded residual: the oracle solution for
+    forward-error checks of the GPU's refined solve.  Returns (x_hi, x_lo, relres history)."""
+    import scipy.sparse as sp
+    import scipy.sparse.linalg as spl
+    Mh, Ah, Qh = (band_sparse(sb[k]) for k in range(3))
+    Qt, Dt, Mt = (band_sparse(tb[k]) for k in range(3))
+    E = (Dt + Dt.T).tocsr()
+    lu = spl.splu((sp.kron(Qt, Mh) + sp.kron(E.T, Ah) + sp.kron(Mt.T, Qh)).tocsc())
+    L = np.longdouble
+    xh = lu.solve(b)
+    xl = np.zeros_like(xh)
+    bn = float(np.linalg.norm(b))
+    hist = []
+    for _ in range(steps):
+        r = wave_residual_banded(sb, tb, b, xh, xl)
+        hist.append(float(np.sqrt(np.sum(r * r))) / bn)
+        s = xh.astype(L) + xl.astype(L) + lu.solve(r.astype(np.float64)).astype(L)
+        xh = s.astype(np.float64)
+        xl = (s - xh.astype(L)).astype(np.float64)
+    r = wave_residual_banded(sb, tb, b, xh, xl)
+    hist.append(float(np.sqrt(np.sum(r * r))) / bn)
+    return xh, xl, hist
+
+
 class WaveSystemNP:
     """numpy/scipy restatement of the wave system: WaveOperator (stk/outer_krylov.hpp:
     168-191), TwoTermPrecond (stk/sylvester.hpp:153-181, scipy eigh) and gmres (:75-164)."""

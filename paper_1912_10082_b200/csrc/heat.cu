@@ -326,11 +326,11 @@ bool dst_half_pass(const stkg_heat& h, int a, const double* src, double* dst, in
 
 // Time-marching fused pass over axis 0 of the padded layout (heat_fused.cuh): forward
 // transform, recurrence and inverse transform of every slice of S in one kernel.
-template <int N, int P = fused_pairs<N>(), bool CS = false, bool TMA = false>
+template <int N, int P = fused_pairs<N>(), bool CS = false, bool TMA = false, int V = half2_v<N>()>
 void launch_fused_axis0(const stkg_heat& h, double* S, int64_t inner, int64_t ntc, int64_t l0) {
-  using C = FusedCfg<N, P, CS, TMA>;
+  using C = FusedCfg<N, P, CS, TMA, V>;
   static const bool configured = [] {
-    STKG_CUDA_CHECK(cudaFuncSetAttribute(heat_fused_axis0_kernel<N, P, CS, TMA>,
+    STKG_CUDA_CHECK(cudaFuncSetAttribute(heat_fused_axis0_kernel<N, P, CS, TMA, V>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(C::kSmem)));
     return true;
@@ -352,7 +352,7 @@ void launch_fused_axis0(const stkg_heat& h, double* S, int64_t inner, int64_t nt
   }
   const int64_t tiles = inner / C::G;
   const double scale = std::sqrt(2.0 / static_cast<double>(N));
-  heat_fused_axis0_kernel<N, P, CS, TMA><<<static_cast<unsigned>(tiles), C::kThreads, C::kSmem,
+  heat_fused_axis0_kernel<N, P, CS, TMA, V><<<static_cast<unsigned>(tiles), C::kThreads, C::kSmem,
                                            h.stream>>>(
       map, S, inner, h.n[0] * inner, ntc, l0, reinterpret_cast<const double2*>(h.twiddle[0].p),
       scale, h.lam[0].p, h.inv_mu[0].p, h.lam_col.p, h.w_col.p, h.d_diag.p, h.d_sup.p,
@@ -411,7 +411,8 @@ void fused_axis0(const stkg_heat& h, double* S, int64_t inner, int64_t ntc, int6
         const char* e = std::getenv("STKG_FUSED_P");
         return e ? std::atoi(e) : fused_pairs<1024>();
       }();
-      // STKG_FUSED_V: 1 = carries in shared memory, 2 = TMA tile staging (tiles of 4 pairs)
+      // STKG_FUSED_V: 1 = carries in shared memory, 2 = TMA tile staging (tiles of 4 pairs),
+      // 8 = 8 values per thread (128-thread FFTs)
       static const int fv = [] {
         const char* e = std::getenv("STKG_FUSED_V");
         return e ? std::atoi(e) : 0;
@@ -420,6 +421,7 @@ void fused_axis0(const stkg_heat& h, double* S, int64_t inner, int64_t ntc, int6
       if (pp == 2) return launch_fused_axis0<1024, 2>(h, S, inner, ntc, l0);
       const bool tma_ok = (reinterpret_cast<uintptr_t>(S) & 15) == 0 &&
                           ntc * h.n[0] < (int64_t(1) << 31) && inner < (int64_t(1) << 31);
+      if (fv == 8) return launch_fused_axis0<1024, 4, false, false, 8>(h, S, inner, ntc, l0);
       switch (tma_ok ? fv : fv & 1) {
         case 1: return launch_fused_axis0<1024, 4, true, false>(h, S, inner, ntc, l0);
         case 2: return launch_fused_axis0<1024, 4, false, true>(h, S, inner, ntc, l0);

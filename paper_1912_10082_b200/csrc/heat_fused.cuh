@@ -33,10 +33,13 @@ namespace stkg {
 // CS: carries in shared memory (one double2 per slot) instead of registers; TMA: the tile is
 // staged by SWIZZLE_64B TMA boxes (one elected thread, mbarrier) instead of per-thread
 // cp.async (P = 4 only: 64-byte rows).
-template <int N, int PP, bool CS = false, bool TMA = false>
+// VV: complex values per thread of the FFTs (16: radix-16,16,4 stages, 64 threads per pair for
+// N = 1024; 8: radix-8,8,8,2 stages, 128 threads per pair -- twice the warps per SM for the
+// same tile, one more shared-memory exchange per transform).
+template <int N, int PP, bool CS = false, bool TMA = false, int VV = half2_v<N>()>
 struct FusedCfg {
-  using B = HalfStrided2Cfg<N, PP, true>;  // pair regions + separate staged tile
-  static constexpr int V = B::V, T = B::T, P = B::P, G = B::G, kThreads = B::kThreads;
+  using B = HalfStrided2Cfg<N, PP, true>;  // tile geometry (swizzle), region size
+  static constexpr int V = VV, T = N / V, P = B::P, G = B::G, kThreads = P * T;
   static constexpr int kRegion = B::kRegion;
   static constexpr int kBoxRows = 256;
   static constexpr int kBoxes = (N - 1 + kBoxRows - 1) / kBoxRows;
@@ -69,10 +72,10 @@ __device__ __forceinline__ double nr_recip(double p) {
 // weight product of the faster axes for each column (inner entries; pad lane 0 / 0).
 // carry (slice entries, indexed like one slice): y_{l0-1} in, y_{l0+ntc-1} out.
 // map (TMA only): S viewed as [ntc n_0 rows] x [inner columns], boxes of {8, 256}.
-template <int N, int PP, bool CS, bool TMA>
-__global__ void __launch_bounds__(FusedCfg<N, PP, CS, TMA>::kThreads,
-                                  FusedCfg<N, PP, CS, TMA>::kThreads >= 256
-                                      ? 1 : 256 / FusedCfg<N, PP, CS, TMA>::kThreads)
+template <int N, int PP, bool CS, bool TMA, int VV>
+__global__ void __launch_bounds__(FusedCfg<N, PP, CS, TMA, VV>::kThreads,
+                                  FusedCfg<N, PP, CS, TMA, VV>::kThreads >= 256
+                                      ? 1 : 256 / FusedCfg<N, PP, CS, TMA, VV>::kThreads)
     heat_fused_axis0_kernel(const __grid_constant__ CUtensorMap map, double* S, int64_t inner,
                             int64_t slice, int64_t ntc, int64_t l0,
                             const double2* __restrict__ tw2, double scale,
@@ -81,7 +84,7 @@ __global__ void __launch_bounds__(FusedCfg<N, PP, CS, TMA>::kThreads,
                             const double* __restrict__ d_diag, const double* __restrict__ d_sup,
                             const double* __restrict__ c_diag, const double* __restrict__ c_sup,
                             double* __restrict__ carry) {
-  using C = FusedCfg<N, PP, CS, TMA>;
+  using C = FusedCfg<N, PP, CS, TMA, VV>;
   using SC = typename C::B;
   using OP = OutPair<N, 4>;
   constexpr int V = C::V, T = C::T, P = C::P, n = N - 1, RG = C::kRegion;
@@ -211,19 +214,23 @@ __global__ void __launch_bounds__(FusedCfg<N, PP, CS, TMA>::kThreads,
           ya[i] = na;
           yb[i] = nb;
         }
-        region[t + T * i] = make_double2(we * wca * na, we * wcb * nb);
+        x[i] = make_double2(we * wca * na, we * wcb * nb);
+        region[t + T * i] = x[i];
       }
     }
     fft_sync<T>(bar);
 
-    // inverse transform along axis 0 (DST-I is its own inverse) from the linear y
+    // inverse transform along axis 0 (DST-I is its own inverse): this thread's own y at
+    // m = t + T p is x[p] already (e = m - 1); only the mirrored y at N - m comes from the
+    // linear layout
 #pragma unroll
     for (int p = 0; p < V; ++p) {
       const int m = t + T * p;
+      const double2 u = x[p];
       x[p] = make_double2(0.0, 0.0);
       if (m > 0) {
         const double s = -__ldg(&tw2[m].y);
-        const double2 u = region[m], w = region[N - m];
+        const double2 w = region[N - m];
         x[p] = half_pre(s, u.x, w.x, u.y, w.y);
       }
     }

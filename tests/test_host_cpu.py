@@ -305,3 +305,26 @@ def test_oracle_rksm_heat_ex1_acceptance(orc, ndim, nh):
             col = np.linalg.norm(U - Ucn, axis=1) / np.linalg.norm(Ucn, axis=1)
             assert col.max() <= 1e-6, col.max()
     assert max(its_all) - min(its_all) <= 3
+
+
+# ----------------------------------- extended-precision wave residual (oracle infra) --
+def test_oracle_banded_wave_residual_matches_apply(orc, ref_bands):
+    """wave_residual_banded in float64 is WaveOperator::apply (the sparse restatement) bit
+    for bit, and its longdouble evaluation agrees to FP64 rounding."""
+    sb, tb = ref_bands["space_31_3"], ref_bands["time_33_3"]
+    W = orc.WaveSystemNP(sb, tb)
+    rng = np.random.default_rng(3)
+    x, b = rng.standard_normal(W.nh * W.nt), rng.standard_normal(W.nh * W.nt)
+    r64 = orc.wave_residual_banded(sb, tb, b, x, dtype=np.float64)
+    assert np.array_equal(r64, b - W.apply(x))
+    rld = orc.wave_residual_banded(sb, tb, b, x)
+    assert np.linalg.norm(rld.astype(np.float64) - r64) <= 1e-14 * np.linalg.norm(r64)
+
+
+def test_oracle_refined_direct_wave_solve(orc, ref_bands):
+    """kron_direct_solve + longdouble iterative refinement reaches a relative residual far
+    below the FP64 direct solve's (the oracle for the GPU refined solve's forward error)."""
+    sb, tb = ref_bands["space_31_3"], ref_bands["time_33_3"]
+    b = np.random.default_rng(4).standard_normal(sb.shape[2] * tb.shape[2])
+    xh, xl, hist = orc.wave_refined_direct(sb, tb, b, steps=3)
+    assert hist[-1] <= 1e-15 and hist[-1] < hist[0]
