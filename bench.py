@@ -316,8 +316,35 @@ def run_reference(args):
     return 0
 
 
+def fused_in_use(cfg) -> bool:
+    """Whether the plan runs the time-marching fused axis-0 pass (heat.cu use_fused_axis0:
+    padded half-length layout, tiles of 2P columns of axis 0, at least half a CTA per SM)."""
+    import torch
+    if os.environ.get("STKG_FUSED") == "0" or not half_kernels(cfg):
+        return False
+    N = cfg.n + 1
+    T = N // 16
+    P = 4 if T >= 32 else 128 // T
+    if N == 1024 and os.environ.get("STKG_FUSED_P"):
+        P = int(os.environ["STKG_FUSED_P"])
+    inner0 = N * cfg.n ** (cfg.ndim - 2)
+    sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    return inner0 % (2 * P) == 0 and (os.environ.get("STKG_FUSED") == "1"
+                                      or inner0 // (2 * P) >= sms // 2)
+
+
+def fused_binding_from_profiles():
+    p = ROOT / "profiles" / "traffic.json"
+    try:
+        return json.loads(p.read_text()).get("fused_binding_resource")
+    except Exception:
+        return None
+
+
 def _timed_path(stk, inputs, cfg, transform, args, stream, barrier, F, U, with_clocks):
-    """Warm up and time args.steps solves of one transform backend on the plan stream."""
+    """Warm up and time args.steps solves of one transform backend on the plan stream (no
+    profiling: 2D plans may run their overlapped multi-stream schedule), then one profiled
+    pass of 2 solves (kernels back to back on the plan stream) for the per-kernel times."""
     import torch
     plan = build_plan(stk, cfg, stream=stream.cuda_stream, transform=transform)
     for _ in range(args.warmup):
@@ -328,7 +355,6 @@ def _timed_path(stk, inputs, cfg, transform, args, stream, barrier, F, U, with_c
         clocks.start()
     barrier()
     torch.cuda.synchronize()
-    plan.profile_begin()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
@@ -336,15 +362,27 @@ def _timed_path(stk, inputs, cfg, transform, args, stream, barrier, F, U, with_c
         plan.solve(F, out=U)
     e1.record(stream)
     stream.synchronize()
-    prof = plan.profile_end()
     torch.cuda.synchronize()
     barrier()
     clk = clocks.stop() if clocks else None
     ms = e0.elapsed_time(e1)
+    nprof = 2
+    plan.profile_begin()
+    p0 = torch.cuda.Event(enable_timing=True)
+    p1 = torch.cuda.Event(enable_timing=True)
+    p0.record(stream)
+    for _ in range(nprof):
+        plan.solve(F, out=U)
+    p1.record(stream)
+    stream.synchronize()
+    prof = plan.profile_end()
+    ms_seq = p0.elapsed_time(p1) / nprof  # the same solve with its kernels back to back
     relres, _ = plan.residual(U, F)
     t_ms, t_n = prof["transform"]
     s_ms, s_n = prof["scan"]
     N = cfg.unknowns
+    sec = ms / 1e3 / args.steps
+    fused = transform == "dst" and fused_in_use(cfg)
     if transform == "dense":
         flops = 2.0 * cfg.n * N  # 2n flop per unknown per axis transform launch
         achieved = flops / (t_ms / t_n / 1e3) / 1e12
@@ -354,39 +392,62 @@ def _timed_path(stk, inputs, cfg, transform, args, stream, barrier, F, U, with_c
                 "peak_source": FP64_PEAK_SOURCE,
                 "whole_solve_frac": (2 * cfg.ndim * flops * args.steps / (ms / 1e3) / 1e12)
                 / FP64_PEAK_TFLOPS}
+        roof["share_of_step"] = t_ms / nprof / (ms_seq)
     else:
-        bytes_launch = 16.0 * N  # read + write each unknown once per axis pass
-        achieved = bytes_launch / (t_ms / t_n / 1e3) / 1e9
-        # which sine-transform kernels the plan runs (heat.cu::dst_pass)
         half = half_kernels(cfg)
         fft_flops = fft_flop_per_unknown(cfg.n, half)  # per element and axis pass
-        kname = ("dst_half_kernel / dst_half_strided2_kernel (FP64 half-length DST-I: "
-                 "N-point Stockham FFT per vector pair)") if half else \
-            "dst_axis_kernel / dst_strided_kernel (FP64 padded 2N-point FFT DST-I)"
-        passes = (t_n + s_n) / (args.steps)  # HBM passes of the executed schedule per solve
-        sec = ms / 1e3 / args.steps
         t_hbm = 16.0 * N / (HBM_GBS * 1e9)  # read F + write U once
-        t_fp64 = (2 * cfg.ndim * fft_flops + 3.0) * N / (FP64_PEAK_TFLOPS * 1e12)
-        roof = {"bound": "hbm", "kernel": kname,
-                "achieved": achieved, "peak": HBM_GBS, "unit": "GB/s",
-                "frac": achieved / HBM_GBS,
-                "traffic": traffic_from_profiles("dst_half" if half else "dst"),
-                "binding_resource": binding_from_profiles() if half else None,
-                "peak_source": HBM_SOURCE,
-                "flop_per_unknown_per_pass": fft_flops,
-                "whole_solve_frac": max(t_hbm, t_fp64) / sec,
-                "whole_solve_basis": "SURVEY 8(d): T_roof = max(16 B/unknown / HBM, executed "
-                                     "DST + scan flops / FP64 peak) over the measured solve",
-                "whole_solve_roof_ms": 1e3 * max(t_hbm, t_fp64),
-                "hbm_passes_per_solve": passes,
-                "whole_solve_frac_executed_passes": passes * t_hbm / sec}
-    roof["share_of_step"] = t_ms / ms
-    roof["scan_share_of_step"] = s_ms / ms
+        rec_flops = 12.0  # recurrence: 2 FMA pivot/coupling, Newton reciprocal, update, weight
+        t_fp64 = (2 * cfg.ndim * fft_flops + rec_flops) * N / (FP64_PEAK_TFLOPS * 1e12)
+        passes = (t_n + s_n) / nprof  # HBM passes of the executed schedule per solve
+        t_tr = t_ms / t_n  # mean transform-only pass
+        contig = {"kernel": "dst_half_kernel (contiguous axis, forward / inverse)",
+                  "ms_per_launch": t_tr, "achieved_gbs": 16.0 * N / (t_tr / 1e3) / 1e9,
+                  "frac_hbm": 16.0 * N / (t_tr / 1e3) / 1e9 / HBM_GBS,
+                  "launches_per_solve": t_n / nprof}
+        if fused:
+            t_f = s_ms / s_n
+            achieved = 16.0 * N / (t_f / 1e3) / 1e9
+            roof = {"bound": "hbm",
+                    "kernel": "heat_fused_axis0_kernel (time-marching: forward DST-I along axis 0, "
+                              "modal recurrence, inverse DST-I; one read + one write of S)",
+                    "achieved": achieved, "peak": HBM_GBS, "unit": "GB/s",
+                    "frac": achieved / HBM_GBS,
+                    "traffic": traffic_from_profiles("fused"),
+                    "binding_resource": fused_binding_from_profiles(),
+                    "ms_per_launch": t_f,
+                    "flop_per_unknown": 2 * fft_flops + rec_flops,
+                    "fp64_tflops": (2 * fft_flops + rec_flops) * N / (t_f / 1e3) / 1e12,
+                    "share_of_sequential_step": s_ms / nprof / ms_seq,
+                    "other_kernel": contig}
+        else:
+            achieved = 16.0 * N / (t_tr / 1e3) / 1e9
+            kname = ("dst_half_kernel / dst_half_strided2_kernel (FP64 half-length DST-I: "
+                     "N-point Stockham FFT per vector pair)") if half else \
+                "dst_axis_kernel / dst_strided_kernel (FP64 padded 2N-point FFT DST-I)"
+            roof = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": HBM_GBS,
+                    "unit": "GB/s", "frac": achieved / HBM_GBS,
+                    "traffic": traffic_from_profiles("dst_half" if half else "dst"),
+                    "binding_resource": binding_from_profiles() if half else None,
+                    "share_of_sequential_step": t_ms / nprof / ms_seq}
+        roof.update({
+            "peak_source": HBM_SOURCE,
+            "flop_per_unknown_per_transform_pass": fft_flops,
+            "whole_solve_frac": max(t_hbm, t_fp64) / sec,
+            "whole_solve_basis": "SURVEY 8(d): T_roof = max(16 B/unknown / HBM, executed "
+                                 "DST + recurrence flops / FP64 peak) over the measured solve",
+            "whole_solve_roof_ms": 1e3 * max(t_hbm, t_fp64),
+            "hbm_passes_per_solve": passes,
+            "whole_solve_frac_executed_passes": passes * t_hbm / sec,
+            "sequential_ms_per_step": ms_seq,
+            "overlap_gain_ms": ms_seq - 1e3 * sec})
     out = {"transform": transform, "ms_per_step": ms / args.steps, "ms": ms,
            "value": N * args.steps / (ms / 1e3), "relres_gpu_k1": relres, "roofline": roof,
-           "launches": int(t_n + s_n),
-           "k3_scan": {"ms_per_launch": s_ms / s_n, "gbs": 16.0 * N / (s_ms / s_n / 1e3) / 1e9,
-                       "frac_hbm": 16.0 * N / (s_ms / s_n / 1e3) / 1e9 / HBM_GBS}}
+           "launches": int(round((t_n + s_n) / nprof * args.steps)),
+           "recurrence_kernel": {"kernel": "heat_fused_axis0_kernel" if fused else
+                                 "heat_scan_kernel", "ms_per_launch": s_ms / s_n,
+                                 "gbs": 16.0 * N / (s_ms / s_n / 1e3) / 1e9,
+                                 "frac_hbm": 16.0 * N / (s_ms / s_n / 1e3) / 1e9 / HBM_GBS}}
     return plan, out, clk
 
 
@@ -408,21 +469,22 @@ def heat_config_leg(stk, inputs, name, stream, steps=10, warmup=3, with_cpu=True
         for _ in range(warmup):
             plan.solve(F, out=U)
         stream.synchronize()
-        plan.profile_begin()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(steps):
             plan.solve(F, out=U)
         e1.record(stream)
         stream.synchronize()
-        prof = plan.profile_end()
         ms = e0.elapsed_time(e1) / steps
+        plan.profile_begin()
+        plan.solve(F, out=U)
+        prof = plan.profile_end()
         relres, _ = plan.residual(U, F)
         out = {"workload": cfg.name, "unknowns": N, "ms": ms, "value": N / (ms / 1e3),
                "relres_gpu_k1": relres,
-               "launches_per_solve": (prof["transform"][1] + prof["scan"][1]) / steps}
+               "launches_per_solve": prof["transform"][1] + prof["scan"][1]}
         half = half_kernels(cfg)
-        fl = (2 * cfg.ndim * fft_flop_per_unknown(cfg.n, half) + 3.0) * N
+        fl = (2 * cfg.ndim * fft_flop_per_unknown(cfg.n, half) + 12.0) * N
         t_roof = max(16.0 * N / (HBM_GBS * 1e9), fl / (FP64_PEAK_TFLOPS * 1e12))
         out["roofline"] = {"bound": "hbm" if 16.0 * N / HBM_GBS / 1e9 >= fl / FP64_PEAK_TFLOPS
                            / 1e12 else "fp64", "roof_ms": 1e3 * t_roof,
@@ -662,7 +724,7 @@ def run_ours(args):
         "k1_residual": {"ms": k1_ms, "gbs": 16.0 * N / (k1_ms / 1e3) / 1e9,
                         "frac_hbm": 16.0 * N / (k1_ms / 1e3) / 1e9 / HBM_GBS,
                         "bytes_alg": 16 * N},
-        "k3_scan": res["k3_scan"],
+        "recurrence_kernel": res["recurrence_kernel"],
         "clocks": clk,
     }
     if args.config == "cfg3":

@@ -145,9 +145,12 @@ int stkg_heat_residual(stkg_heat* plan, const double* U, const double* F, double
 
 /* Kernel-class timing for roofline evidence (no reference counterpart).  enable = 1 resets
  * and starts recording CUDA events around every launch on the plan's stream; enable = 0
- * stops, synchronizes and writes, per class [0] = basis transforms (DMMA GEMM launches),
- * [1] = modal recurrence (scan), the summed device milliseconds (ms_out[2]) and launch
- * counts (launches_out[2]).  Either output may be NULL. */
+ * stops, synchronizes and writes, per class [0] = basis transforms alone (DMMA GEMM or
+ * sine-transform passes), [1] = kernels that run the modal recurrence (the scan, or the
+ * fused axis-0 pass: transforms + recurrence), the summed device milliseconds (ms_out[2])
+ * and launch counts (launches_out[2]).  Either output may be NULL.  While recording, 2D
+ * solves run their passes back to back on the plan stream (no overlapped schedule), so the
+ * per-launch times are those of the kernels alone. */
 int stkg_heat_profile(stkg_heat* plan, int enable, double* ms_out, int64_t* launches_out);
 
 /* ------------------------------------------------------------------ wave plans --- */

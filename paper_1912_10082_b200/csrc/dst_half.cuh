@@ -460,11 +460,15 @@ struct HalfCfg {
 // ld_dst > n (the padded internal layout of heat.cu's device solve) also writes zeros into
 // the ld_dst - n pad entries, so that the padded lanes stay finite through later passes.
 // dst may alias src when ld_src == ld_dst (an item is read completely before it is written).
-template <int N>
+// ticket != nullptr: items are handed out dynamically (atomicAdd on *ticket, which must be 0
+// at launch) instead of by grid stride -- used when the kernel runs beside the fused axis-0
+// pass on the SMs that pass leaves idle (heat.cu run_chunk_padded_overlap), where a static
+// split would leave the items of not-yet-resident CTAs waiting.
+template <int N, bool DYN = false>
 __global__ void __launch_bounds__(HalfCfg<N>::kThreads, HalfCfg<N>::kMinBlocks)
     dst_half_kernel(const double* src, double* dst, int64_t nvec,
                     const double2* __restrict__ tw2, double scale, int64_t ld_src,
-                    int64_t ld_dst) {
+                    int64_t ld_dst, unsigned long long* ticket = nullptr) {
   using C = HalfCfg<N>;
   constexpr int V = C::V, T = C::T, F = C::F, n = N - 1;
   extern __shared__ __align__(16) double2 hbuf[];
@@ -478,7 +482,17 @@ __global__ void __launch_bounds__(HalfCfg<N>::kThreads, HalfCfg<N>::kMinBlocks)
   const int64_t nitems = (npairs + F - 1) / F;
   const double hs = 0.5 * scale;
   const int ldo = static_cast<int>(ld_dst);
-  for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x) {
+  __shared__ int64_t s_next[2];
+  int64_t item = blockIdx.x;
+  if constexpr (DYN) {
+    if (threadIdx.x == 0) s_next[1] = static_cast<int64_t>(atomicAdd(ticket, 1ull));
+    __syncthreads();
+    item = s_next[1];
+  }
+  for (int it = 0; item < nitems; ++it) {
+    if constexpr (DYN) {
+      if (threadIdx.x == 0) s_next[it & 1] = static_cast<int64_t>(atomicAdd(ticket, 1ull));
+    }
     const int64_t g0 = 2 * (item * F + f);  // first vector of this FFT's pair
     const bool has_a = F == 1 || g0 < nvec, has_b = g0 + 1 < nvec;
     const double* sa = src + (has_a ? g0 : 0) * ld_src;
@@ -495,7 +509,7 @@ __global__ void __launch_bounds__(HalfCfg<N>::kThreads, HalfCfg<N>::kMinBlocks)
         x[p] = half_pre(s, sa[m - 1], sa[mm - 1], xb, xbm);
       }
     }
-    if constexpr (STKG_DST_PREFETCH > 0) {  // a later item's 2F vectors into L2
+    if (STKG_DST_PREFETCH > 0 && !DYN) {  // a later item's 2F vectors into L2
       const int64_t nitem = item + STKG_DST_PREFETCH * int64_t(gridDim.x);
       if (nitem < nitems) {
         const int64_t nv0 = 2 * F * nitem;
@@ -511,6 +525,17 @@ __global__ void __launch_bounds__(HalfCfg<N>::kThreads, HalfCfg<N>::kMinBlocks)
     // __syncthreads below)
     half_fft_post<N, V, true>(x, fbuf, tw2, t, hs, red, OutSplit<V>{oa, ob});
     __syncthreads();
+    if (STKG_DST_PREFETCH > 0 && DYN) {  // the next ticket's item into L2
+      const int64_t nitem = s_next[it & 1];
+      if (nitem < nitems) {
+        const int64_t nv0 = 2 * F * nitem;
+        const int64_t nv = nvec - nv0 < 2 * F ? nvec - nv0 : 2 * F;
+        const char* base = reinterpret_cast<const char*>(src + nv0 * ld_src);
+        const int64_t bytes = nv * ld_src * int64_t(sizeof(double));
+        for (int64_t o = int64_t(threadIdx.x) * 128; o < bytes; o += int64_t(C::kThreads) * 128)
+          prefetch_l2(base + o);
+      }
+    }
     if constexpr (F == 1) {
       double* da = dst + g0 * ld_dst;
       for (int e = t; e < ldo; e += T) da[e] = e < n ? oa[opad<V>(e)] : 0.0;
@@ -528,6 +553,13 @@ __global__ void __launch_bounds__(HalfCfg<N>::kThreads, HalfCfg<N>::kMinBlocks)
         d0[e] = idx < n ? o_q[opad<V>(idx)] : 0.0;
       }
       __syncthreads();  // other FFTs' buffers were read: next item may overwrite them
+    }
+    // (the barriers above ordered thread 0's ticket write of this iteration before this read;
+    // the slot is rewritten two iterations later, after every thread has passed this read)
+    if constexpr (DYN) {
+      item = s_next[it & 1];
+    } else {
+      item += gridDim.x;
     }
   }
 }

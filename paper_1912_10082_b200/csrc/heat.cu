@@ -80,6 +80,9 @@ ModeWeight mode_weight(const stkg_heat& h) {
 // The same over the padded internal layout (h.pitch > 0): n_last -> pitch, pad lanes get
 // lambda 0 and weight 0 (their transformed data are zero, and stay zero).
 int64_t padded_nx(const stkg_heat& h) { return h.nx / h.n[h.ndim - 1] * h.pitch; }
+// The stream the DST / fused launchers use: the plan stream unless an overlapped schedule
+// (run_chunk_padded_overlap) has redirected them.
+cudaStream_t launch_stream(const stkg_heat& h) { return h.run_stream ? h.run_stream : h.stream; }
 ModeLambda mode_lambda_padded(const stkg_heat& h) {
   if (h.ndim == 2) return ModeLambda{h.lam[0].p, h.lam_pad.p, nullptr, h.pitch, 1, 2};
   return ModeLambda{h.lam[0].p, h.lam[1].p, h.lam_pad.p, h.n[1], h.pitch, 3};
@@ -204,7 +207,7 @@ void launch_dst_half_strided_tma(const stkg_heat& h, const double* src, double* 
   }();
   const int64_t blocks = std::min<int64_t>(nvec / C::G, int64_t(num_sms()) * per_sm);
   dst_half_strided_tma_kernel<N><<<static_cast<unsigned>(blocks), C::kThreads, TC::kSmem,
-                                   h.stream>>>(map, dst, inner, nvec, tw2, scale);
+                                   launch_stream(h)>>>(map, dst, inner, nvec, tw2, scale);
 }
 
 template <int N, int P, bool PF>
@@ -222,7 +225,7 @@ void launch_dst_half_strided2(const stkg_heat& h, const double* src, double* dst
   }();
   const int64_t blocks = std::min<int64_t>(nvec / C::G, int64_t(num_sms()) * per_sm);
   dst_half_strided2_kernel<N, P, PF><<<static_cast<unsigned>(blocks), C::kThreads, C::kSmem,
-                                       h.stream>>>(src, dst, inner, nvec, tw2, scale);
+                                       launch_stream(h)>>>(src, dst, inner, nvec, tw2, scale);
 }
 
 // Half-length kernels (dst_half.cuh) for N = n + 1 in [16, 1024].  Contiguous axis
@@ -248,8 +251,21 @@ void launch_dst_half(const stkg_heat& h, int a, const double* src, double* dst, 
     }();
     const int64_t blocks = std::min<int64_t>(ceil_div(nvec, 2 * C::F), int64_t(num_sms()) * per_sm);
     const int64_t lds = ld_src > 0 ? ld_src : N - 1, ldd = ld_dst > 0 ? ld_dst : N - 1;
-    dst_half_kernel<N><<<static_cast<unsigned>(blocks), C::kThreads, C::kSmem, h.stream>>>(
-        src, dst, nvec, tw2, scale, lds, ldd);
+    if (h.run_ticket) {
+      static const bool dyn_configured = [] {
+        STKG_CUDA_CHECK(cudaFuncSetAttribute(dst_half_kernel<N, true>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(C::kSmem)));
+        return true;
+      }();
+      (void)dyn_configured;
+      dst_half_kernel<N, true><<<static_cast<unsigned>(blocks), C::kThreads, C::kSmem,
+                                 launch_stream(h)>>>(src, dst, nvec, tw2, scale, lds, ldd,
+                                                     h.run_ticket);
+    } else {
+      dst_half_kernel<N><<<static_cast<unsigned>(blocks), C::kThreads, C::kSmem,
+                           launch_stream(h)>>>(src, dst, nvec, tw2, scale, lds, ldd);
+    }
   } else if (wide && inner % HalfStrided2Cfg<N>::G == 0) {
     if constexpr (N / half_v<N>() >= 32) {  // tiles of 4 pairs: optional TMA staging
       if (use_tma_strided() && (reinterpret_cast<uintptr_t>(src) & 15) == 0 &&
@@ -284,7 +300,7 @@ void launch_dst_half(const stkg_heat& h, int a, const double* src, double* dst, 
       return std::max(b, 1);
     }();
     const int64_t blocks = std::min<int64_t>(ceil_div(nvec, C::G), int64_t(num_sms()) * per_sm);
-    dst_half_strided_kernel<N><<<static_cast<unsigned>(blocks), C::kThreads, C::kSmem, h.stream>>>(
+    dst_half_strided_kernel<N><<<static_cast<unsigned>(blocks), C::kThreads, C::kSmem, launch_stream(h)>>>(
         src, dst, inner, nvec, tw2, scale);
   }
   STKG_CUDA_CHECK(cudaGetLastError());
@@ -353,7 +369,7 @@ void launch_fused_axis0(const stkg_heat& h, double* S, int64_t inner, int64_t nt
   const int64_t tiles = inner / C::G;
   const double scale = std::sqrt(2.0 / static_cast<double>(N));
   heat_fused_axis0_kernel<N, P, CS, TMA, V><<<static_cast<unsigned>(tiles), C::kThreads, C::kSmem,
-                                           h.stream>>>(
+                                              launch_stream(h)>>>(
       map, S, inner, h.n[0] * inner, ntc, l0, reinterpret_cast<const double2*>(h.twiddle[0].p),
       scale, h.lam[0].p, h.inv_mu[0].p, h.lam_col.p, h.w_col.p, h.d_diag.p, h.d_sup.p,
       h.c_diag.p, h.c_sup.p, h.carry.p);
@@ -522,6 +538,107 @@ void axis_pass(stkg_heat& h, int a, bool forward, const double* src, double* dst
 }  // namespace stkg
 
 namespace {
+// STKG_OVERLAP: time chunks of the overlapped 2D schedule (0 or 1: off).
+int overlap_chunks() {
+  static const int k = [] {
+    const char* e = std::getenv("STKG_OVERLAP");
+    return e ? std::atoi(e) : 4;
+  }();
+  return k;
+}
+
+// 2D plans whose fused axis-0 pass has fewer tiles than the GPU has SMs (cfg3: 128 tiles on
+// 148 SMs) leave SMs idle for the whole fused pass.  This schedule cuts time into K chunks and
+// runs, on a low-priority stream, the contiguous forward pass of later chunks and the
+// contiguous inverse pass of earlier ones while the fused pass of chunk c runs on a
+// high-priority stream:
+//   lo:  C1(0) C1(1) C1(2) [X0] C2(0) C1(3) [X1] C2(1) [X2] C2(2) [X3] C2(3)
+//   hi:  [C1(0)] X(0) [C1(1)] X(1) [C1(2)] X(2) [C1(3)] X(3)
+// (brackets: event waits).  The fused pass holds all registers of its SMs, so the contiguous
+// CTAs land only on the idle SMs while it runs; they take their items from a ticket counter
+// (dst_half_kernel's dynamic mode), so the items of CTAs that are not yet resident are not
+// stranded behind the fused pass.  The recurrence carries cross chunks through h.carry
+// (X(c) follows X(c-1) on the same stream).  Same arithmetic as run_chunk_padded.
+void run_chunk_padded_overlap(stkg_heat& h, const double* F, double* U, double* S, int64_t l0,
+                              int64_t ntc, int K, int64_t inner0) {
+  const int64_t nl = h.n[1], P = h.pitch, lines = h.nx / nl, sp = padded_nx(h);
+  if (!h.s_hi) {
+    int least = 0, greatest = 0;
+    STKG_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    STKG_CUDA_CHECK(cudaStreamCreateWithPriority(&h.s_hi, cudaStreamNonBlocking, greatest));
+    STKG_CUDA_CHECK(cudaStreamCreateWithPriority(&h.s_lo, cudaStreamNonBlocking, least));
+  }
+  const size_t nev = 2 * size_t(K) + 3;
+  while (h.ov_ev.size() < nev) {
+    cudaEvent_t e;
+    STKG_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    h.ov_ev.push_back(e);
+  }
+  if (h.tickets_n < 2 * K) {
+    if (h.tickets) STKG_CUDA_CHECK(cudaFree(h.tickets));
+    STKG_CUDA_CHECK(cudaMalloc(&h.tickets, 2 * K * sizeof(unsigned long long)));
+    h.tickets_n = 2 * K;
+  }
+  cudaEvent_t* ev_c1 = h.ov_ev.data();
+  cudaEvent_t* ev_x = ev_c1 + K;
+  cudaEvent_t ev_start = ev_x[K], ev_lo = ev_x[K + 1], ev_hi = ev_x[K + 2];
+  STKG_CUDA_CHECK(cudaEventRecord(ev_start, h.stream));
+  STKG_CUDA_CHECK(cudaStreamWaitEvent(h.s_hi, ev_start, 0));
+  STKG_CUDA_CHECK(cudaStreamWaitEvent(h.s_lo, ev_start, 0));
+  STKG_CUDA_CHECK(cudaMemsetAsync(h.tickets, 0, 2 * K * sizeof(unsigned long long), h.s_lo));
+  // even slice counts per chunk: every chunk then starts at an even vector index, so the
+  // contiguous passes pair the same vectors in one complex FFT as the unchunked pass does
+  // (bit-identical results; tests/test_heat_gpu.py::test_overlapped_schedule_bit_identical)
+  const int64_t chunk = ((ntc + K - 1) / K + 1) / 2 * 2;
+  auto c0 = [&](int c) { return std::min<int64_t>(ntc, c * chunk); };
+  while (K > 1 && c0(K - 1) >= ntc) --K;  // rounding up may leave trailing chunks empty
+  auto len = [&](int c) { return c0(c + 1) - c0(c); };
+  auto C1 = [&](int c) {
+    h.run_stream = h.s_lo;
+    h.run_ticket = h.tickets + c;
+    dst_half_pass(h, 1, F + c0(c) * h.nx, S + c0(c) * sp, 1, lines * len(c), nl, P);
+    STKG_CUDA_CHECK(cudaEventRecord(ev_c1[c], h.s_lo));
+  };
+  auto C2 = [&](int c) {
+    STKG_CUDA_CHECK(cudaStreamWaitEvent(h.s_lo, ev_x[c], 0));
+    h.run_stream = h.s_lo;
+    h.run_ticket = h.tickets + K + c;
+    dst_half_pass(h, 1, S + c0(c) * sp, U + c0(c) * h.nx, 1, lines * len(c), P, nl);
+  };
+  auto X = [&](int c) {
+    STKG_CUDA_CHECK(cudaStreamWaitEvent(h.s_hi, ev_c1[c], 0));
+    h.run_stream = h.s_hi;
+    h.run_ticket = nullptr;
+    fused_axis0(h, S + c0(c) * sp, inner0, len(c), l0 + c0(c));
+    STKG_CUDA_CHECK(cudaEventRecord(ev_x[c], h.s_hi));
+  };
+  try {
+    // host enqueue order keeps every event record ahead of its waits
+    C1(0);
+    X(0);
+    if (K > 1) C1(1);
+    for (int c = 1; c < K; ++c) {
+      X(c);
+      if (c + 1 < K) C1(c + 1);
+      C2(c - 1);
+    }
+    C2(K - 1);
+  } catch (...) {
+    h.run_stream = nullptr;
+    h.run_ticket = nullptr;
+    throw;
+  }
+  h.run_stream = nullptr;
+  h.run_ticket = nullptr;
+  STKG_CUDA_CHECK(cudaEventRecord(ev_lo, h.s_lo));
+  STKG_CUDA_CHECK(cudaEventRecord(ev_hi, h.s_hi));
+  STKG_CUDA_CHECK(cudaStreamWaitEvent(h.stream, ev_lo, 0));
+  STKG_CUDA_CHECK(cudaStreamWaitEvent(h.stream, ev_hi, 0));
+}
+
+}  // namespace
+
+namespace {
 // Full solve of ntc time slices starting at l0 (carry holds y_{l0-1} when l0 > 0), P1_DST
 // 2D/3D plans (h.pitch > 0).  Every intermediate lives in S in the padded layout (fastest
 // axis at pitch N = n + 1, pad entries zero), so that the strided passes run the 16-byte
@@ -539,17 +656,23 @@ void run_chunk_padded(stkg_heat& h, const double* F, double* U, double* S, int64
     ProfScope ps(h, 0);
     dst_half_pass(h, a, S, S, inner, outer, 0, 0, true);
   };
+  int64_t inner0 = P;  // columns of axis 0
+  for (int b = 1; b < last; ++b) inner0 *= h.n[b];
+  const bool fused = use_fused_axis0(h, inner0);
+  if (fused && d == 2 && !h.prof_on && overlap_chunks() > 1 &&
+      ntc >= 8 * overlap_chunks() && inner0 / fused_tile_cols(h.n[0]) < num_sms()) {
+    run_chunk_padded_overlap(h, F, U, S, l0, ntc, overlap_chunks(), inner0);
+    return;
+  }
   {
     ProfScope ps(h, 0);
     dst_half_pass(h, last, F, S, 1, lines, nl, P);
   }
-  int64_t inner0 = P;  // columns of axis 0
-  for (int b = 1; b < last; ++b) inner0 *= h.n[b];
-  if (use_fused_axis0(h, inner0)) {
+  if (fused) {
     // axes last-1 .. 1 forward, then axis 0 forward + recurrence + inverse marching in time
     for (int a = last - 1; a >= 1; --a) strided(a);
     {
-      ProfScope ps(h, 0);
+      ProfScope ps(h, 1);  // the fused pass runs the modal recurrence (class 1)
       fused_axis0(h, S, inner0, ntc, l0);
     }
     for (int a = 1; a < last; ++a) strided(a);
@@ -1030,6 +1153,10 @@ int stkg_heat_destroy(stkg_heat* h) {
       if (h->ev_d2h[b]) cudaEventDestroy(h->ev_d2h[b]);
     }
     if (h->s_h2d) cudaStreamDestroy(h->s_h2d);
+    if (h->s_hi) cudaStreamSynchronize(h->s_hi), cudaStreamDestroy(h->s_hi);
+    if (h->s_lo) cudaStreamSynchronize(h->s_lo), cudaStreamDestroy(h->s_lo);
+    for (auto e : h->ov_ev) cudaEventDestroy(e);
+    if (h->tickets) cudaFree(h->tickets);
     if (h->s_d2h) cudaStreamDestroy(h->s_d2h);
     delete h;
   });

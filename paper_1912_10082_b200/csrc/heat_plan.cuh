@@ -80,6 +80,14 @@ struct stkg_heat {
   DevBuf pf[2], pu[2], ps;
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
   cudaEvent_t ev_h2d[2] = {}, ev_comp[2] = {}, ev_d2h[2] = {};
+  // overlapped 2D schedule (run_chunk_padded_overlap): launch-stream / work-ticket overrides
+  // read by the DST launchers, high / low priority streams, per-chunk events
+  mutable cudaStream_t run_stream = nullptr;
+  mutable unsigned long long* run_ticket = nullptr;
+  cudaStream_t s_hi = nullptr, s_lo = nullptr;
+  std::vector<cudaEvent_t> ov_ev;
+  unsigned long long* tickets = nullptr;
+  int tickets_n = 0;
   // kernel-class profiling (stkg_heat_profile)
   bool prof_on = false;
   std::vector<cudaEvent_t> prof_ev[2];  // begin/end pairs per class

@@ -264,7 +264,9 @@ class HeatPlan:
         check(lib.stkg_heat_profile(self._h, 1, None, None))
 
     def profile_end(self):
-        """-> {"transform": (ms, launches), "scan": (ms, launches)} since profile_begin."""
+        """-> {"transform": (ms, launches), "scan": (ms, launches)} since profile_begin:
+        class "transform" = transform-only passes, "scan" = kernels that run the modal
+        recurrence (the scan kernel, or the fused axis-0 pass)."""
         ms = (C.c_double * 2)()
         n = (C.c_int64 * 2)()
         check(lib.stkg_heat_profile(self._h, 0, ms, n))
