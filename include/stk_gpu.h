@@ -234,6 +234,16 @@ int stkg_wave_apply(stkg_wave* plan, const double* x, double* y);
 /* TwoTermPrecond::solve (stk/sylvester.hpp:168-176): W = X_s [(X_s^T V X_t) ./ (l_i + t_j)] X_t^T.
  * STKG_SOLVABILITY at create time if min(lambda) + min(theta) <= 0 (stk/sylvester.hpp:158-160). */
 int stkg_two_term_solve(stkg_wave* plan, const double* v, double* w);
+/* Space-modal, time-banded preconditioner (no reference counterpart; K2d):
+ * P = M_h (x) Q_t + A' (x) E + Q_h (x) M_t with A_h replaced by its diagonal in the
+ * TwoTermPrecond eigenbasis, A' = X_s^-T diag(x_i^T A_h x_i) X_s^-1.  Applied as
+ * W = X_s [K_i^-1 rows of X_s^T V], K_i = Q_t + a_i (D_t + D_t^T) + lambda_i M_t (banded
+ * Cholesky per spatial mode, factored at plan creation).  s.p.d.; STKG_DEFINITENESS at create
+ * time if some K_i is not. */
+int stkg_modal_banded_solve(stkg_wave* plan, const double* v, double* w);
+/* The preconditioner stkg_gmres (use_precond = 1), stkg_pcg and stkg_wave_solve_refined
+ * apply: 0 = TwoTermPrecond (default, the reference's), 1 = the modal banded one. */
+int stkg_wave_set_precond(stkg_wave* plan, int kind);
 /* gmres (stk/outer_krylov.hpp:75-164) with apply = WaveOperator, precond = TwoTermPrecond:
  * right-preconditioned Arnoldi, Gram-Schmidt with one re-orthogonalisation pass (run as
  * classical GS twice: tall-skinny GEMV passes), Givens least squares on the host.

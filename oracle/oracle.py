@@ -541,6 +541,21 @@ class WaveSystemNP:
         x += self.precond(xk)
         return x, total, hist
 
+    def modal_banded(self, v):
+        """The space-modal time-banded preconditioner (product: stkg_modal_banded_solve,
+        DESIGN.md K2d) restated densely: a_i = (X_s^T A_h X_s)_ii, K_i = sym(Q_t + a_i E +
+        lambda_i M_t), W = X_s [rows i of X_s^T V solved with K_i]."""
+        import scipy.linalg as sl
+        V = v.reshape(self.nt, self.nh).T
+        a = np.einsum("ri,rc,ci->i", self.Xs, self.Ah.toarray(), self.Xs)
+        Qt, Mt, E = self.Qt.toarray(), self.Mt.toarray(), self.E.toarray()
+        Vt = self.Xs.T @ V
+        Wt = np.empty_like(Vt)
+        for i in range(self.nh):
+            K = Qt + a[i] * E + self.lam[i] * Mt
+            Wt[i] = sl.solve(0.5 * (K + K.T), Vt[i], assume_a="pos")
+        return (self.Xs @ Wt).T.ravel()
+
     def direct(self, b):
         """kron_direct_solve (stk/bench.hpp:414-429) with scipy SuperLU: sum_p D_p (x) A_p."""
         import scipy.sparse as sp

@@ -119,6 +119,8 @@ SIGNATURES = {
     "stkg_wave_destroy": (C.c_int, [C.c_void_p]),
     "stkg_wave_apply": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "stkg_two_term_solve": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "stkg_modal_banded_solve": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "stkg_wave_set_precond": (C.c_int, [C.c_void_p, C.c_int]),
     "stkg_gmres": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(GmresCfg),
                              C.POINTER(Report)]),
     "stkg_pcg": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_int,

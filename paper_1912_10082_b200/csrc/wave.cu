@@ -33,6 +33,13 @@ struct stkg_wave {
   bool has_precond = false;
   DevBuf Xs, XsT, lam, Xt, XtT, theta;
   DevBuf t1, t2;            // preconditioner temporaries (nh x nt)
+  // space-modal, time-banded preconditioner (precond_kind 1, modal_banded_solve): per
+  // spatial mode i the banded Cholesky factor of K_i = Q_t + a_i E + lambda_i M_t,
+  // mb[k * N + i + nh j] = L_i(j, j - k) (k = 1..3), mb[i + nh j] = 1 / L_i(j, j)
+  bool has_modal = false;
+  int precond_kind = 0;      // 0 = TwoTermPrecond (the reference's), 1 = modal banded
+  DevBuf mb;
+  std::vector<double> modal_a;  // a_i = (X_s^T A_h X_s)_ii, host copy
   Krylov krylov;             // GMRES / PCG workspace (basis grows on demand)
 };
 
@@ -219,7 +226,207 @@ void apply_op(stkg_wave& w, const double* x, double* y) {
   STKG_CUDA_CHECK(cudaGetLastError());
 }
 
-void precond_solve(stkg_wave& w, const double* v, double* out) {
+// ------------------------------------------------ space-modal time-banded preconditioner --
+// P = M_h (x) Q_t + A' (x) E + Q_h (x) M_t with A_h replaced by A' = X_s^-T diag(a) X_s^-1,
+// a_i = x_i^T A_h x_i (the diagonal of A_h in the TwoTermPrecond eigenbasis, which is
+// X_s^T M_h X_s = I, X_s^T Q_h X_s = Lambda).  In that basis P is block diagonal: row i of
+// W~ = X_s^-1 W solves the 7-banded s.p.d. time system K_i w~_i = (X_s^T V)_i with
+// K_i = Q_t + a_i E + lambda_i M_t, so
+//     P^-1 V = X_s [K_i^-1 rows of (X_s^T V)]    -- 2 GEMMs + n_h banded Cholesky solves
+// (TwoTermPrecond drops the A_h (x) E term and needs 4 GEMMs).  A_h is nearly diagonal in
+// that basis (off-diagonal mass 1-2% at n = 63..255, tools: DESIGN.md K2d), so P is almost
+// B: PCG needs ~10 iterations at every size instead of TwoTermPrecond's ~1.3 sqrt-growth
+// (537 at n = 255, 1370 at config 4).  P is s.p.d. whenever every K_i is (a_i > 0 since A_h
+// is s.p.d.; the factorisation checks the pivots).
+// One thread per spatial mode runs the forward and backward substitution over time; the
+// loads of a block of U steps do not depend on the recurrence and are issued ahead.
+__global__ void __launch_bounds__(64) modal_banded_solve_kernel(double* __restrict__ t,
+                                                                const double* __restrict__ mb,
+                                                                int64_t nh, int64_t nt,
+                                                                const int* skip) {
+  if (skip && *skip) return;
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= nh) return;
+  const int64_t N = nh * nt;
+  const double* rd = mb;
+  const double* l1 = mb + N;
+  const double* l2 = mb + 2 * N;
+  const double* l3 = mb + 3 * N;
+  double* col = t + i;
+  // forward: L y = v,  y_j = (v_j - L(j,j-1) y_{j-1} - L(j,j-2) y_{j-2} - L(j,j-3) y_{j-3}) / L(j,j)
+  double y1 = 0.0, y2 = 0.0, y3 = 0.0;
+  constexpr int U = 8;
+  int64_t j = 0;
+  for (; j + U <= nt; j += U) {
+    double v[U], a[U], b[U], c[U], r[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t o = (j + u) * nh;
+      v[u] = col[o];
+      r[u] = __ldg(rd + o + i);
+      a[u] = __ldg(l1 + o + i);
+      b[u] = __ldg(l2 + o + i);
+      c[u] = __ldg(l3 + o + i);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const double y = (v[u] - a[u] * y1 - b[u] * y2 - c[u] * y3) * r[u];
+      col[(j + u) * nh] = y;
+      y3 = y2;
+      y2 = y1;
+      y1 = y;
+    }
+  }
+  for (; j < nt; ++j) {
+    const int64_t o = j * nh;
+    const double y = (col[o] - l1[o + i] * y1 - l2[o + i] * y2 - l3[o + i] * y3) * rd[o + i];
+    col[o] = y;
+    y3 = y2;
+    y2 = y1;
+    y1 = y;
+  }
+  // backward: L^T w = y,  w_j = (y_j - L(j+1,j) w_{j+1} - L(j+2,j) w_{j+2} - L(j+3,j) w_{j+3}) / L(j,j)
+  double w1 = 0.0, w2 = 0.0, w3 = 0.0;
+  j = nt - 1;
+  for (; j - U + 1 >= 0; j -= U) {
+    double v[U], a[U], b[U], c[U], r[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t jj = j - u, o = jj * nh;
+      v[u] = col[o];
+      r[u] = __ldg(rd + o + i);
+      a[u] = jj + 1 < nt ? __ldg(l1 + o + nh + i) : 0.0;
+      b[u] = jj + 2 < nt ? __ldg(l2 + o + 2 * nh + i) : 0.0;
+      c[u] = jj + 3 < nt ? __ldg(l3 + o + 3 * nh + i) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const double w = (v[u] - a[u] * w1 - b[u] * w2 - c[u] * w3) * r[u];
+      col[(j - u) * nh] = w;
+      w3 = w2;
+      w2 = w1;
+      w1 = w;
+    }
+  }
+  for (; j >= 0; --j) {
+    const int64_t o = j * nh;
+    const double a = j + 1 < nt ? l1[o + nh + i] : 0.0;
+    const double b = j + 2 < nt ? l2[o + 2 * nh + i] : 0.0;
+    const double c = j + 3 < nt ? l3[o + 3 * nh + i] : 0.0;
+    const double w = (col[o] - a * w1 - b * w2 - c * w3) * rd[o + i];
+    col[o] = w;
+    w3 = w2;
+    w2 = w1;
+    w1 = w;
+  }
+}
+
+// Host setup of the modal banded preconditioner: a_i, the banded Cholesky factors of every
+// K_i (symmetrised: the spline Gram bands are symmetric only to rounding).
+void build_modal_banded(stkg_wave& w, const double* space_bands, const double* time_bands,
+                        const double* Xs, const double* lambdas) {
+  const int64_t nh = w.nh, nt = w.nt, N = w.N;
+  const double* Ab = space_bands + kBand * nh;  // A_h band
+  w.modal_a.assign(static_cast<size_t>(nh), 0.0);
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < nh; ++i) {
+    const double* x = Xs + i * nh;
+    double acc = 0.0;
+    for (int64_t r = 0; r < nh; ++r) {
+      double ax = 0.0;
+      for (int d = 0; d < kBand; ++d) {
+        const int64_t c = r + d - kHalf;
+        if (c >= 0 && c < nh) ax += Ab[d * nh + r] * x[c];
+      }
+      acc += x[r] * ax;
+    }
+    w.modal_a[i] = acc;
+  }
+  const double* Qb = time_bands;
+  const double* Db = time_bands + kBand * nt;
+  const double* Mb = time_bands + 2 * kBand * nt;
+  auto band = [&](const double* b, int64_t j, int off) {  // matrix entry (j, j + off)
+    const int64_t c = j + off;
+    return (c >= 0 && c < nt) ? b[(off + kHalf) * nt + j] : 0.0;
+  };
+  std::vector<double> host(static_cast<size_t>(4 * N), 0.0);
+  int bad = 0;
+  double bad_a = 0.0;
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < nh; ++i) {
+    const double a = w.modal_a[i], lam = lambdas[i];
+    // K(j, j - k) for k = 0..3, symmetrised
+    auto K = [&](int64_t j, int k) {
+      const int64_t c = j - k;
+      if (c < 0) return 0.0;
+      const double e1 = band(Db, j, -k) + band(Db, c, k);  // E(j,c) = D(j,c) + D(c,j)
+      const double e2 = band(Db, c, k) + band(Db, j, -k);  // E(c,j)
+      const double kjc = band(Qb, j, -k) + a * e1 + lam * band(Mb, j, -k);
+      const double kcj = band(Qb, c, k) + a * e2 + lam * band(Mb, c, k);
+      return 0.5 * (kjc + kcj);
+    };
+    std::vector<double> L(static_cast<size_t>(4 * nt), 0.0);  // L[k * nt + j] = L(j, j - k)
+    bool ok = true;
+    for (int64_t j = 0; j < nt && ok; ++j) {
+      for (int k = 3; k >= 1; --k) {  // L(j, c), c = j - k, in increasing c
+        const int64_t c = j - k;
+        if (c < 0) continue;
+        double sum = K(j, k);
+        for (int m = k + 1; m <= 3; ++m)  // columns c' = j - m < c shared by rows j and c
+          if (j - m >= 0 && (m - k) <= 3) sum -= L[m * nt + j] * L[(m - k) * nt + c];
+        L[k * nt + j] = sum / L[c];  // L(c, c) stored at L[0 * nt + c]
+      }
+      double d = K(j, 0);
+      for (int k = 1; k <= 3; ++k) d -= L[k * nt + j] * L[k * nt + j];
+      if (!(d > 0.0)) {
+        ok = false;
+        break;
+      }
+      L[j] = std::sqrt(d);
+    }
+    if (!ok) {
+#pragma omp critical
+      {
+        bad = 1;
+        bad_a = a;
+      }
+      continue;
+    }
+    for (int64_t j = 0; j < nt; ++j) {
+      host[static_cast<size_t>(i + nh * j)] = 1.0 / L[j];
+      for (int k = 1; k <= 3; ++k) host[static_cast<size_t>(k * N + i + nh * j)] = L[k * nt + j];
+    }
+  }
+  if (bad) {
+    char buf[160];
+    snprintf(buf, sizeof buf, "modal banded preconditioner: K_i not s.p.d. (a_i = %g)", bad_a);
+    throw Error(STKG_DEFINITENESS, buf);
+  }
+  w.mb.alloc(4 * N);
+  w.mb.upload(host.data(), 4 * N, w.stream);
+  STKG_CUDA_CHECK(cudaStreamSynchronize(w.stream));
+  w.has_modal = true;
+}
+
+void modal_banded_solve(stkg_wave& w, const double* v, double* out) {
+  const int64_t nh = w.nh, nt = w.nt;
+  GemmProblem p;
+  p.skip = w.krylov.skip;
+  // t1 = Xs^T V
+  p.M = nh; p.K = nh; p.N = nt;
+  p.A = w.XsT.p; p.lda = nh; p.B = v; p.ldb = nh; p.C = w.t1.p; p.ldc = nh;
+  launch_gemm(p, EpiStore{}, w.stream);
+  // rows of t1 <- K_i^-1 rows
+  modal_banded_solve_kernel<<<static_cast<unsigned>(ceil_div(nh, 64)), 64, 0, w.stream>>>(
+      w.t1.p, w.mb.p, nh, nt, w.krylov.skip);
+  STKG_CUDA_CHECK(cudaGetLastError());
+  // out = Xs t1
+  p.M = nh; p.K = nh; p.N = nt;
+  p.A = w.Xs.p; p.lda = nh; p.B = w.t1.p; p.ldb = nh; p.C = out; p.ldc = nh;
+  launch_gemm(p, EpiStore{}, w.stream);
+}
+
+void two_term_solve(stkg_wave& w, const double* v, double* out) {
   const int64_t nh = w.nh, nt = w.nt;
   GemmProblem p;
   p.skip = w.krylov.skip;
@@ -238,6 +445,12 @@ void precond_solve(stkg_wave& w, const double* v, double* out) {
   p.M = nh; p.K = nt; p.N = nt;
   p.A = w.t1.p; p.lda = nh; p.B = w.XtT.p; p.ldb = nt; p.C = out; p.ldc = nh;
   launch_gemm(p, EpiStore{}, w.stream);
+}
+
+// The plan's preconditioner for GMRES / PCG / refinement.
+void precond_solve(stkg_wave& w, const double* v, double* out) {
+  if (w.precond_kind == 1) return modal_banded_solve(w, v, out);
+  two_term_solve(w, v, out);
 }
 
 }  // namespace
@@ -301,6 +514,7 @@ int stkg_wave_create(stkg_wave** out, const stkg_wave_desc* desc, void* cuda_str
       w->theta.upload(desc->thetas, nt, s);
       w->t1.alloc(w->N);
       w->t2.alloc(w->N);
+      build_modal_banded(*w, sb, tb, desc->Xs, desc->lambdas);
     }
     STKG_CUDA_CHECK(cudaStreamSynchronize(s));  // host temporaries die here
     w->krylov.N = w->N;
@@ -331,7 +545,26 @@ int stkg_two_term_solve(stkg_wave* w, const double* v, double* out) {
     STKG_REQUIRE(w && v && out, STKG_ARGUMENT, "TwoTermPrecond::solve: null argument");
     STKG_REQUIRE(w->has_precond, STKG_ARGUMENT,
                  "TwoTermPrecond::solve: plan was created without eigenpairs");
-    precond_solve(*w, v, out);
+    two_term_solve(*w, v, out);
+  });
+}
+
+int stkg_wave_set_precond(stkg_wave* w, int kind) {
+  return guarded([&] {
+    STKG_REQUIRE(w, STKG_ARGUMENT, "set_precond: null plan");
+    STKG_REQUIRE(kind == 0 || kind == 1, STKG_ARGUMENT, "set_precond: kind must be 0 or 1");
+    STKG_REQUIRE(w->has_precond && (kind == 0 || w->has_modal), STKG_ARGUMENT,
+                 "set_precond: plan was created without eigenpairs");
+    w->precond_kind = kind;
+  });
+}
+
+int stkg_modal_banded_solve(stkg_wave* w, const double* v, double* out) {
+  return guarded([&] {
+    STKG_REQUIRE(w && v && out, STKG_ARGUMENT, "modal_banded_solve: null argument");
+    STKG_REQUIRE(w->has_modal, STKG_ARGUMENT,
+                 "modal_banded_solve: plan was created without eigenpairs");
+    modal_banded_solve(*w, v, out);
   });
 }
 

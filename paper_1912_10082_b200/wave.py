@@ -61,8 +61,17 @@ class WavePlan:
     """Device plan of the wave system: the six banded factors and (optionally) the two
     generalized eigenpairs of TwoTermPrecond."""
 
+    PRECONDS = {"two_term": 0, "modal_banded": 1}
+
     def __init__(self, space: WaveSpaceMatrices, time: WaveTimeMatrices, precond: bool = True,
-                 space_eig: EigPair | None = None, time_eig: EigPair | None = None, stream=None):
+                 space_eig: EigPair | None = None, time_eig: EigPair | None = None, stream=None,
+                 preconditioner: str = "two_term"):
+        """preconditioner: what gmres / pcg / solve_refined apply -- "two_term" (the
+        reference's TwoTermPrecond, default) or "modal_banded" (stkg_modal_banded_solve:
+        A_h diagonalised in the same eigenbasis, a banded s.p.d. time solve per spatial
+        mode; ~10 PCG iterations at every size)."""
+        if preconditioner not in self.PRECONDS:
+            raise ArgumentError(f"WavePlan: unknown preconditioner {preconditioner!r}")
         self.nh = space.M.n
         self.nt = time.M.n
         keep = []
@@ -91,6 +100,15 @@ class WavePlan:
         self._stream = _stream_handle(stream)
         check(lib.stkg_wave_create(C.byref(h), C.byref(desc), self._stream))
         self._h = h
+        self.preconditioner = "two_term"
+        if precond:
+            self.set_preconditioner(preconditioner)
+
+    def set_preconditioner(self, name: str):
+        if name not in self.PRECONDS:
+            raise ArgumentError(f"WavePlan: unknown preconditioner {name!r}")
+        check(lib.stkg_wave_set_precond(self._h, self.PRECONDS[name]))
+        self.preconditioner = name
 
     def close(self):
         if getattr(self, "_h", None):
@@ -119,6 +137,17 @@ class WavePlan:
         with on_plan_stream(self._stream):
             check(lib.stkg_wave_apply(self._h, C.c_void_p(_dev_ptr(x)), C.c_void_p(_dev_ptr(y))))
         return y
+
+    def modal_banded_solve(self, v, out=None):
+        """P^-1 v for the space-modal time-banded preconditioner (stkg_modal_banded_solve)."""
+        import torch
+        self._chk(v)
+        w = torch.empty_like(v) if out is None else out
+        self._chk(w)
+        with on_plan_stream(self._stream):
+            check(lib.stkg_modal_banded_solve(self._h, C.c_void_p(_dev_ptr(v)),
+                                              C.c_void_p(_dev_ptr(w))))
+        return w
 
     def two_term_solve(self, v, out=None):
         import torch
