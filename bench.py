@@ -572,21 +572,85 @@ def rksm_leg(stk, inputs, with_cpu=True, name="cfg1"):
     return out
 
 
+def _event_ms(stream, fn, reps):
+    import torch
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    fn()
+    e0.record(stream)
+    for _ in range(reps):
+        fn()
+    e1.record(stream)
+    stream.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
 def wave_leg(stk, inputs, with_cpu=True, cpu_iters=10):
-    """SURVEY 8(a) rows a8-a10 on BASELINE config 4 (1D wave, cubic splines, 1023 x 1025):
-    the reference's GMRES + TwoTermPrecond for a fixed 300-iteration budget and the PCG
-    performance path, timed on the device; the reference-faithful oracle GMRES (numpy +
-    multithreaded BLAS) timed per iteration on the host for a bounded number of iterations."""
+    """SURVEY 8(a) rows a8-a10 on BASELINE config 4 (1D wave, cubic splines, 1023 x 1025).
+    Headline: PCG with the space-modal time-banded preconditioner (stkg_modal_banded_solve)
+    to 1e-7, and the double-double refined solve to the north_star 1e-10 bar.  Beside it the
+    reference's preconditioner (TwoTermPrecond): PCG to 1e-7 and the reference's GMRES for a
+    fixed 300-iteration budget.  The reference-faithful oracle GMRES (numpy + multithreaded
+    BLAS) is timed per iteration on the host for a bounded number of iterations."""
     import torch
     cfg = inputs.CONFIGS["cfg4"]
     sm = stk.wave_space_matrices(stk.SpaceGrid1D(0.0, 1.0, cfg.nh))
     tm = stk.wave_time_matrices(stk.TimeGrid(cfg.nt, 1.0))
-    plan = stk.WavePlan(sm, tm)
+    plan = stk.WavePlan(sm, tm, preconditioner="modal_banded")
     Fh = inputs.wave_rhs_host(cfg)
     F = torch.tensor(Fh, device="cuda")
-    # warm-up: sizes the 301-column Krylov basis (gmres_run reserves maxit + 1 columns up
-    # front) and exits after the first iteration, so no allocation lands in the timed run
-    plan.gmres(F, stk.GmresConfig(tol=0.999, maxit=300))
+    N = cfg.nh * (cfg.nt + 1)
+    stream = torch.cuda.current_stream()
+    # --- headline: modal banded preconditioner
+    plan.pcg(F, tol=1e-7, maxit=500)  # warm-up (sizes the Krylov workspace)
+    torch.cuda.synchronize()
+    reps = 5
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        _, rm = plan.pcg(F, tol=1e-7, maxit=500)
+    torch.cuda.synchronize()
+    tm_ = (time.perf_counter() - t0) / reps
+    plan.solve_refined(F, tol=1e-10, inner_tol=1e-6, max_refine=6)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        _, _, rr = plan.solve_refined(F, tol=1e-10, inner_tol=1e-6, max_refine=6)
+    torch.cuda.synchronize()
+    tr = (time.perf_counter() - t0) / reps
+    w = torch.empty_like(F)
+    y = torch.empty_like(F)
+    ms_prec = _event_ms(stream, lambda: plan.modal_banded_solve(F, out=w), 20)
+    ms_tt = _event_ms(stream, lambda: plan.two_term_solve(F, out=w), 20)
+    ms_op = _event_ms(stream, lambda: plan.apply(F, out=y), 20)
+    # 2 GEMMs of 2 nh^2 nt flop + 2 banded triangular solves (~14 flop/unknown) + operator
+    fl_prec = 2 * 2.0 * cfg.nh * cfg.nh * (cfg.nt + 1) + 14.0 * N
+    fl_iter = fl_prec + 84.0 * N
+    out = {"workload": cfg.name, "unknowns": N,
+           "pcg": {"preconditioner": "modal_banded", "iterations": rm.iterations,
+                   "final_relres": rm.final_relres, "tol": 1e-7, "s": tm_,
+                   "ms_per_iteration": 1e3 * tm_ / max(rm.iterations, 1),
+                   "unknowns_per_s": N / tm_,
+                   "roofline": {"bound": "tensor", "flop_per_iteration": fl_iter,
+                                "roof_ms_per_iteration": 1e3 * fl_iter / (FP64_PEAK_TFLOPS * 1e12),
+                                "peak": FP64_PEAK_TFLOPS, "peak_source": FP64_PEAK_SOURCE,
+                                "frac": (1e3 * fl_iter / (FP64_PEAK_TFLOPS * 1e12))
+                                / (1e3 * tm_ / max(rm.iterations, 1)),
+                                "basis": "2 DMMA GEMMs + 2 banded solves per spatial mode "
+                                         "(stkg_modal_banded_solve) + the banded WaveOperator "
+                                         "per iteration; wall clock incl. the host "
+                                         "convergence checks"}},
+           "refined_dd": {"tol": 1e-10, "rounds": len(rr.rel_res_history) - 1,
+                          "pcg_iterations": rr.iterations, "final_relres_dd": rr.final_relres,
+                          "history": rr.rel_res_history, "converged": rr.converged, "s": tr,
+                          "unknowns_per_s": N / tr,
+                          "note": "mixed-precision iterative refinement, residual in "
+                                  "double-double (stkg_wave_solve_refined), modal banded "
+                                  "preconditioner"},
+           "kernels_ms": {"modal_banded_solve": ms_prec, "two_term_solve": ms_tt,
+                          "wave_apply": ms_op,
+                          "modal_banded_tflops": fl_prec / (ms_prec / 1e3) / 1e12}}
+    # --- the reference's preconditioner (TwoTermPrecond)
+    plan.set_preconditioner("two_term")
+    plan.gmres(F, stk.GmresConfig(tol=0.999, maxit=300))  # sizes the 301-column basis
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     _, rg = plan.gmres(F, stk.GmresConfig(tol=1e-9, maxit=300))
@@ -596,31 +660,19 @@ def wave_leg(stk, inputs, with_cpu=True, cpu_iters=10):
     _, rp = plan.pcg(F, tol=1e-7, maxit=6000)
     torch.cuda.synchronize()
     tp = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    _, _, rr = plan.solve_refined(F, tol=1e-10, inner_tol=1e-6, max_refine=6)
-    torch.cuda.synchronize()
-    tr = time.perf_counter() - t0
-    N = cfg.nh * (cfg.nt + 1)
-    out = {"workload": cfg.name, "unknowns": N,
-           "refined_dd": {"tol": 1e-10, "rounds": len(rr.rel_res_history) - 1,
-                          "pcg_iterations": rr.iterations, "final_relres_dd": rr.final_relres,
-                          "history": rr.rel_res_history, "converged": rr.converged, "s": tr,
-                          "note": "mixed-precision iterative refinement, residual in "
-                                  "double-double (stkg_wave_solve_refined)"},
-           "gmres": {"iterations": rg.iterations, "final_relres": rg.final_relres,
-                     "s": tg, "ms_per_iteration": 1e3 * tg / max(rg.iterations, 1)},
-           "pcg": {"iterations": rp.iterations, "final_relres": rp.final_relres, "tol": 1e-7,
-                   "s": tp, "ms_per_iteration": 1e3 * tp / max(rp.iterations, 1),
-                   "unknowns_per_s": N / tp}}
     fl = WAVE_FLOP_PER_PCG_ITER(cfg.nh, cfg.nt + 1)
     roof_ms = 1e3 * fl / (FP64_PEAK_TFLOPS * 1e12)
-    out["pcg"]["roofline"] = {"bound": "tensor", "flop_per_iteration": fl,
-                              "roof_ms_per_iteration": roof_ms, "peak": FP64_PEAK_TFLOPS,
-                              "peak_source": FP64_PEAK_SOURCE,
-                              "frac": roof_ms / out["pcg"]["ms_per_iteration"],
-                              "basis": "4 DMMA GEMMs of TwoTermPrecond::solve + the banded "
-                                       "WaveOperator per iteration (wall clock incl. the "
-                                       "per-chunk host convergence checks)"}
+    out["two_term"] = {
+        "gmres": {"iterations": rg.iterations, "final_relres": rg.final_relres,
+                  "s": tg, "ms_per_iteration": 1e3 * tg / max(rg.iterations, 1)},
+        "pcg": {"iterations": rp.iterations, "final_relres": rp.final_relres, "tol": 1e-7,
+                "s": tp, "ms_per_iteration": 1e3 * tp / max(rp.iterations, 1),
+                "unknowns_per_s": N / tp,
+                "roofline": {"bound": "tensor", "flop_per_iteration": fl,
+                             "roof_ms_per_iteration": roof_ms,
+                             "frac": roof_ms / (1e3 * tp / max(rp.iterations, 1)),
+                             "basis": "4 DMMA GEMMs of TwoTermPrecond::solve + the banded "
+                                      "WaveOperator per iteration"}}}
     if with_cpu:
         sys.path.insert(0, str(ROOT))
         from oracle import oracle as orc
@@ -636,7 +688,8 @@ def wave_leg(stk, inputs, with_cpu=True, cpu_iters=10):
                                    "cores": os.cpu_count(), "kind": "port",
                                    "sample": f"{its} reference-faithful GMRES iterations "
                                              "(numpy/scipy, MGS + re-orth, dense eigenbasis "
-                                             "preconditioner) on the full config-4 system"}
+                                             "TwoTermPrecond) on the full config-4 system"}
+    plan.close()
     return out
 
 
@@ -755,11 +808,15 @@ def run_ours(args):
         if "wave" in line:
             wv = line["wave"]
             cfgs["cfg4"] = {"workload": wv["workload"], "unknowns": wv["unknowns"],
+                            "solve_s_1e-7": wv["pcg"]["s"],
+                            "value": wv["pcg"]["unknowns_per_s"],
                             "pcg_ms_per_iteration": wv["pcg"]["ms_per_iteration"],
                             "pcg_iterations_1e-7": wv["pcg"]["iterations"],
                             "roofline": wv["pcg"]["roofline"],
                             "refined_dd_relres": wv["refined_dd"]["final_relres_dd"],
                             "refined_s": wv["refined_dd"]["s"],
+                            "two_term_pcg_iterations_1e-7": wv["two_term"]["pcg"]["iterations"],
+                            "two_term_pcg_s": wv["two_term"]["pcg"]["s"],
                             "cpu_baseline": wv.get("cpu_oracle_gmres")}
         line["configs"] = dict(sorted(cfgs.items()))
     if rank == 0 and world == 1 and not args.no_cpu:

@@ -240,7 +240,12 @@ void apply_op(stkg_wave& w, const double* x, double* y) {
 // is s.p.d.; the factorisation checks the pivots).
 // One thread per spatial mode runs the forward and backward substitution over time; the
 // loads of a block of U steps do not depend on the recurrence and are issued ahead.
-__global__ void __launch_bounds__(64) modal_banded_solve_kernel(double* __restrict__ t,
+template <int U>
+struct BandBlock {  // one block of U steps of a mode's substitution: operands only
+  double v[U], r[U], a[U], b[U], c[U];
+};
+
+__global__ void __launch_bounds__(32) modal_banded_solve_kernel(double* __restrict__ t,
                                                                 const double* __restrict__ mb,
                                                                 int64_t nh, int64_t nt,
                                                                 const int* skip) {
@@ -248,38 +253,47 @@ __global__ void __launch_bounds__(64) modal_banded_solve_kernel(double* __restri
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= nh) return;
   const int64_t N = nh * nt;
-  const double* rd = mb;
-  const double* l1 = mb + N;
-  const double* l2 = mb + 2 * N;
-  const double* l3 = mb + 3 * N;
+  const double* rd = mb + i;
+  const double* l1 = mb + N + i;
+  const double* l2 = mb + 2 * N + i;
+  const double* l3 = mb + 3 * N + i;
   double* col = t + i;
-  // forward: L y = v,  y_j = (v_j - L(j,j-1) y_{j-1} - L(j,j-2) y_{j-2} - L(j,j-3) y_{j-3}) / L(j,j)
-  double y1 = 0.0, y2 = 0.0, y3 = 0.0;
   constexpr int U = 8;
-  int64_t j = 0;
-  for (; j + U <= nt; j += U) {
-    double v[U], a[U], b[U], c[U], r[U];
+  const int64_t nb = nt / U;  // full blocks; the remainder runs unpipelined
+  // forward: L y = v,  y_j = (v_j - L(j,j-1) y_{j-1} - L(j,j-2) y_{j-2} - L(j,j-3) y_{j-3}) / L(j,j)
+  // The operands of block k+1 are loaded while block k's dependent chain runs (the chain
+  // is two FP64 ops per step; unpipelined, every block waited a full L2 round trip).
+  auto load_fwd = [&](int64_t k, BandBlock<U>& B) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int64_t o = (j + u) * nh;
-      v[u] = col[o];
-      r[u] = __ldg(rd + o + i);
-      a[u] = __ldg(l1 + o + i);
-      b[u] = __ldg(l2 + o + i);
-      c[u] = __ldg(l3 + o + i);
+      const int64_t o = (k * U + u) * nh;
+      B.v[u] = col[o];
+      B.r[u] = __ldg(rd + o);
+      B.a[u] = __ldg(l1 + o);
+      B.b[u] = __ldg(l2 + o);
+      B.c[u] = __ldg(l3 + o);
     }
+  };
+  double y1 = 0.0, y2 = 0.0, y3 = 0.0;
+  {
+    BandBlock<U> cur, nxt;
+    if (nb > 0) load_fwd(0, cur);
+    for (int64_t k = 0; k < nb; ++k) {
+      if (k + 1 < nb) load_fwd(k + 1, nxt);
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const double y = (v[u] - a[u] * y1 - b[u] * y2 - c[u] * y3) * r[u];
-      col[(j + u) * nh] = y;
-      y3 = y2;
-      y2 = y1;
-      y1 = y;
+      for (int u = 0; u < U; ++u) {
+        const double y = (fma(-cur.c[u], y3, fma(-cur.b[u], y2, cur.v[u])) - cur.a[u] * y1) * cur.r[u];
+        col[(k * U + u) * nh] = y;
+        y3 = y2;
+        y2 = y1;
+        y1 = y;
+      }
+      cur = nxt;
     }
   }
-  for (; j < nt; ++j) {
+  for (int64_t j = nb * U; j < nt; ++j) {
     const int64_t o = j * nh;
-    const double y = (col[o] - l1[o + i] * y1 - l2[o + i] * y2 - l3[o + i] * y3) * rd[o + i];
+    const double y = (fma(-l3[o], y3, fma(-l2[o], y2, col[o])) - l1[o] * y1) * rd[o];
     col[o] = y;
     y3 = y2;
     y2 = y1;
@@ -287,37 +301,44 @@ __global__ void __launch_bounds__(64) modal_banded_solve_kernel(double* __restri
   }
   // backward: L^T w = y,  w_j = (y_j - L(j+1,j) w_{j+1} - L(j+2,j) w_{j+2} - L(j+3,j) w_{j+3}) / L(j,j)
   double w1 = 0.0, w2 = 0.0, w3 = 0.0;
-  j = nt - 1;
-  for (; j - U + 1 >= 0; j -= U) {
-    double v[U], a[U], b[U], c[U], r[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t jj = j - u, o = jj * nh;
-      v[u] = col[o];
-      r[u] = __ldg(rd + o + i);
-      a[u] = jj + 1 < nt ? __ldg(l1 + o + nh + i) : 0.0;
-      b[u] = jj + 2 < nt ? __ldg(l2 + o + 2 * nh + i) : 0.0;
-      c[u] = jj + 3 < nt ? __ldg(l3 + o + 3 * nh + i) : 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const double w = (v[u] - a[u] * w1 - b[u] * w2 - c[u] * w3) * r[u];
-      col[(j - u) * nh] = w;
-      w3 = w2;
-      w2 = w1;
-      w1 = w;
-    }
-  }
-  for (; j >= 0; --j) {
+  const int64_t rem = nt - nb * U;  // the top rows (j >= nb U) first, unpipelined
+  for (int64_t j = nt - 1; j >= nt - rem; --j) {
     const int64_t o = j * nh;
-    const double a = j + 1 < nt ? l1[o + nh + i] : 0.0;
-    const double b = j + 2 < nt ? l2[o + 2 * nh + i] : 0.0;
-    const double c = j + 3 < nt ? l3[o + 3 * nh + i] : 0.0;
-    const double w = (col[o] - a * w1 - b * w2 - c * w3) * rd[o + i];
+    const double a = j + 1 < nt ? l1[o + nh] : 0.0;
+    const double b = j + 2 < nt ? l2[o + 2 * nh] : 0.0;
+    const double c = j + 3 < nt ? l3[o + 3 * nh] : 0.0;
+    const double w = (fma(-c, w3, fma(-b, w2, col[o])) - a * w1) * rd[o];
     col[o] = w;
     w3 = w2;
     w2 = w1;
     w1 = w;
+  }
+  auto load_bwd = [&](int64_t k, BandBlock<U>& B) {  // block k = rows k U + U - 1 .. k U
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t j = k * U + U - 1 - u, o = j * nh;
+      B.v[u] = col[o];
+      B.r[u] = __ldg(rd + o);
+      B.a[u] = j + 1 < nt ? __ldg(l1 + o + nh) : 0.0;
+      B.b[u] = j + 2 < nt ? __ldg(l2 + o + 2 * nh) : 0.0;
+      B.c[u] = j + 3 < nt ? __ldg(l3 + o + 3 * nh) : 0.0;
+    }
+  };
+  {
+    BandBlock<U> cur, nxt;
+    if (nb > 0) load_bwd(nb - 1, cur);
+    for (int64_t k = nb - 1; k >= 0; --k) {
+      if (k > 0) load_bwd(k - 1, nxt);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const double w = (fma(-cur.c[u], w3, fma(-cur.b[u], w2, cur.v[u])) - cur.a[u] * w1) * cur.r[u];
+        col[(k * U + U - 1 - u) * nh] = w;
+        w3 = w2;
+        w2 = w1;
+        w1 = w;
+      }
+      cur = nxt;
+    }
   }
 }
 
@@ -417,7 +438,7 @@ void modal_banded_solve(stkg_wave& w, const double* v, double* out) {
   p.A = w.XsT.p; p.lda = nh; p.B = v; p.ldb = nh; p.C = w.t1.p; p.ldc = nh;
   launch_gemm(p, EpiStore{}, w.stream);
   // rows of t1 <- K_i^-1 rows
-  modal_banded_solve_kernel<<<static_cast<unsigned>(ceil_div(nh, 64)), 64, 0, w.stream>>>(
+  modal_banded_solve_kernel<<<static_cast<unsigned>(ceil_div(nh, 32)), 32, 0, w.stream>>>(
       w.t1.p, w.mb.p, nh, nt, w.krylov.skip);
   STKG_CUDA_CHECK(cudaGetLastError());
   // out = Xs t1
