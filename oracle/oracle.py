@@ -556,6 +556,16 @@ class WaveSystemNP:
             Wt[i] = sl.solve(0.5 * (K + K.T), Vt[i], assume_a="pos")
         return (self.Xs @ Wt).T.ravel()
 
+    def modal_banded_apply(self, w):
+        """P w for the modal banded preconditioner's operator (the wave operator with A_h
+        replaced by A' = M_h X_s diag(a) X_s^T M_h): the backward-error check of P^-1."""
+        U = w.reshape(self.nt, self.nh).T
+        a = np.einsum("ri,rc,ci->i", self.Xs, self.Ah.toarray(), self.Xs)
+        MX = self.Mh @ self.Xs
+        Ap = (MX * a[None, :]) @ MX.T
+        out = (self.Mh @ U) @ self.Qt.T + (Ap @ U) @ self.E + (self.Qh @ U) @ self.Mt
+        return out.T.ravel()
+
     def direct(self, b):
         """kron_direct_solve (stk/bench.hpp:414-429) with scipy SuperLU: sum_p D_p (x) A_p."""
         import scipy.sparse as sp

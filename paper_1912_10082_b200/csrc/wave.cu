@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <memory>
 #include <string>
 #include <vector>
@@ -342,6 +343,156 @@ __global__ void __launch_bounds__(32) modal_banded_solve_kernel(double* __restri
   }
 }
 
+// Parallel-in-time form of modal_banded_solve_kernel: a CTA of 32 x P threads takes 32
+// consecutive modes (lane = mode, coalesced) and cuts each mode's time axis into P chunks
+// (warp = chunk).  Each substitution is an order-3 linear recurrence on the state
+// s_j = (y_j, y_{j-1}, y_{j-2}); per direction:
+//   A  every chunk runs its rows from a zero state (giving e_c) and, in lockstep, the three
+//      homogeneous runs from unit states (the columns of the chunk's 3 x 3 transfer G_c);
+//   B  warp 0 chains the P chunks: s_in(c+1) = G_c s_in(c) + e_c;
+//   C  every chunk reruns its rows from its true incoming state and stores them.
+// The dependent chain per thread drops from 2 n_t steps to about 4 n_t / P, and the SM
+// holds P times more warps.  Same arithmetic per step as the sequential kernel in pass C;
+// the incoming states differ from the sequential ones only in rounding.
+template <int P>
+__global__ void __launch_bounds__(32 * P) modal_banded_solve_chunked_kernel(
+    double* __restrict__ t, const double* __restrict__ mb, int64_t nh, int64_t nt,
+    const int* skip) {
+  if (skip && *skip) return;
+  // per chunk and lane: e (3) and G columns (9); pass B overwrites e with the incoming state
+  __shared__ double sh[P][12][32];
+  const int lane = threadIdx.x & 31, c = threadIdx.x >> 5;
+  const int64_t i = int64_t(blockIdx.x) * 32 + lane;
+  const bool act = i < nh;
+  const int64_t N = nh * nt;
+  const int64_t ii = act ? i : 0;
+  const double* rd = mb + ii;
+  const double* l1 = mb + N + ii;
+  const double* l2 = mb + 2 * N + ii;
+  const double* l3 = mb + 3 * N + ii;
+  double* col = t + ii;
+  const int64_t L = (nt + P - 1) / P, j0 = c * L, j1 = j0 + L < nt ? j0 + L : nt;
+
+  // ---------------- forward: y_j = (v_j - l1 y_{j-1} - l2 y_{j-2} - l3 y_{j-3}) rd
+  {
+    double z[3] = {0, 0, 0}, g0[3] = {1, 0, 0}, g1[3] = {0, 1, 0}, g2[3] = {0, 0, 1};
+    for (int64_t j = j0; j < j1; ++j) {
+      const int64_t o = j * nh;
+      const double a = act ? __ldg(l1 + o) : 0.0, b = act ? __ldg(l2 + o) : 0.0;
+      const double cc = act ? __ldg(l3 + o) : 0.0, r = act ? __ldg(rd + o) : 0.0;
+      const double v = act ? col[o] : 0.0;
+      const double zn = (fma(-cc, z[2], fma(-b, z[1], v)) - a * z[0]) * r;
+      const double h0 = -(fma(cc, g0[2], fma(b, g0[1], a * g0[0]))) * r;
+      const double h1 = -(fma(cc, g1[2], fma(b, g1[1], a * g1[0]))) * r;
+      const double h2 = -(fma(cc, g2[2], fma(b, g2[1], a * g2[0]))) * r;
+      z[2] = z[1]; z[1] = z[0]; z[0] = zn;
+      g0[2] = g0[1]; g0[1] = g0[0]; g0[0] = h0;
+      g1[2] = g1[1]; g1[1] = g1[0]; g1[0] = h1;
+      g2[2] = g2[1]; g2[1] = g2[0]; g2[0] = h2;
+    }
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      sh[c][q][lane] = z[q];
+      sh[c][3 + q][lane] = g0[q];
+      sh[c][6 + q][lane] = g1[q];
+      sh[c][9 + q][lane] = g2[q];
+    }
+    __syncthreads();
+    if (c == 0) {
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+      for (int k = 0; k < P; ++k) {
+        double ns[3];
+#pragma unroll
+        for (int q = 0; q < 3; ++q)
+          ns[q] = sh[k][q][lane] + sh[k][3 + q][lane] * s0 + sh[k][6 + q][lane] * s1 +
+                  sh[k][9 + q][lane] * s2;
+        sh[k][0][lane] = s0;
+        sh[k][1][lane] = s1;
+        sh[k][2][lane] = s2;
+        s0 = ns[0];
+        s1 = ns[1];
+        s2 = ns[2];
+      }
+    }
+    __syncthreads();
+    double y1 = sh[c][0][lane], y2 = sh[c][1][lane], y3 = sh[c][2][lane];
+    if (act) {
+      for (int64_t j = j0; j < j1; ++j) {
+        const int64_t o = j * nh;
+        const double y = (fma(-__ldg(l3 + o), y3, fma(-__ldg(l2 + o), y2, col[o])) -
+                          __ldg(l1 + o) * y1) * __ldg(rd + o);
+        col[o] = y;
+        y3 = y2;
+        y2 = y1;
+        y1 = y;
+      }
+    }
+    __syncthreads();  // every chunk's y is stored (the backward pass reads across chunks)
+  }
+  // ---------------- backward: w_j = (y_j - L(j+1,j) w_{j+1} - L(j+2,j) w_{j+2} - L(j+3,j) w_{j+3}) rd
+  {
+    auto coef = [&](int64_t j, double& a, double& b, double& cc, double& r) {
+      const int64_t o = j * nh;
+      a = (act && j + 1 < nt) ? __ldg(l1 + o + nh) : 0.0;
+      b = (act && j + 2 < nt) ? __ldg(l2 + o + 2 * nh) : 0.0;
+      cc = (act && j + 3 < nt) ? __ldg(l3 + o + 3 * nh) : 0.0;
+      r = act ? __ldg(rd + o) : 0.0;
+    };
+    double z[3] = {0, 0, 0}, g0[3] = {1, 0, 0}, g1[3] = {0, 1, 0}, g2[3] = {0, 0, 1};
+    for (int64_t j = j1 - 1; j >= j0; --j) {
+      double a, b, cc, r;
+      coef(j, a, b, cc, r);
+      const double v = act ? col[j * nh] : 0.0;
+      const double zn = (fma(-cc, z[2], fma(-b, z[1], v)) - a * z[0]) * r;
+      const double h0 = -(fma(cc, g0[2], fma(b, g0[1], a * g0[0]))) * r;
+      const double h1 = -(fma(cc, g1[2], fma(b, g1[1], a * g1[0]))) * r;
+      const double h2 = -(fma(cc, g2[2], fma(b, g2[1], a * g2[0]))) * r;
+      z[2] = z[1]; z[1] = z[0]; z[0] = zn;
+      g0[2] = g0[1]; g0[1] = g0[0]; g0[0] = h0;
+      g1[2] = g1[1]; g1[1] = g1[0]; g1[0] = h1;
+      g2[2] = g2[1]; g2[1] = g2[0]; g2[0] = h2;
+    }
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      sh[c][q][lane] = z[q];
+      sh[c][3 + q][lane] = g0[q];
+      sh[c][6 + q][lane] = g1[q];
+      sh[c][9 + q][lane] = g2[q];
+    }
+    __syncthreads();
+    if (c == 0) {
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+      for (int k = P - 1; k >= 0; --k) {
+        double ns[3];
+#pragma unroll
+        for (int q = 0; q < 3; ++q)
+          ns[q] = sh[k][q][lane] + sh[k][3 + q][lane] * s0 + sh[k][6 + q][lane] * s1 +
+                  sh[k][9 + q][lane] * s2;
+        sh[k][0][lane] = s0;
+        sh[k][1][lane] = s1;
+        sh[k][2][lane] = s2;
+        s0 = ns[0];
+        s1 = ns[1];
+        s2 = ns[2];
+      }
+    }
+    __syncthreads();
+    double w1 = sh[c][0][lane], w2 = sh[c][1][lane], w3 = sh[c][2][lane];
+    if (act) {
+      for (int64_t j = j1 - 1; j >= j0; --j) {
+        double a, b, cc, r;
+        coef(j, a, b, cc, r);
+        const int64_t o = j * nh;
+        const double w = (fma(-cc, w3, fma(-b, w2, col[o])) - a * w1) * r;
+        col[o] = w;
+        w3 = w2;
+        w2 = w1;
+        w1 = w;
+      }
+    }
+  }
+}
+
 // Host setup of the modal banded preconditioner: a_i, the banded Cholesky factors of every
 // K_i (symmetrised: the spline Gram bands are symmetric only to rounding).
 void build_modal_banded(stkg_wave& w, const double* space_bands, const double* time_bands,
@@ -437,9 +588,20 @@ void modal_banded_solve(stkg_wave& w, const double* v, double* out) {
   p.M = nh; p.K = nh; p.N = nt;
   p.A = w.XsT.p; p.lda = nh; p.B = v; p.ldb = nh; p.C = w.t1.p; p.ldc = nh;
   launch_gemm(p, EpiStore{}, w.stream);
-  // rows of t1 <- K_i^-1 rows
-  modal_banded_solve_kernel<<<static_cast<unsigned>(ceil_div(nh, 32)), 32, 0, w.stream>>>(
-      w.t1.p, w.mb.p, nh, nt, w.krylov.skip);
+  // rows of t1 <- K_i^-1 rows (STKG_MB_CHUNKS: time chunks per mode, 1 = sequential kernel)
+  static const int chunks = [] {
+    const char* e = std::getenv("STKG_MB_CHUNKS");
+    return e ? std::atoi(e) : 16;
+  }();
+  const unsigned g32 = static_cast<unsigned>(ceil_div(nh, 32));
+  if (chunks >= 16 && nt >= 16 * 16)
+    modal_banded_solve_chunked_kernel<16><<<g32, 512, 0, w.stream>>>(w.t1.p, w.mb.p, nh, nt,
+                                                                   w.krylov.skip);
+  else if (chunks >= 8 && nt >= 8 * 16)
+    modal_banded_solve_chunked_kernel<8><<<g32, 256, 0, w.stream>>>(w.t1.p, w.mb.p, nh, nt,
+                                                                  w.krylov.skip);
+  else
+    modal_banded_solve_kernel<<<g32, 32, 0, w.stream>>>(w.t1.p, w.mb.p, nh, nt, w.krylov.skip);
   STKG_CUDA_CHECK(cudaGetLastError());
   // out = Xs t1
   p.M = nh; p.K = nh; p.N = nt;

@@ -328,3 +328,11 @@ def test_oracle_refined_direct_wave_solve(orc, ref_bands):
     b = np.random.default_rng(4).standard_normal(sb.shape[2] * tb.shape[2])
     xh, xl, hist = orc.wave_refined_direct(sb, tb, b, steps=3)
     assert hist[-1] <= 1e-15 and hist[-1] < hist[0]
+
+
+def test_oracle_modal_banded_inverse_pair(orc, ref_bands):
+    """The oracle's modal banded preconditioner solve and its operator are inverses."""
+    sb, tb = ref_bands["space_31_3"], ref_bands["time_33_3"]
+    W = orc.WaveSystemNP(sb, tb)
+    v = np.random.default_rng(9).standard_normal(W.nh * W.nt)
+    assert np.linalg.norm(W.modal_banded_apply(W.modal_banded(v)) - v) <= 1e-11 * np.linalg.norm(v)
