@@ -36,7 +36,9 @@ namespace stkg {
 // VV: complex values per thread of the FFTs (16: radix-16,16,4 stages, 64 threads per pair for
 // N = 1024; 8: radix-8,8,8,2 stages, 128 threads per pair -- twice the warps per SM for the
 // same tile, one more shared-memory exchange per transform).
-template <int N, int PP, bool CS = false, bool TMA = false, int VV = half2_v<N>()>
+// MB: minimum resident CTAs per SM for __launch_bounds__ (2 caps registers at 128 so that
+// other kernels' CTAs can share the SM -- the overlapped 2D schedule's contiguous passes).
+template <int N, int PP, bool CS = false, bool TMA = false, int VV = half2_v<N>(), int MB = 1>
 struct FusedCfg {
   using B = HalfStrided2Cfg<N, PP, true>;  // tile geometry (swizzle), region size
   static constexpr int V = VV, T = N / V, P = B::P, G = B::G, kThreads = P * T;
@@ -49,8 +51,14 @@ struct FusedCfg {
       TMA ? size_t(kBoxes) * kBoxRows * 64 : size_t(B::kTile) * sizeof(double2);
   static constexpr size_t kTileOff = TMA ? (kRegionBytes + 511) / 512 * 512 : kRegionBytes;
   static constexpr size_t kCarryOff = kTileOff + kTileBytes;
-  static constexpr size_t kSmem = kCarryOff + (CS ? size_t(P) * N * sizeof(double2) : 0) +
-                                  (TMA ? 512 : 0);  // slack: the base is aligned at run time
+  // (the dynamic buffer is declared 1024-byte aligned, so kTileOff's 512-byte alignment is
+  // the SWIZZLE_64B pattern's; kernels check the base at run time)
+  // scan partials and the mbarrier live in the dynamic buffer too: with no static shared
+  // memory the dynamic buffer starts at the (1024-byte aligned) start of the CTA's window
+  static constexpr int kRedPer = T > 32 ? 2 * (T / 32) : 2;
+  static constexpr size_t kRedOff = kCarryOff + (CS ? size_t(P) * N * sizeof(double2) : 0);
+  static constexpr size_t kBarOff = kRedOff + size_t(P) * kRedPer * sizeof(double);
+  static constexpr size_t kSmem = kBarOff + 16;
   static_assert(!TMA || P == 4, "TMA staging: tiles of 4 pairs (64-byte rows)");
 };
 
@@ -72,10 +80,10 @@ __device__ __forceinline__ double nr_recip(double p) {
 // weight product of the faster axes for each column (inner entries; pad lane 0 / 0).
 // carry (slice entries, indexed like one slice): y_{l0-1} in, y_{l0+ntc-1} out.
 // map (TMA only): S viewed as [ntc n_0 rows] x [inner columns], boxes of {8, 256}.
-template <int N, int PP, bool CS, bool TMA, int VV>
-__global__ void __launch_bounds__(FusedCfg<N, PP, CS, TMA, VV>::kThreads,
-                                  FusedCfg<N, PP, CS, TMA, VV>::kThreads >= 256
-                                      ? 1 : 256 / FusedCfg<N, PP, CS, TMA, VV>::kThreads)
+template <int N, int PP, bool CS, bool TMA, int VV, int MB>
+__global__ void __launch_bounds__(FusedCfg<N, PP, CS, TMA, VV, MB>::kThreads,
+                                  FusedCfg<N, PP, CS, TMA, VV, MB>::kThreads >= 256
+                                      ? MB : 256 / FusedCfg<N, PP, CS, TMA, VV, MB>::kThreads)
     heat_fused_axis0_kernel(const __grid_constant__ CUtensorMap map, double* S, int64_t inner,
                             int64_t slice, int64_t ntc, int64_t l0,
                             const double2* __restrict__ tw2, double scale,
@@ -84,18 +92,19 @@ __global__ void __launch_bounds__(FusedCfg<N, PP, CS, TMA, VV>::kThreads,
                             const double* __restrict__ d_diag, const double* __restrict__ d_sup,
                             const double* __restrict__ c_diag, const double* __restrict__ c_sup,
                             double* __restrict__ carry) {
-  using C = FusedCfg<N, PP, CS, TMA, VV>;
+  using C = FusedCfg<N, PP, CS, TMA, VV, MB>;
   using SC = typename C::B;
   using OP = OutPair<N, 4>;
   constexpr int V = C::V, T = C::T, P = C::P, n = N - 1, RG = C::kRegion;
-  extern __shared__ __align__(128) unsigned char sraw[];
-  unsigned char* sbase = TMA ? reinterpret_cast<unsigned char*>(
-                                   (reinterpret_cast<uintptr_t>(sraw) + 511) & ~uintptr_t(511))
-                             : sraw;
+  extern __shared__ __align__(1024) unsigned char sraw[];
+  unsigned char* sbase = sraw;
+  if constexpr (TMA) {  // the SWIZZLE_64B tile needs a 512-byte aligned destination
+    if ((static_cast<unsigned>(__cvta_generic_to_shared(sraw)) & 511u) != 0u) __trap();
+  }
   double2* sreg = reinterpret_cast<double2*>(sbase);
   double2* stile = reinterpret_cast<double2*>(sbase + C::kTileOff);
-  __shared__ double red[P][T > 32 ? 2 * (T / 32) : 2];
-  __shared__ __align__(8) uint64_t mbar;
+  double* red = reinterpret_cast<double*>(sbase + C::kRedOff);  // [P][kRedPer]
+  uint64_t& mbar = *reinterpret_cast<uint64_t*>(sbase + C::kBarOff);
   const int f = threadIdx.x / T, t = threadIdx.x % T;
   const int bar = P > 1 ? 1 + f : 0;
   double2* region = sreg + f * RG;
@@ -178,7 +187,7 @@ __global__ void __launch_bounds__(FusedCfg<N, PP, CS, TMA, VV>::kThreads,
     if (j + 1 < ntc) load_tile(j + 1);
 
     // forward transform along axis 0 -> OutPair (g~ of both columns, unweighted)
-    half_fft_post<N, V>(x, region, tw2, t, hs, red[f], OP{region}, bar);
+    half_fft_post<N, V>(x, region, tw2, t, hs, red + f * C::kRedPer, OP{region}, bar);
     fft_sync<T>(bar);
 
     // recurrence (stk/sylvester.hpp:131-139): y = (g~ - sub y) / piv per mode
@@ -234,7 +243,7 @@ __global__ void __launch_bounds__(FusedCfg<N, PP, CS, TMA, VV>::kThreads,
         x[p] = half_pre(s, u.x, w.x, u.y, w.y);
       }
     }
-    half_fft_post<N, V>(x, region, tw2, t, hs, red[f], OP{region}, bar);
+    half_fft_post<N, V>(x, region, tw2, t, hs, red + f * C::kRedPer, OP{region}, bar);
     __syncthreads();
     double* dst = S + j * slice + i0;
     for (int e = threadIdx.x; e < P * n; e += C::kThreads) {
