@@ -5,6 +5,7 @@
 //   solve_projected_heat_with   stk/sylvester.hpp:117-142   -> stk::gpu::solve_projected_heat_with
 //   KronOp::apply (heat)        stk/sylvester.hpp:32-38     -> stk::gpu::HeatPlan::apply
 //   TwoTermPrecond::solve       stk/sylvester.hpp:168-176   -> stk::gpu::WavePlan::two_term_solve
+//   (new) modal banded preconditioner                      -> stk::gpu::WavePlan::modal_banded_solve
 //   WaveOperator::apply         stk/outer_krylov.hpp:178-186 -> stk::gpu::WavePlan::apply
 //   gmres(VecOp, VecOp, b, cfg) stk/outer_krylov.hpp:75-164 -> stk::gpu::gmres
 // Failures are rethrown as the reference's exception classes (stk/errors.hpp:9-42).  When
@@ -405,6 +406,12 @@ class WavePlan {
 
   void apply(const double* x, double* y) { check(stkg_wave_apply(w_, x, y)); }
   void two_term_solve(const double* v, double* w) { check(stkg_two_term_solve(w_, v, w)); }
+  // The space-modal time-banded preconditioner (no reference counterpart, K2d).
+  void modal_banded_solve(const double* v, double* w) {
+    check(stkg_modal_banded_solve(w_, v, w));
+  }
+  // What gmres / pcg / solve_refined apply: false = TwoTermPrecond (default), true = modal.
+  void use_modal_banded(bool on) { check(stkg_wave_set_precond(w_, on ? 1 : 0)); }
 
   SolveReport gmres(const double* b, double* x, const GmresConfig& cfg = {}, bool precond = true) {
     stkg_gmres_config c{cfg.tol, cfg.maxit, cfg.restart, precond ? 1 : 0};
