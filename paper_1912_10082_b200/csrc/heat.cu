@@ -625,8 +625,14 @@ void run_chunk_padded_overlap(stkg_heat& h, const double* F, double* U, double* 
     }
     C2(K - 1);
   } catch (...) {
+    // rejoin whatever was enqueued before the error, so later work on the plan stream
+    // cannot overtake it (best effort: the error being reported is the first one)
     h.run_stream = nullptr;
     h.run_ticket = nullptr;
+    cudaEventRecord(ev_lo, h.s_lo);
+    cudaEventRecord(ev_hi, h.s_hi);
+    cudaStreamWaitEvent(h.stream, ev_lo, 0);
+    cudaStreamWaitEvent(h.stream, ev_hi, 0);
     throw;
   }
   h.run_stream = nullptr;
