@@ -445,7 +445,13 @@ struct HalfCfg {
   static constexpr int T = N / V;             // threads per FFT
   static constexpr int F = T >= 64 ? 1 : 64 / T;  // FFTs per CTA
   static constexpr int kThreads = F * T;
-  static constexpr int kBuf = hpadded_len<N>();  // complex per FFT buffer
+  // complex per FFT buffer.  With T in [2, 8] a half-warp holds 16/T FFTs, whose 8-byte
+  // output-staging accesses run in the same phase: the buffers are skewed to kBuf = T/2
+  // (mod 8) complex so those FFTs start T 8-byte banks apart (unskewed, every buffer began
+  // at the same bank and the puts / scan accesses were 2-way conflicted: 29% excess
+  // wavefronts at N = 128, profiles/r02 notes in DESIGN.md K2b).
+  static constexpr int kBuf0 = hpadded_len<N>();
+  static constexpr int kBuf = (T >= 2 && T <= 8) ? kBuf0 + ((T / 2 - kBuf0 % 8) + 8) % 8 : kBuf0;
   static constexpr size_t kSmem = size_t(F) * kBuf * sizeof(double2);
 #ifdef STKG_HALF_MINB
   static constexpr int kMinBlocks = STKG_HALF_MINB;
@@ -546,11 +552,11 @@ __global__ void __launch_bounds__(HalfCfg<N>::kThreads, HalfCfg<N>::kMinBlocks)
       const int64_t v0 = 2 * item * F;
       const int nv = static_cast<int>(nvec - v0 < 2 * F ? nvec - v0 : 2 * F);
       double* d0 = dst + v0 * ld_dst;
-      for (int e = threadIdx.x; e < nv * ldo; e += C::kThreads) {
-        const int q = e / ldo, idx = e - q * ldo;  // vector q of the item
+      for (int q = 0; q < nv; ++q) {  // vector q of the item (no division in the loop)
         const double* o_q = reinterpret_cast<const double*>(hbuf + (q >> 1) * C::kBuf) +
                             ((q & 1) ? opad<V>(N) : 0);
-        d0[e] = idx < n ? o_q[opad<V>(idx)] : 0.0;
+        for (int idx = threadIdx.x; idx < ldo; idx += C::kThreads)
+          d0[int64_t(q) * ldo + idx] = idx < n ? o_q[opad<V>(idx)] : 0.0;
       }
       __syncthreads();  // other FFTs' buffers were read: next item may overwrite them
     }
