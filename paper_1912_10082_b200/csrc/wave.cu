@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <memory>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "common.cuh"
@@ -360,7 +361,9 @@ __global__ void __launch_bounds__(32 * P) modal_banded_solve_chunked_kernel(
     const int* skip) {
   if (skip && *skip) return;
   // per chunk and lane: e (3) and G columns (9); pass B overwrites e with the incoming state
-  __shared__ double sh[P][12][32];
+  // (dynamic shared memory: P * 12 * 32 doubles, 96 KB at P = 32)
+  extern __shared__ double sh_raw[];
+  double (*sh)[12][32] = reinterpret_cast<double (*)[12][32]>(sh_raw);
   const int lane = threadIdx.x & 31, c = threadIdx.x >> 5;
   const int64_t i = int64_t(blockIdx.x) * 32 + lane;
   const bool act = i < nh;
@@ -591,15 +594,27 @@ void modal_banded_solve(stkg_wave& w, const double* v, double* out) {
   // rows of t1 <- K_i^-1 rows (STKG_MB_CHUNKS: time chunks per mode, 1 = sequential kernel)
   static const int chunks = [] {
     const char* e = std::getenv("STKG_MB_CHUNKS");
-    return e ? std::atoi(e) : 16;
+    return e ? std::atoi(e) : 32;
   }();
   const unsigned g32 = static_cast<unsigned>(ceil_div(nh, 32));
-  if (chunks >= 16 && nt >= 16 * 16)
-    modal_banded_solve_chunked_kernel<16><<<g32, 512, 0, w.stream>>>(w.t1.p, w.mb.p, nh, nt,
-                                                                   w.krylov.skip);
+  auto chunked = [&](auto pc) {
+    constexpr int P = decltype(pc)::value;
+    constexpr int smem = P * 12 * 32 * int(sizeof(double));
+    static const bool configured = [] {
+      STKG_CUDA_CHECK(cudaFuncSetAttribute(modal_banded_solve_chunked_kernel<P>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      return true;
+    }();
+    (void)configured;
+    modal_banded_solve_chunked_kernel<P><<<g32, 32 * P, smem, w.stream>>>(w.t1.p, w.mb.p, nh, nt,
+                                                                          w.krylov.skip);
+  };
+  if (chunks >= 32 && nt >= 32 * 16)
+    chunked(std::integral_constant<int, 32>{});
+  else if (chunks >= 16 && nt >= 16 * 16)
+    chunked(std::integral_constant<int, 16>{});
   else if (chunks >= 8 && nt >= 8 * 16)
-    modal_banded_solve_chunked_kernel<8><<<g32, 256, 0, w.stream>>>(w.t1.p, w.mb.p, nh, nt,
-                                                                  w.krylov.skip);
+    chunked(std::integral_constant<int, 8>{});
   else
     modal_banded_solve_kernel<<<g32, 32, 0, w.stream>>>(w.t1.p, w.mb.p, nh, nt, w.krylov.skip);
   STKG_CUDA_CHECK(cudaGetLastError());
