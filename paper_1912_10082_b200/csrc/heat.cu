@@ -343,12 +343,13 @@ bool dst_half_pass(const stkg_heat& h, int a, const double* src, double* dst, in
 // Time-marching fused pass over axis 0 of the padded layout (heat_fused.cuh): forward
 // transform, recurrence and inverse transform of every slice of S in one kernel.
 template <int N, int P = fused_pairs<N>(), bool CS = false, bool TMA = false,
-          int V = half2_v<N>(), int MB = 1>
+          int V = half2_v<N>(), int MB = 1, int MAXR = 0>
 void launch_fused_axis0(const stkg_heat& h, double* S, int64_t inner, int64_t ntc, int64_t l0) {
   using C = FusedCfg<N, P, CS, TMA, V, MB>;
-  static const bool configured = [] {
-    STKG_CUDA_CHECK(cudaFuncSetAttribute(heat_fused_axis0_kernel<N, P, CS, TMA, V, MB>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+  static_assert(MAXR == 0, "register-capped instantiation removed (DESIGN.md K2c)");
+  auto kern = heat_fused_axis0_kernel<N, P, CS, TMA, V, MB>;
+  static const bool configured = [kern] {
+    STKG_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(C::kSmem)));
     return true;
   }();
@@ -369,7 +370,7 @@ void launch_fused_axis0(const stkg_heat& h, double* S, int64_t inner, int64_t nt
   }
   const int64_t tiles = inner / C::G;
   const double scale = std::sqrt(2.0 / static_cast<double>(N));
-  heat_fused_axis0_kernel<N, P, CS, TMA, V, MB><<<static_cast<unsigned>(tiles), C::kThreads, C::kSmem,
+  kern<<<static_cast<unsigned>(tiles), C::kThreads, C::kSmem,
                                               launch_stream(h)>>>(
       map, S, inner, h.n[0] * inner, ntc, l0, reinterpret_cast<const double2*>(h.twiddle[0].p),
       scale, h.lam[0].p, h.inv_mu[0].p, h.lam_col.p, h.w_col.p, h.d_diag.p, h.d_sup.p,

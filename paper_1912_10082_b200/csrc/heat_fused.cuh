@@ -80,18 +80,18 @@ __device__ __forceinline__ double nr_recip(double p) {
 // weight product of the faster axes for each column (inner entries; pad lane 0 / 0).
 // carry (slice entries, indexed like one slice): y_{l0-1} in, y_{l0+ntc-1} out.
 // map (TMA only): S viewed as [ntc n_0 rows] x [inner columns], boxes of {8, 256}.
+#define STKG_FUSED_PARAMS                                                                   \
+  double *S, int64_t inner, int64_t slice, int64_t ntc, int64_t l0,                        \
+      const double2 *__restrict__ tw2, double scale, const double *__restrict__ lam_ax,     \
+      const double *__restrict__ w_ax, const double *__restrict__ lam_col,                  \
+      const double *__restrict__ w_col, const double *__restrict__ d_diag,                  \
+      const double *__restrict__ d_sup, const double *__restrict__ c_diag,                  \
+      const double *__restrict__ c_sup, double *__restrict__ carry
+#define STKG_FUSED_ARGS \
+  S, inner, slice, ntc, l0, tw2, scale, lam_ax, w_ax, lam_col, w_col, d_diag, d_sup, c_diag, c_sup, carry
+
 template <int N, int PP, bool CS, bool TMA, int VV, int MB>
-__global__ void __launch_bounds__(FusedCfg<N, PP, CS, TMA, VV, MB>::kThreads,
-                                  FusedCfg<N, PP, CS, TMA, VV, MB>::kThreads >= 256
-                                      ? MB : 256 / FusedCfg<N, PP, CS, TMA, VV, MB>::kThreads)
-    heat_fused_axis0_kernel(const __grid_constant__ CUtensorMap map, double* S, int64_t inner,
-                            int64_t slice, int64_t ntc, int64_t l0,
-                            const double2* __restrict__ tw2, double scale,
-                            const double* __restrict__ lam_ax, const double* __restrict__ w_ax,
-                            const double* __restrict__ lam_col, const double* __restrict__ w_col,
-                            const double* __restrict__ d_diag, const double* __restrict__ d_sup,
-                            const double* __restrict__ c_diag, const double* __restrict__ c_sup,
-                            double* __restrict__ carry) {
+__device__ __forceinline__ void heat_fused_axis0_body(const CUtensorMap& map, STKG_FUSED_PARAMS) {
   using C = FusedCfg<N, PP, CS, TMA, VV, MB>;
   using SC = typename C::B;
   using OP = OutPair<N, 4>;
@@ -271,5 +271,14 @@ __global__ void __launch_bounds__(FusedCfg<N, PP, CS, TMA, VV, MB>::kThreads,
   }
 }
 
+
+
+template <int N, int PP, bool CS, bool TMA, int VV, int MB>
+__global__ void __launch_bounds__(FusedCfg<N, PP, CS, TMA, VV, MB>::kThreads,
+                                  FusedCfg<N, PP, CS, TMA, VV, MB>::kThreads >= 256
+                                      ? MB : 256 / FusedCfg<N, PP, CS, TMA, VV, MB>::kThreads)
+    heat_fused_axis0_kernel(const __grid_constant__ CUtensorMap map, STKG_FUSED_PARAMS) {
+  heat_fused_axis0_body<N, PP, CS, TMA, VV, MB>(map, STKG_FUSED_ARGS);
+}
 
 }  // namespace stkg
