@@ -14,6 +14,9 @@
 // the four products of TwoTermPrecond::solve (stk/sylvester.hpp:171,175).
 #pragma once
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace stkg {
@@ -98,26 +101,18 @@ __device__ __forceinline__ void dmma_m16n8k4(double (&c)[4], double a0, double a
       : "d"(a0), "d"(a1), "d"(b));
 }
 
-template <class Cfg, class Epi>
-__global__ void __launch_bounds__(Cfg::kThreads, Cfg::kMinBlocks)
-    gemm_f64_kernel(const GemmProblem p, const Epi epi) {
-  if (p.skip && *p.skip) return;  // device-side early exit (converged Krylov iteration)
-  extern __shared__ __align__(16) double smem[];
+// One output tile (tm, tn) of batch bt, K-tiles [kt0, kt1), accumulated into acc (zeroed
+// here).  Shared by the one-tile-per-CTA kernel and the stream-K kernel.
+template <class Cfg>
+__device__ __forceinline__ void gemm_tile_accumulate(const GemmProblem& p, int64_t tm, int64_t tn,
+                                                     int64_t bt, int64_t kt0, int64_t kt1,
+                                                     double* smem,
+                                                     double (&acc)[Cfg::kMi][Cfg::kNi][4]) {
   double* sA = smem;                                   // [STAGES][BK][kLdsA]
   double* sB = smem + Cfg::STAGES * Cfg::kStageA;      // [STAGES][BN][kLdsB]
-
-  const int64_t tiles_m = (p.M + Cfg::BM - 1) / Cfg::BM;
-  const int64_t tiles_n = (p.N + Cfg::BN - 1) / Cfg::BN;
-  int64_t bid = blockIdx.x;
-  const int64_t tm = bid % tiles_m;
-  bid /= tiles_m;
-  const int64_t tn = bid % tiles_n;
-  const int64_t bt = bid / tiles_n;
   const int64_t m0 = tm * Cfg::BM, n0 = tn * Cfg::BN;
-
   const double* A = p.A + bt * p.strideA;
   const double* B = p.B + bt * p.strideB;
-  double* C = p.C + bt * p.strideC;
 
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
@@ -148,7 +143,6 @@ __global__ void __launch_bounds__(Cfg::kThreads, Cfg::kMinBlocks)
   static_assert((kColsB & (kColsB - 1)) == 0, "kColsB must be a power of two");
   const int b_dst = bk * Cfg::kLdsB + perm16(bn);
 
-  const int64_t ktiles = (p.K + Cfg::BK - 1) / Cfg::BK;
   const int64_t kfull = p.K / Cfg::BK;
 
   auto load_stage = [&](int stage, int64_t kt) {
@@ -170,7 +164,6 @@ __global__ void __launch_bounds__(Cfg::kThreads, Cfg::kMinBlocks)
     }
   };
 
-  double acc[Cfg::kMi][Cfg::kNi][4];
 #pragma unroll
   for (int mi = 0; mi < Cfg::kMi; ++mi)
 #pragma unroll
@@ -178,9 +171,10 @@ __global__ void __launch_bounds__(Cfg::kThreads, Cfg::kMinBlocks)
 #pragma unroll
       for (int r = 0; r < 4; ++r) acc[mi][ni][r] = 0.0;
 
+  const int64_t nk = kt1 - kt0;
 #pragma unroll
   for (int s = 0; s < Cfg::STAGES - 1; ++s) {
-    if (s < ktiles) load_stage(s, s);
+    if (s < nk) load_stage(s, kt0 + s);
     cp_async_commit();
   }
 
@@ -203,10 +197,10 @@ __global__ void __launch_bounds__(Cfg::kThreads, Cfg::kMinBlocks)
     }
   };
 
-  for (int64_t kt = 0; kt < ktiles; ++kt) {
+  for (int64_t i = 0; i < nk; ++i) {
     cp_async_wait<Cfg::STAGES - 2>();
     __syncthreads();
-    const int stage = static_cast<int>(kt % Cfg::STAGES);
+    const int stage = static_cast<int>(i % Cfg::STAGES);
     const double* a_s = sA + stage * Cfg::kStageA;
     const double* b_s = sB + stage * Cfg::kStageB;
     load_frags(0, a_s, b_s, 0);
@@ -222,15 +216,26 @@ __global__ void __launch_bounds__(Cfg::kThreads, Cfg::kMinBlocks)
       if (kk == 0) {
         // refill the stage consumed in the previous iteration while the tensor pipe
         // works through the first sub-step's DMMAs
-        const int64_t nk = kt + Cfg::STAGES - 1;
-        if (nk < ktiles) load_stage(static_cast<int>(nk % Cfg::STAGES), nk);
+        const int64_t nx = i + Cfg::STAGES - 1;
+        if (nx < nk) load_stage(static_cast<int>(nx % Cfg::STAGES), kt0 + nx);
         cp_async_commit();
       }
     }
   }
   cp_async_wait<0>();
+  __syncthreads();  // the shared stages may be refilled by the caller's next tile
+}
 
-  // Epilogue: direct stores (each quad of lanes writes 2 adjacent columns of 8 rows).
+// Epilogue: direct stores (each quad of lanes writes 2 adjacent columns of 8 rows).
+template <class Cfg, class Epi>
+__device__ __forceinline__ void gemm_tile_store(const GemmProblem& p, int64_t tm, int64_t tn,
+                                                int64_t bt, const Epi& epi,
+                                                const double (&acc)[Cfg::kMi][Cfg::kNi][4]) {
+  double* C = p.C + bt * p.strideC;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = warp % Cfg::kWarpsM, wn = warp / Cfg::kWarpsM;
+  const int64_t m0 = tm * Cfg::BM, n0 = tn * Cfg::BN;
 #pragma unroll
   for (int mi = 0; mi < Cfg::kMi; ++mi) {
 #pragma unroll
@@ -244,6 +249,133 @@ __global__ void __launch_bounds__(Cfg::kThreads, Cfg::kMinBlocks)
         if (r < p.M && c < p.N) C[c * p.ldc + r] = epi(acc[mi][ni][q], r, c);
       }
     }
+  }
+}
+
+template <class Cfg, class Epi>
+__global__ void __launch_bounds__(Cfg::kThreads, Cfg::kMinBlocks)
+    gemm_f64_kernel(const GemmProblem p, const Epi epi) {
+  if (p.skip && *p.skip) return;  // device-side early exit (converged Krylov iteration)
+  extern __shared__ __align__(16) double smem[];
+  const int64_t tiles_m = (p.M + Cfg::BM - 1) / Cfg::BM;
+  const int64_t tiles_n = (p.N + Cfg::BN - 1) / Cfg::BN;
+  int64_t bid = blockIdx.x;
+  const int64_t tm = bid % tiles_m;
+  bid /= tiles_m;
+  const int64_t tn = bid % tiles_n;
+  const int64_t bt = bid / tiles_n;
+  const int64_t ktiles = (p.K + Cfg::BK - 1) / Cfg::BK;
+  double acc[Cfg::kMi][Cfg::kNi][4];
+  gemm_tile_accumulate<Cfg>(p, tm, tn, bt, 0, ktiles, smem, acc);
+  gemm_tile_store<Cfg>(p, tm, tn, bt, epi, acc);
+}
+
+// ---------------------------------------------------------------------------- stream-K --
+// Persistent stream-K schedule for single GEMMs whose tile count leaves CTA slots idle (the
+// 1023 x 1023 x 1025 wave preconditioner products: 272 tiles of 64 x 64 for 444 slots).  The
+// (tile, K-tile) iteration space is cut into G equal contiguous ranges, one per resident CTA
+// (G = the occupancy-limited slot count, so every CTA is resident and the flag waits below
+// cannot deadlock).  A tile split across CTAs is finished by the CTA holding its first
+// K-tiles, which reaches them at the END of its range -- the later segments' CTAs met theirs at
+// the start of their ranges, so the finisher rarely waits (finishing on the last segment
+// instead would make that CTA idle through its predecessor's whole range).  The other segments
+// store their accumulators to a workspace slot and publish a flag (the launch's epoch); the
+// finisher adds the slots in segment order (deterministic) and applies the epilogue.
+struct StreamKWork {
+  double* partials = nullptr;   // tiles * kMaxSeg * BM * BN doubles
+  unsigned* flags = nullptr;    // tiles * kMaxSeg
+  int64_t tiles_cap = 0;
+  unsigned epoch = 0;
+  static constexpr int kMaxSeg = 4;
+};
+
+template <class Cfg, class Epi>
+__global__ void __launch_bounds__(Cfg::kThreads, Cfg::kMinBlocks)
+    gemm_f64_streamk_kernel(const GemmProblem p, const Epi epi, double* __restrict__ partials,
+                            unsigned* __restrict__ flags, unsigned epoch) {
+  if (p.skip && *p.skip) return;
+  extern __shared__ __align__(16) double smem[];
+  constexpr int kFrag = Cfg::kMi * Cfg::kNi * 4;
+  const int64_t tiles_m = (p.M + Cfg::BM - 1) / Cfg::BM;
+  const int64_t tiles_n = (p.N + Cfg::BN - 1) / Cfg::BN;
+  const int64_t ktiles = (p.K + Cfg::BK - 1) / Cfg::BK;
+  const int64_t W = tiles_m * tiles_n * ktiles;
+  const int64_t G = gridDim.x, c = blockIdx.x;
+  auto start = [&](int64_t cc) { return cc * W / G; };
+  const int64_t u_end = start(c + 1);
+  double acc[Cfg::kMi][Cfg::kNi][4];
+  for (int64_t u = start(c); u < u_end;) {
+    const int64_t tile = u / ktiles, kt0 = u - tile * ktiles;
+    const int64_t kt1 = (tile + 1) * ktiles < u_end ? ktiles : u_end - tile * ktiles;
+    const int64_t tm = tile % tiles_m, tn = tile / tiles_m;
+    gemm_tile_accumulate<Cfg>(p, tm, tn, 0, kt0, kt1, smem, acc);
+    // segments of the tile: CTAs c0 .. c1 (owners of its first and last K-tile); this CTA is
+    // segment c - c0, the finisher is segment 0 (kt0 == 0)
+    auto owner = [&](int64_t uu) {
+      int64_t cc = uu * G / W;
+      while (start(cc + 1) <= uu) ++cc;
+      while (start(cc) > uu) --cc;
+      return cc;
+    };
+    const int64_t c0 = owner(tile * ktiles), c1 = owner(tile * ktiles + ktiles - 1);
+    const int seg = static_cast<int>(c - c0), nseg = static_cast<int>(c1 - c0 + 1);
+    double* slot_base = partials + (tile * StreamKWork::kMaxSeg) * int64_t(kFrag) * Cfg::kThreads;
+    unsigned* flag_base = flags + tile * StreamKWork::kMaxSeg;
+    if (kt0 == 0 && kt1 == ktiles) {
+      gemm_tile_store<Cfg>(p, tm, tn, 0, epi, acc);
+    } else if (kt0 > 0) {  // not the finisher: publish the partial sums
+      double* slot = slot_base + int64_t(seg) * kFrag * Cfg::kThreads;
+      int f = 0;
+#pragma unroll
+      for (int mi = 0; mi < Cfg::kMi; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < Cfg::kNi; ++ni)
+#pragma unroll
+          for (int r = 0; r < 4; ++r, ++f) __stcg(slot + f * Cfg::kThreads + threadIdx.x, acc[mi][ni][r]);
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(flag_base + seg), "r"(epoch)
+                     : "memory");
+      }
+    } else {  // finisher (segment 0): add the later segments in order, then the epilogue
+      if (threadIdx.x >= 1 && threadIdx.x < nseg) {
+        unsigned v;
+        do {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n"
+                       : "=r"(v)
+                       : "l"(flag_base + threadIdx.x)
+                       : "memory");
+        } while (v != epoch);
+      }
+      __syncthreads();
+      double tot[Cfg::kMi][Cfg::kNi][4];
+#pragma unroll
+      for (int mi = 0; mi < Cfg::kMi; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < Cfg::kNi; ++ni)
+#pragma unroll
+          for (int r = 0; r < 4; ++r) tot[mi][ni][r] = 0.0;
+      for (int sg = 1; sg < nseg; ++sg) {
+        const double* slot = slot_base + int64_t(sg) * kFrag * Cfg::kThreads;
+        int f = 0;
+#pragma unroll
+        for (int mi = 0; mi < Cfg::kMi; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < Cfg::kNi; ++ni)
+#pragma unroll
+            for (int r = 0; r < 4; ++r, ++f)
+              tot[mi][ni][r] += __ldcg(slot + f * Cfg::kThreads + threadIdx.x);
+      }
+#pragma unroll
+      for (int mi = 0; mi < Cfg::kMi; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < Cfg::kNi; ++ni)
+#pragma unroll
+          for (int r = 0; r < 4; ++r) tot[mi][ni][r] += acc[mi][ni][r];
+      gemm_tile_store<Cfg>(p, tm, tn, 0, epi, tot);
+    }
+    u = tile * ktiles + kt1;
   }
 }
 
@@ -267,6 +399,58 @@ void launch_gemm_cfg(const GemmProblem& p, const Epi& epi, cudaStream_t stream) 
 template <class Epi>
 void launch_gemm(const GemmProblem& p, const Epi& epi, cudaStream_t stream) {
   launch_gemm_cfg<GemmTile>(p, epi, stream);
+}
+
+// Stream-K launch for a single (batch 1) GEMM when its tiles would leave CTA slots idle
+// (opt-in, STKG_STREAMK=1: measured slower than one tile per CTA at the 1k^3 wave shape,
+// 0.296 vs 0.262 ms per modal preconditioner solve -- DESIGN.md K2); falls back to the
+// one-tile-per-CTA kernel otherwise.  ws is the caller's workspace (grown here; the
+// caller's stream orders its reuse).
+template <class Epi>
+void launch_gemm_streamk(const GemmProblem& p, const Epi& epi, cudaStream_t stream,
+                         StreamKWork& ws) {
+  using Cfg = GemmTile;
+  static const bool enabled = [] {
+    const char* e = std::getenv("STKG_STREAMK");
+    return e && e[0] == '1';
+  }();
+  static const int per_sm = [] {
+    STKG_CUDA_CHECK(cudaFuncSetAttribute(gemm_f64_streamk_kernel<Cfg, Epi>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(Cfg::kSmemBytes)));
+    int b = 0;
+    STKG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &b, gemm_f64_streamk_kernel<Cfg, Epi>, Cfg::kThreads, Cfg::kSmemBytes));
+    return std::max(b, 1);
+  }();
+  const int64_t tiles = ceil_div(p.M, Cfg::BM) * ceil_div(p.N, Cfg::BN);
+  const int64_t ktiles = ceil_div(p.K, Cfg::BK);
+  const int64_t slots = int64_t(num_sms()) * per_sm;
+  if (!enabled || p.batch != 1 || tiles >= slots || tiles == 0 ||
+      ktiles * tiles < slots * 2) {
+    launch_gemm(p, epi, stream);
+    return;
+  }
+  constexpr int kFrag = Cfg::kMi * Cfg::kNi * 4;
+  if (ws.tiles_cap < tiles) {
+    STKG_CUDA_CHECK(cudaStreamSynchronize(stream));
+    if (ws.partials) STKG_CUDA_CHECK(cudaFree(ws.partials));
+    if (ws.flags) STKG_CUDA_CHECK(cudaFree(ws.flags));
+    STKG_CUDA_CHECK(cudaMalloc(&ws.partials, sizeof(double) * tiles * StreamKWork::kMaxSeg *
+                                                 kFrag * Cfg::kThreads));
+    STKG_CUDA_CHECK(cudaMalloc(&ws.flags, sizeof(unsigned) * tiles * StreamKWork::kMaxSeg));
+    STKG_CUDA_CHECK(cudaMemsetAsync(ws.flags, 0, sizeof(unsigned) * tiles * StreamKWork::kMaxSeg,
+                                    stream));
+    ws.tiles_cap = tiles;
+  }
+  // every split tile has at most kMaxSeg segments: each CTA's range covers >= 2 K-tiles' worth
+  STKG_REQUIRE(ktiles * tiles / slots >= (ktiles + StreamKWork::kMaxSeg - 2) / (StreamKWork::kMaxSeg - 1),
+               STKG_ARGUMENT, "stream-K: too many segments per tile");
+  ws.epoch = ws.epoch + 1 == 0 ? 1 : ws.epoch + 1;
+  gemm_f64_streamk_kernel<Cfg, Epi><<<static_cast<unsigned>(slots), Cfg::kThreads,
+                                      Cfg::kSmemBytes, stream>>>(p, epi, ws.partials, ws.flags,
+                                                                 ws.epoch);
+  STKG_CUDA_CHECK(cudaGetLastError());
 }
 
 }  // namespace stkg

@@ -43,6 +43,11 @@ struct stkg_wave {
   DevBuf mb;
   std::vector<double> modal_a;  // a_i = (X_s^T A_h X_s)_ii, host copy
   Krylov krylov;             // GMRES / PCG workspace (basis grows on demand)
+  StreamKWork sk;            // stream-K GEMM workspace (1k^3 preconditioner products)
+  ~stkg_wave() {
+    if (sk.partials) cudaFree(sk.partials);
+    if (sk.flags) cudaFree(sk.flags);
+  }
 };
 
 namespace {
@@ -590,7 +595,7 @@ void modal_banded_solve(stkg_wave& w, const double* v, double* out) {
   // t1 = Xs^T V
   p.M = nh; p.K = nh; p.N = nt;
   p.A = w.XsT.p; p.lda = nh; p.B = v; p.ldb = nh; p.C = w.t1.p; p.ldc = nh;
-  launch_gemm(p, EpiStore{}, w.stream);
+  launch_gemm_streamk(p, EpiStore{}, w.stream, w.sk);
   // rows of t1 <- K_i^-1 rows (STKG_MB_CHUNKS: time chunks per mode, 1 = sequential kernel)
   static const int chunks = [] {
     const char* e = std::getenv("STKG_MB_CHUNKS");
@@ -621,7 +626,7 @@ void modal_banded_solve(stkg_wave& w, const double* v, double* out) {
   // out = Xs t1
   p.M = nh; p.K = nh; p.N = nt;
   p.A = w.Xs.p; p.lda = nh; p.B = w.t1.p; p.ldb = nh; p.C = out; p.ldc = nh;
-  launch_gemm(p, EpiStore{}, w.stream);
+  launch_gemm_streamk(p, EpiStore{}, w.stream, w.sk);
 }
 
 void two_term_solve(stkg_wave& w, const double* v, double* out) {
@@ -631,18 +636,18 @@ void two_term_solve(stkg_wave& w, const double* v, double* out) {
   // t1 = Xs^T V   (stk/sylvester.hpp:171, evaluated left to right as Eigen does)
   p.M = nh; p.K = nh; p.N = nt;
   p.A = w.XsT.p; p.lda = nh; p.B = v; p.ldb = nh; p.C = w.t1.p; p.ldc = nh;
-  launch_gemm(p, EpiStore{}, w.stream);
+  launch_gemm_streamk(p, EpiStore{}, w.stream, w.sk);
   // t2 = (t1 Xt) ./ (lambda_i + theta_j)   (:172-174)
   p.M = nh; p.K = nt; p.N = nt;
   p.A = w.t1.p; p.lda = nh; p.B = w.Xt.p; p.ldb = nt; p.C = w.t2.p; p.ldc = nh;
-  launch_gemm(p, EpiDivide{w.lam.p, w.theta.p}, w.stream);
+  launch_gemm_streamk(p, EpiDivide{w.lam.p, w.theta.p}, w.stream, w.sk);
   // t1 = Xs t2 ; out = t1 Xt^T   (:175)
   p.M = nh; p.K = nh; p.N = nt;
   p.A = w.Xs.p; p.lda = nh; p.B = w.t2.p; p.ldb = nh; p.C = w.t1.p; p.ldc = nh;
-  launch_gemm(p, EpiStore{}, w.stream);
+  launch_gemm_streamk(p, EpiStore{}, w.stream, w.sk);
   p.M = nh; p.K = nt; p.N = nt;
   p.A = w.t1.p; p.lda = nh; p.B = w.XtT.p; p.ldb = nt; p.C = out; p.ldc = nh;
-  launch_gemm(p, EpiStore{}, w.stream);
+  launch_gemm_streamk(p, EpiStore{}, w.stream, w.sk);
 }
 
 // The plan's preconditioner for GMRES / PCG / refinement.

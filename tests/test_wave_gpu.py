@@ -312,3 +312,35 @@ def test_modal_banded_chunked_substitution_vs_oracle(stk, orc, cuda, nh, nt):
     # FP64 evaluation of P w is no sharper); the Krylov solves' true residuals are the
     # accuracy check that matters (test_modal_banded_pcg_and_gmres, cfg4 test)
     assert rel(w, W.modal_banded(v)) < 1e-7
+
+
+_SK_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_1912_10082_b200 as stk
+sm = stk.wave_space_matrices(stk.SpaceGrid1D(0.0, 1.0, 300))
+tm = stk.wave_time_matrices(stk.TimeGrid(320, 1.0))
+plan = stk.WavePlan(sm, tm)
+v = torch.from_numpy(np.random.default_rng(5).standard_normal(plan.N)).cuda()
+out = {"tt": plan.two_term_solve(v).cpu().numpy(), "mb": plan.modal_banded_solve(v).cpu().numpy()}
+np.savez(sys.argv[2], **out)
+"""
+
+
+def test_streamk_gemm_matches_default(tmp_path):
+    """The opt-in stream-K GEMM schedule (STKG_STREAMK=1: split tiles finished by their first
+    segment's CTA, later segments' partials added in fixed order) gives the preconditioner
+    products of the one-tile-per-CTA kernel to rounding."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = str(Path(__file__).resolve().parent.parent)
+    res = {}
+    for v in ("1", "0"):
+        f = tmp_path / f"sk{v}.npz"
+        subprocess.run([sys.executable, "-c", _SK_SCRIPT, root, str(f)], check=True,
+                       env=dict(os.environ, STKG_STREAMK=v))
+        res[v] = dict(np.load(f))
+    for k in res["0"]:
+        assert rel(res["1"][k], res["0"][k]) < 1e-12, k
