@@ -144,6 +144,9 @@ def test_plan_level_errors(stk, cuda):
         plan.apply(F)
     with pytest.raises(stk.ArgumentError, match="alias"):
         plan.solve(F, out=F)
+    big = torch.zeros((5, 15), dtype=torch.float64, device="cuda")  # partial overlap
+    with pytest.raises(stk.ArgumentError, match="alias"):
+        plan.solve(big[:4], out=big[1:])
     p2 = stk.HeatPlan.p1_uniform(1, 15, 4)
     L = torch.ones((1, 15), dtype=torch.float64, device="cuda")
     R = torch.ones((1, 4), dtype=torch.float64, device="cuda")
