@@ -44,6 +44,9 @@ struct stkg_wave {
   std::vector<double> modal_a;  // a_i = (X_s^T A_h X_s)_ii, host copy
   Krylov krylov;             // GMRES / PCG workspace (basis grows on demand)
   StreamKWork sk;            // stream-K GEMM workspace (1k^3 preconditioner products)
+  DevBuf ref_r, ref_d;       // refinement residual / correction, kept across calls (a per-call
+                             // cudaMalloc + cudaFree synchronises the device: 10 -> 64 ms
+                             // swings for the config-4 refined solve)
   ~stkg_wave() {
     if (sk.partials) cudaFree(sk.partials);
     if (sk.flags) cudaFree(sk.flags);
@@ -806,11 +809,10 @@ int stkg_wave_residual_dd(stkg_wave* wv, const double* b, const double* x_hi,
     STKG_REQUIRE(wv && b && x_hi && relres, STKG_ARGUMENT, "residual_dd: null argument");
     stkg_wave& w = *wv;
     w.krylov.ensure(0, 0);
-    DevBuf tmp;
     double* rr = r;
     if (!rr) {
-      tmp.alloc(w.N);
-      rr = tmp.p;
+      if (w.ref_r.n < static_cast<size_t>(w.N)) w.ref_r.alloc(w.N);
+      rr = w.ref_r.p;
     }
     *relres = residual_dd(w, b, x_hi, x_lo, rr);
   });
@@ -829,7 +831,10 @@ int stkg_wave_solve_refined(stkg_wave* wv, const double* b, double* x_hi, double
     w.krylov.ensure(0, 0);
     const DevOp apply = [&](const double* in, double* out) { apply_op(w, in, out); };
     const DevOp precond = [&](const double* in, double* out) { precond_solve(w, in, out); };
-    DevBuf r(w.N), d(w.N);
+    if (w.ref_r.n < static_cast<size_t>(w.N)) w.ref_r.alloc(w.N);
+    if (w.ref_d.n < static_cast<size_t>(w.N)) w.ref_d.alloc(w.N);
+    DevBuf& r = w.ref_r;
+    DevBuf& d = w.ref_d;
     STKG_CUDA_CHECK(cudaMemsetAsync(x_hi, 0, sizeof(double) * w.N, w.stream));
     STKG_CUDA_CHECK(cudaMemsetAsync(x_lo, 0, sizeof(double) * w.N, w.stream));
     int total = 0, len = 0;
