@@ -96,10 +96,10 @@ __device__ __forceinline__ void heat_fused_axis0_body(const CUtensorMap& map, ST
   using SC = typename C::B;
   using OP = OutPair<N, 4>;
   constexpr int V = C::V, T = C::T, P = C::P, n = N - 1, RG = C::kRegion;
-  extern __shared__ __align__(1024) unsigned char sraw[];
-  unsigned char* sbase = sraw;
+  extern __shared__ __align__(1024) unsigned char fsraw[];
+  unsigned char* sbase = fsraw;
   if constexpr (TMA) {  // the SWIZZLE_64B tile needs a 512-byte aligned destination
-    if ((static_cast<unsigned>(__cvta_generic_to_shared(sraw)) & 511u) != 0u) __trap();
+    if ((static_cast<unsigned>(__cvta_generic_to_shared(fsraw)) & 511u) != 0u) __trap();
   }
   double2* sreg = reinterpret_cast<double2*>(sbase);
   double2* stile = reinterpret_cast<double2*>(sbase + C::kTileOff);
