@@ -716,6 +716,10 @@ for n, nt in [(1023, 40), (1023, 37), (511, 64)]:
     U2 = p.solve(Fd)  # repeated: tickets and events reused
     out[f"v{n}_{nt}"] = U2.cpu().numpy()
     out[f"r{n}_{nt}"] = np.array(p.residual(U, Fd)[0])
+# host-buffer path in 40-slice chunks: the overlapped schedule with carried modes (l0 > 0)
+F = np.random.default_rng(3).standard_normal((80, 1023 * 1023))
+ph = stk.HeatPlan.p1_uniform(2, 1023, 80, transform="dst", time_chunk=40)
+out["h1023_80"] = ph.solve_host(F)
 np.savez(sys.argv[2], **out)
 """
 
