@@ -355,6 +355,7 @@ namespace {
 // only polls `done` every kPcgChunk iterations.
 struct PcgState {
   double rz, pq, alpha, beta, normb, tol;
+  double rel_prev, rel_last;  // the last two relative residuals (sizing the next chunk)
   int done, iters, error, maxit;
 };
 constexpr int kPcgChunk = 8;
@@ -378,6 +379,7 @@ __global__ void __launch_bounds__(kReduceThreads) pcg_init_kernel(const double* 
     st->done = 0;
     st->iters = 0;
     st->error = 0;
+    st->rel_prev = st->rel_last = 1.0;
   }
 }
 
@@ -423,6 +425,8 @@ __global__ void __launch_bounds__(kReduceThreads) pcg_check_kernel(const double*
   if (threadIdx.x == 0) {
     const double relres = sqrt(r2) / st->normb;
     hist[st->iters] = relres;
+    st->rel_prev = st->rel_last;
+    st->rel_last = relres;
     st->iters += 1;
     if (!isfinite(relres)) {
       st->error = 2;
@@ -508,8 +512,9 @@ void pcg_run(Krylov& k, const DevOp& apply, const DevOp& precond, const double* 
   PcgState hs{};
   k.pin(sizeof(PcgState) / 8 + 1);
   int enqueued = 0;
+  int chunk = kPcgChunk;
   while (true) {
-    for (int c = 0; c < kPcgChunk && enqueued < maxit; ++c, ++enqueued) {
+    for (int c = 0; c < chunk && enqueued < maxit; ++c, ++enqueued) {
       apply(p, q);
       pcg_dot_kernel<<<kReduceBlocks, kReduceThreads, 0, s>>>(st, p, q, N, k.partials.p);
       pcg_alpha_kernel<<<1, kReduceThreads, 0, s>>>(k.partials.p, st);
@@ -525,6 +530,15 @@ void pcg_run(Krylov& k, const DevOp& apply, const DevOp& precond, const double* 
     STKG_CUDA_CHECK(cudaStreamSynchronize(s));
     std::memcpy(&hs, k.pinned, sizeof(PcgState));
     if (hs.done || enqueued >= maxit) break;
+    // size the next chunk from the observed contraction (iterations past convergence still
+    // launch their kernels, as no-ops): a rapidly converging preconditioner (the modal banded
+    // one needs ~9 iterations) otherwise pays up to kPcgChunk - 1 wasted iterations
+    chunk = kPcgChunk;
+    if (hs.iters >= 2 && hs.rel_prev > 0.0 && hs.rel_last > 0.0 && hs.rel_last < hs.rel_prev) {
+      const double rho = hs.rel_last / hs.rel_prev;
+      const double need = std::log(tol / hs.rel_last) / std::log(rho);
+      if (need > 0.0 && need < kPcgChunk) chunk = std::max(1, static_cast<int>(std::ceil(need)) + 1);
+    }
   }
   k.skip = nullptr;  // the true-residual apply below must run
   if (hs.error == 1)
