@@ -27,6 +27,7 @@
 #include "dst.cuh"
 #include "dst_half.cuh"
 #include "heat_fused.cuh"  // K2b + K3: time-marching fused axis-0 pass
+#include "heat_tridiag.cuh"  // K2e: time-marching line-solve axis-0 pass (uniform time grids)
 #include "gemm_f64.cuh"
 #include "heat_plan.cuh"
 #include "heat_scan.cuh"   // K3: modal recurrences
@@ -378,6 +379,54 @@ void launch_fused_axis0(const stkg_heat& h, double* S, int64_t inner, int64_t nt
   STKG_CUDA_CHECK(cudaGetLastError());
 }
 
+// Time-marching line-solve pass over axis 0 (heat_tridiag.cuh): one tridiagonal solve per
+// column and slice instead of the two transforms; plans with h.tri_ok.
+template <int N, int P, int ST = 3>
+void launch_tridiag_axis0(const stkg_heat& h, double* S, int64_t inner, int64_t ntc, int64_t l0) {
+  using C = TriCfg<N, P, ST>;
+  auto kern = heat_tridiag_axis0_kernel<N, P, ST>;
+  static const bool configured = [kern] {
+    STKG_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(C::kSmem)));
+    return true;
+  }();
+  (void)configured;
+  const int64_t tiles = inner / C::G;
+  const double ds = h.nt > 1 ? h.d_sup_h[0] : 0.0, cs = h.nt > 1 ? h.c_sup_h[0] : 0.0;
+  kern<<<static_cast<unsigned>(tiles), C::kThreads, C::kSmem, launch_stream(h)>>>(
+      S, inner, h.n[0] * inner, ntc, l0, h.tri_iw.p, h.lam_col.p, h.w_col.p, h.d_diag_h[0], ds,
+      h.c_diag_h[0], cs, h.tri_md, h.tri_mo, h.tri_ad, h.tri_ao, h.carry.p);
+  STKG_CUDA_CHECK(cudaGetLastError());
+}
+
+// Columns per line-solve tile for axis-0 length n0 (0: no such kernel for that length).
+int64_t tri_tile_cols(int64_t n0) {
+  switch (n0 + 1) {
+    case 64: return 64;
+    case 128: return 64;
+    case 256: return 32;
+    case 512: return 16;
+    case 1024: return 8;
+    default: return 0;
+  }
+}
+
+void tridiag_axis0(const stkg_heat& h, double* S, int64_t inner, int64_t ntc, int64_t l0) {
+  switch (h.n[0] + 1) {
+    case 64: return launch_tridiag_axis0<64, 32>(h, S, inner, ntc, l0);
+    case 128: return launch_tridiag_axis0<128, 32>(h, S, inner, ntc, l0);
+    case 256: return launch_tridiag_axis0<256, 16>(h, S, inner, ntc, l0);
+    case 512: return launch_tridiag_axis0<512, 8>(h, S, inner, ntc, l0);
+    case 1024: return launch_tridiag_axis0<1024, 4>(h, S, inner, ntc, l0);
+    default: throw Error(STKG_ARGUMENT, "line-solve pass: unsupported axis length");
+  }
+}
+
+bool use_tridiag(const stkg_heat& h, int64_t inner) {
+  const int64_t G = tri_tile_cols(h.n[0]);
+  return h.tri_ok && G > 0 && inner % G == 0;
+}
+
 // Columns per fused tile for axis-0 length n0 (0: no fused kernel for that length).
 int64_t fused_tile_cols(int64_t n0) {
   switch (n0 + 1) {
@@ -405,9 +454,14 @@ int fused_mode() {
   return m;
 }
 
+// Columns per tile of whichever time-marching axis-0 pass the plan runs.
+int64_t axis0_tile_cols(const stkg_heat& h, int64_t inner) {
+  return use_tridiag(h, inner) ? tri_tile_cols(h.n[0]) : fused_tile_cols(h.n[0]);
+}
+
 bool use_fused_axis0(const stkg_heat& h, int64_t inner) {
   if (h.pitch <= 0 || h.lam_col.p == nullptr) return false;
-  const int64_t G = fused_tile_cols(h.n[0]);
+  const int64_t G = axis0_tile_cols(h, inner);
   if (G == 0 || inner % G != 0) return false;
   const int m = fused_mode();
   if (m == 0) return false;
@@ -416,6 +470,7 @@ bool use_fused_axis0(const stkg_heat& h, int64_t inner) {
 }
 
 void fused_axis0(const stkg_heat& h, double* S, int64_t inner, int64_t ntc, int64_t l0) {
+  if (use_tridiag(h, inner)) return tridiag_axis0(h, S, inner, ntc, l0);
   switch (h.n[0] + 1) {
     case 16: return launch_fused_axis0<16>(h, S, inner, ntc, l0);
     case 32: return launch_fused_axis0<32>(h, S, inner, ntc, l0);
@@ -668,7 +723,7 @@ void run_chunk_padded(stkg_heat& h, const double* F, double* U, double* S, int64
   for (int b = 1; b < last; ++b) inner0 *= h.n[b];
   const bool fused = use_fused_axis0(h, inner0);
   if (fused && d == 2 && !h.prof_on && overlap_chunks() > 1 &&
-      ntc >= 8 * overlap_chunks() && inner0 / fused_tile_cols(h.n[0]) < num_sms()) {
+      ntc >= 8 * overlap_chunks() && inner0 / axis0_tile_cols(h, inner0) < num_sms()) {
     run_chunk_padded_overlap(h, F, U, S, l0, ntc, overlap_chunks(), inner0);
     return;
   }
@@ -930,6 +985,55 @@ std::vector<double> transpose(const double* X, int64_t n) {
 
 }  // namespace
 
+namespace {
+// STKG_TRIDIAG=0 keeps the transform-based fused pass (heat_fused.cuh).
+bool tridiag_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("STKG_TRIDIAG");
+    return !(e && std::atoi(e) == 0);
+  }();
+  return on;
+}
+
+// Line-solve axis-0 pass (heat_tridiag.cuh): uniform time grid, axis 0 a uniform P1 axis whose
+// pencil the caller's eigenvalues confirm (lambda_k mu_k = a_d + 2 a_o cos(pi k / N) with the
+// P1 stencils M_0 = (h/6) tridiag(1, 4, 1), A_0 = (1/h) tridiag(-1, 2, -1)), every column's
+// T_c positive definite.  Otherwise the plan keeps the transform-based pass.
+void setup_tridiag(stkg_heat& h, const double* lam0, double hh) {
+  h.tri_ok = false;
+  if (!tridiag_enabled() || !h.uniform_time || h.pitch <= 0 || h.lam_col.p == nullptr) return;
+  const int64_t n0 = h.n[0], N = n0 + 1;
+  if (tri_tile_cols(n0) == 0) return;
+  const double md = 2.0 * hh / 3.0, mo = hh / 6.0, ad = 2.0 / hh, ao = -1.0 / hh;
+  for (int64_t k = 1; k <= n0; ++k) {
+    const double ck = cospi_ratio(k, N);
+    const double alpha = lam0[k - 1] * (md + 2.0 * mo * ck), want = ad + 2.0 * ao * ck;
+    if (!(std::fabs(alpha - want) <= 1e-9 * ad)) return;
+  }
+  int64_t inner = h.pitch;
+  for (int b = 1; b + 1 < h.ndim; ++b) inner *= h.n[b];
+  if (inner % tri_tile_cols(n0) != 0) return;
+  h.tri_md = md, h.tri_mo = mo, h.tri_ad = ad, h.tri_ao = ao;
+  h.tri_iw.alloc(static_cast<size_t>(N * inner));
+  int* bad = nullptr;
+  STKG_CUDA_CHECK(cudaMalloc(&bad, sizeof(int)));
+  STKG_CUDA_CHECK(cudaMemsetAsync(bad, 0, sizeof(int), h.stream));
+  tri_factor_kernel<<<static_cast<unsigned>(ceil_div(inner, 128)), 128, 0, h.stream>>>(
+      h.tri_iw.p, inner, static_cast<int>(n0), h.lam_col.p, h.d_diag_h[0], h.c_diag_h[0], md, mo,
+      ad, ao, bad);
+  int hb = 1;
+  cudaError_t e1 = cudaGetLastError();
+  cudaError_t e2 = cudaMemcpyAsync(&hb, bad, sizeof hb, cudaMemcpyDeviceToHost, h.stream);
+  cudaError_t e3 = cudaStreamSynchronize(h.stream);
+  cudaFree(bad);
+  STKG_CUDA_CHECK(e1);
+  STKG_CUDA_CHECK(e2);
+  STKG_CUDA_CHECK(e3);
+  h.tri_ok = hb == 0;
+  if (!h.tri_ok) h.tri_iw.release();
+}
+}  // namespace
+
 // ------------------------------------------------------------------------ C ABI -----
 extern "C" {
 
@@ -1109,6 +1213,7 @@ int stkg_heat_create(stkg_heat** out, const stkg_heat_desc* desc, void* cuda_str
           h->w_col.upload(wc.data(), wc.size(), s);
         }
         STKG_CUDA_CHECK(cudaStreamSynchronize(s));
+        setup_tridiag(*h, desc->lambdas[0], desc->p1_h[0]);
       }
     }
     h->carry.alloc(h->pitch > 0 ? padded_nx(*h) : h->nx);

@@ -52,6 +52,11 @@ struct stkg_heat {
   int64_t pitch = 0;
   DevBuf lam_pad, inv_mu_pad;
   DevBuf lam_col, w_col;  // fused axis-0 pass: per-column lambda sum / weight product
+  // line-solve axis-0 pass (heat_tridiag.cuh): reciprocal pivots [N_0][columns] and the
+  // axis-0 P1 stencil entries; tri_ok: the plan runs it instead of the transform-based pass
+  DevBuf tri_iw;
+  bool tri_ok = false;
+  double tri_md = 0.0, tri_mo = 0.0, tri_ad = 0.0, tri_ao = 0.0;
   bool uniform_time = false;  // all temporal bidiagonal coefficients equal (factored scan)
   DevBuf d_diag, d_sup, c_diag, c_sup;
   // host copies used by the host-side parts of the rational Krylov solver
