@@ -399,6 +399,49 @@ void launch_tridiag_axis0(const stkg_heat& h, double* S, int64_t inner, int64_t 
   STKG_CUDA_CHECK(cudaGetLastError());
 }
 
+// STKG_TRI_V: 1 (default) = TMA tile staging and stores, 0 = cp.async staging.
+int tri_variant() {
+  static const int v = [] {
+    const char* e = std::getenv("STKG_TRI_V");
+    return e ? std::atoi(e) : 1;
+  }();
+  return v;
+}
+
+template <int N, int P>
+void launch_tridiag_tma(const stkg_heat& h, double* S, int64_t inner, int64_t ntc, int64_t l0) {
+  using C = TriTmaCfg<N, P>;
+  auto kern = heat_tridiag_tma_kernel<N, P>;
+  static const bool configured = [kern] {
+    STKG_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(C::kSmem)));
+    return true;
+  }();
+  (void)configured;
+  // the launch's slices as [ntc][n_0][inner]: rows >= n_0 are out of bounds (zero-filled on
+  // load, clipped on store)
+  CUtensorMap map;
+  std::memset(&map, 0, sizeof map);
+  const cuuint64_t dims[3] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(h.n[0]),
+                              static_cast<cuuint64_t>(ntc)};
+  const cuuint64_t strides[2] = {static_cast<cuuint64_t>(inner * sizeof(double)),
+                                 static_cast<cuuint64_t>(h.n[0] * inner * sizeof(double))};
+  const cuuint32_t box[3] = {C::CW / 8, C::BR, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = tensor_map_encoder()(
+      &map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, S, dims, strides, box, estr,
+      CU_TENSOR_MAP_INTERLEAVE_NONE,
+      C::CW == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B, tma_promotion(),
+      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  STKG_REQUIRE(r == CUDA_SUCCESS, STKG_CUDA, "cuTensorMapEncodeTiled failed (line-solve pass)");
+  const int64_t tiles = inner / C::G;
+  const double ds = h.nt > 1 ? h.d_sup_h[0] : 0.0, cs = h.nt > 1 ? h.c_sup_h[0] : 0.0;
+  kern<<<static_cast<unsigned>(tiles), C::kThreads, C::kSmem, launch_stream(h)>>>(
+      map, inner, ntc, l0, h.lam_col.p, h.w_col.p, h.d_diag_h[0], ds, h.c_diag_h[0], cs, h.tri_md,
+      h.tri_mo, h.tri_ad, h.tri_ao, h.carry.p);
+  STKG_CUDA_CHECK(cudaGetLastError());
+}
+
 // Columns per line-solve tile for axis-0 length n0 (0: no such kernel for that length).
 int64_t tri_tile_cols(int64_t n0) {
   switch (n0 + 1) {
@@ -412,6 +455,20 @@ int64_t tri_tile_cols(int64_t n0) {
 }
 
 void tridiag_axis0(const stkg_heat& h, double* S, int64_t inner, int64_t ntc, int64_t l0) {
+  const bool tma_ok = (reinterpret_cast<uintptr_t>(S) & 15) == 0 && inner < (int64_t(1) << 31) &&
+                      ntc < (int64_t(1) << 31);
+  STKG_REQUIRE(tri_variant() == 0 || tma_ok, STKG_ARGUMENT,
+               "line-solve pass: scratch not addressable by a tensor map");
+  if (tri_variant() != 0) {
+    switch (h.n[0] + 1) {
+      case 64: return launch_tridiag_tma<64, 32>(h, S, inner, ntc, l0);
+      case 128: return launch_tridiag_tma<128, 32>(h, S, inner, ntc, l0);
+      case 256: return launch_tridiag_tma<256, 16>(h, S, inner, ntc, l0);
+      case 512: return launch_tridiag_tma<512, 8>(h, S, inner, ntc, l0);
+      case 1024: return launch_tridiag_tma<1024, 4>(h, S, inner, ntc, l0);
+      default: break;
+    }
+  }
   switch (h.n[0] + 1) {
     case 64: return launch_tridiag_axis0<64, 32>(h, S, inner, ntc, l0);
     case 128: return launch_tridiag_axis0<128, 32>(h, S, inner, ntc, l0);
@@ -1014,13 +1071,31 @@ void setup_tridiag(stkg_heat& h, const double* lam0, double hh) {
   for (int b = 1; b + 1 < h.ndim; ++b) inner *= h.n[b];
   if (inner % tri_tile_cols(n0) != 0) return;
   h.tri_md = md, h.tri_mo = mo, h.tri_ad = ad, h.tri_ao = ao;
+  // every column's T_c = tridiag(a, b, a) must have a positive symbol (b > 2|a|) and a decay
+  // q = |a| / w with q^N well below 1 (the image sums divide by 1 - q^{2N})
+  std::vector<double> lc(static_cast<size_t>(inner));
+  STKG_CUDA_CHECK(cudaMemcpyAsync(lc.data(), h.lam_col.p, inner * sizeof(double),
+                                  cudaMemcpyDeviceToHost, h.stream));
+  STKG_CUDA_CHECK(cudaStreamSynchronize(h.stream));
+  const double dd = h.d_diag_h[0], cd = h.c_diag_h[0];
+  for (int64_t c = 0; c < inner; ++c) {
+    const double p = dd + lc[c] * cd;
+    const double a = p * mo + cd * ao, b = p * md + cd * ad;
+    const double bp = p * (md + 2.0 * mo) + cd * (ad + 2.0 * ao);
+    const double bm = p * (md - 2.0 * mo) + cd * (ad - 2.0 * ao);
+    if (!(b > 0.0 && bp > 0.0 && bm > 0.0)) return;
+    const double q = std::fabs(a) / (0.5 * (b + std::sqrt(bp * bm)));
+    if (!(std::pow(q, static_cast<double>(N)) < 0.25)) return;
+  }
+  h.tri_ok = true;
+  if (tri_variant() != 0) return;
+  // the cp.async LDL^T variant keeps a table of reciprocal pivots
   h.tri_iw.alloc(static_cast<size_t>(N * inner));
   int* bad = nullptr;
   STKG_CUDA_CHECK(cudaMalloc(&bad, sizeof(int)));
   STKG_CUDA_CHECK(cudaMemsetAsync(bad, 0, sizeof(int), h.stream));
   tri_factor_kernel<<<static_cast<unsigned>(ceil_div(inner, 128)), 128, 0, h.stream>>>(
-      h.tri_iw.p, inner, static_cast<int>(n0), h.lam_col.p, h.d_diag_h[0], h.c_diag_h[0], md, mo,
-      ad, ao, bad);
+      h.tri_iw.p, inner, static_cast<int>(n0), h.lam_col.p, dd, cd, md, mo, ad, ao, bad);
   int hb = 1;
   cudaError_t e1 = cudaGetLastError();
   cudaError_t e2 = cudaMemcpyAsync(&hb, bad, sizeof hb, cudaMemcpyDeviceToHost, h.stream);

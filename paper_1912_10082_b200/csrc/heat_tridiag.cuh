@@ -323,4 +323,361 @@ __global__ void __launch_bounds__(TriCfg<N, PP, ST>::kThreads, 1)
   }
 }
 
+
+// ---------------------------------------------------------------------------------------
+// TMA variant (the default): the tile of slice j is loaded by cp.async.bulk.tensor boxes into
+// one of two input buffers (full / empty mbarriers; the load of slice j + 2 is issued as soon
+// as every thread has read slice j's tile, early in step j, so two slices are in flight) and
+// the solved tile leaves from an output buffer by a bulk tensor store; no thread copies data.
+// The tensor map views the launch's slices as [ntc][n_0 rows][inner columns]: rows past n_0
+// are zero-filled on load and clipped on store, so the phantom rows need no special case.
+// A thread owns R = 17 rows (odd): rows 17 t + k of 8 consecutive t differ in their low three
+// bits, so TMA's own SWIZZLE_64B / SWIZZLE_128B row mirrors are read and written
+// bank-conflict free (with 16-row chunks every lane of a quarter-warp would hit one bank group).
+template <int N, int PP>
+struct TriTmaCfg {
+  static constexpr int R = 17, T = N / 16, P = PP, G = 2 * PP, kThreads = PP * T, n = N - 1;
+  static constexpr int W = T < 32 ? T : 32, LW = tri_ilog2(W);
+  static constexpr int CW = P >= 8 ? 128 : 64;          // bytes per smem row of one column box
+  static constexpr int CPB = CW / 16;                   // column pairs per column box
+  static constexpr int NCB = P / CPB;                   // column boxes
+  static constexpr int BR = N < 256 ? N : 256;          // rows per TMA box
+  static constexpr int NRB = N / BR;                    // row boxes
+  static constexpr int kRows = (T * R + 7) / 8 * 8;     // buffer rows (every lane's chunk)
+  static constexpr int kBufBytes = NCB * kRows * CW;    // one tile buffer
+  static constexpr unsigned kTxBytes = unsigned(NCB) * NRB * BR * CW;
+  static constexpr size_t kXchOff = size_t(3) * kBufBytes;
+  static constexpr size_t kBarOff = kXchOff + size_t(P) * 8 * sizeof(double2);
+  static constexpr size_t kSmem = kBarOff + 8 * sizeof(uint64_t);
+  static_assert(P == 4 || P % 8 == 0, "64-byte rows or whole 128-byte column boxes");
+  static_assert(T >= 2 && (T <= 32 || T == 64), "2..32 lanes or two warps per column pair");
+  static_assert(T * R >= N, "the chunks cover every row");
+  static_assert(kBufBytes % 1024 == 0, "buffers keep the swizzle pattern's alignment");
+};
+
+__device__ __forceinline__ void tma_load_3d(void* smem, const CUtensorMap* map, int c0, int c1,
+                                            int c2, uint64_t* bar) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  const unsigned b = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(s),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(b)
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, int c0, int c1, int c2,
+                                             const void* smem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile(
+      "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];\n" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(c0), "r"(c1), "r"(c2), "r"(s)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(a) : "memory");
+}
+
+// q^e for an integer e >= 0 (q may be negative or zero; 0^0 = 1).
+__device__ __forceinline__ double tri_ipow(double q, int e) {
+  double r = 1.0;
+  while (e > 0) {
+    if (e & 1) r *= q;
+    q *= q;
+    e >>= 1;
+  }
+  return r;
+}
+
+// The solve itself uses the Toeplitz structure once more: T = tridiag(a, b, a) is the
+// restriction of the bi-infinite Toeplitz operator T_inf = L D L^T (constant pivot
+// w = (b + sqrt(b^2 - 4 a^2)) / 2, multiplier m = a / w, |m| < 1) to odd, 2N-periodic
+// sequences (method of images: the Dirichlet rows 0 and N are the mirror points).  With
+// q = -m and gamma = 1 / sqrt(b^2 - 4 a^2), T_inf^{-1} is the convolution with
+// gamma q^|k|, i.e. one causal and one anti-causal first-order recurrence with the CONSTANT
+// coefficient q:
+//     A_i = r_i + q A_{i-1},   B_i = r_i + q B_{i+1},   z_i = gamma (A_i + q B_{i+1})
+// whose start values follow from the two zero-start totals a_N = sum_j q^{N-j} r_j and
+// b_0 = sum_j q^j r_j:  A_0 = (q^N a_N - b_0) / (1 - q^{2N}),  B_N = -(q^N A_0 + a_N).
+// So no per-row pivots are stored at all (the LDL^T variant above keeps 17 reciprocal pivots
+// per column in registers); both zero-start recurrences and both chunk scans run side by
+// side, one barrier per step joins the two warps of a column pair, and r is recovered from
+// A in the second sweep (r_i = A_i - q A_{i-1}), so one register array holds z, r, A and z
+// again.
+template <int N, int PP>
+__global__ void __launch_bounds__(TriTmaCfg<N, PP>::kThreads, 1)
+    heat_tridiag_tma_kernel(const __grid_constant__ CUtensorMap map, int64_t inner, int64_t ntc,
+                            int64_t l0, const double* __restrict__ lam_col,
+                            const double* __restrict__ w_col, double dd, double ds, double cd,
+                            double cs, double md, double mo, double ad, double ao,
+                            double* __restrict__ carry) {
+  using C = TriTmaCfg<N, PP>;
+  constexpr int R = C::R, T = C::T, n = C::n, W = C::W, LW = C::LW, CW = C::CW;
+  extern __shared__ __align__(1024) unsigned char tmraw[];
+  if ((static_cast<unsigned>(__cvta_generic_to_shared(tmraw)) & 1023u) != 0u) __trap();
+  unsigned char* bin[2] = {tmraw, tmraw + C::kBufBytes};
+  unsigned char* bout = tmraw + 2 * C::kBufBytes;
+  double2* xch = reinterpret_cast<double2*>(tmraw + C::kXchOff);  // [P][8]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(tmraw + C::kBarOff);
+  uint64_t* full = bars;       // [2] tile landed (TMA transaction bytes)
+  uint64_t* empty = bars + 2;  // [2] every warp has read the tile
+  uint64_t* ofree = bars + 4;  // the previous store has read the output buffer
+  const int tid = threadIdx.x;
+  const int f = tid / T, t = tid % T;
+  const int sl = t & (W - 1);
+  const int bar = 1 + f;
+  const int i0 = static_cast<int>(blockIdx.x) * C::G;
+  const int64_t ca = i0 + 2 * f;
+  const int row0 = R * t;
+  const int cnt = n - row0 < 0 ? 0 : (n - row0 > R ? R : n - row0);  // real rows of this chunk
+  double2* xp = xch + f * 8;
+  // byte offset of this pair's 16-byte chunk in row r of a tile buffer (TMA swizzle)
+  const int cbase = (f / C::CPB) * (C::kRows * CW), cc = f % C::CPB;
+  auto off = [&](int r) {
+    const int sw = CW == 64 ? ((r >> 1) & 3) : (r & 7);
+    return cbase + r * CW + ((cc ^ sw) << 4);
+  };
+
+  // per-column constants (.x / .y: the pair's two columns)
+  double2 q, gam, sa, sb, wc, qc, gf, gb, qN, inv, pw0, pw1;
+  {
+    double qq[2], gg[2], s1[2], s2[2];
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const double la = lam_col[ca + c];
+      const double p = dd + la * cd;
+      const double a = p * mo + cd * ao, b = p * md + cd * ad;
+      const double bp = p * (md + 2.0 * mo) + cd * (ad + 2.0 * ao);  // b + 2a
+      const double bm = p * (md - 2.0 * mo) + cd * (ad - 2.0 * ao);  // b - 2a
+      const double sq = sqrt(bp * bm);
+      qq[c] = -a / (0.5 * (b + sq));
+      gg[c] = 1.0 / sq;
+      const double pq = ds + la * cs;
+      s1[c] = pq * mo + cs * ao;
+      s2[c] = pq * md + cs * ad;
+    }
+    q = make_double2(qq[0], qq[1]);
+    gam = make_double2(gg[0], gg[1]);
+    sa = make_double2(s1[0], s1[1]);
+    sb = make_double2(s2[0], s2[1]);
+    wc = make_double2(w_col[ca], w_col[ca + 1]);
+    const int above = row0 < n ? row0 : n;                      // real rows above the chunk
+    const int below = n - row0 - R > 0 ? n - row0 - R : 0;      // real rows below it
+    qc = make_double2(tri_ipow(q.x, cnt), tri_ipow(q.y, cnt));
+    gf = make_double2(tri_ipow(q.x, above), tri_ipow(q.y, above));
+    gb = make_double2(tri_ipow(q.x, below), tri_ipow(q.y, below));
+    qN = make_double2(tri_ipow(q.x, N), tri_ipow(q.y, N));
+    inv = make_double2(1.0 / (1.0 - qN.x * qN.x), 1.0 / (1.0 - qN.y * qN.y));
+    constexpr int lo_rows = 32 * R < n ? 32 * R : n;  // real rows of chunks 0..31
+    pw0 = make_double2(tri_ipow(q.x, lo_rows), tri_ipow(q.y, lo_rows));
+    pw1 = make_double2(tri_ipow(q.x, n - lo_rows), tri_ipow(q.y, n - lo_rows));
+  }
+
+  // zero the tile buffers once: rows the TMA boxes never write stay zero; barriers
+  for (int e = tid; e < 3 * C::kBufBytes / 16; e += C::kThreads)
+    reinterpret_cast<double2*>(tmraw)[e] = make_double2(0.0, 0.0);
+  if (tid == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    mbar_init(&empty[0], C::kThreads / 32);
+    mbar_init(&empty[1], C::kThreads / 32);
+    mbar_init(ofree, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // zeros before the TMA writes
+  __syncthreads();
+
+  auto issue_load = [&](int64_t j, int s) {  // one thread
+    mbar_arrive_expect_tx(&full[s], C::kTxBytes);
+#pragma unroll
+    for (int cb = 0; cb < C::NCB; ++cb)
+#pragma unroll
+      for (int rb = 0; rb < C::NRB; ++rb)
+        tma_load_3d(bin[s] + cb * (C::kRows * CW) + rb * (C::BR * CW), &map,
+                    i0 + cb * (CW / 8), rb * C::BR, static_cast<int>(j), &full[s]);
+  };
+  if (tid == 0) {
+    if (ntc > 0) issue_load(0, 0);
+    if (ntc > 1) issue_load(1, 1);
+  }
+
+  // z_{l0-1}: this thread's rows, the row above its first (zu) and below its last (zn)
+  double2 x[R], zn = make_double2(0.0, 0.0), zu = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    const int r = row0 + k;
+    x[k] = (l0 > 0 && r < n) ? *reinterpret_cast<const double2*>(carry + int64_t(r) * inner + ca)
+                             : make_double2(0.0, 0.0);
+  }
+  if (l0 > 0) {
+    if (row0 > 0 && row0 - 1 < n)
+      zu = *reinterpret_cast<const double2*>(carry + int64_t(row0 - 1) * inner + ca);
+    if (row0 + R < n) zn = *reinterpret_cast<const double2*>(carry + int64_t(row0 + R) * inner + ca);
+  }
+
+  for (int64_t j = 0; j < ntc; ++j) {
+    const int s = static_cast<int>(j & 1);
+    const unsigned ph = static_cast<unsigned>(j >> 1) & 1u;
+    if (j > 0) {  // the neighbours' edge rows of z_{l-1}
+      zu = shfl_up2(x[R - 1], 1, W);
+      zn = shfl_down2(x[0], 1, W);
+      if (sl == 0) zu = (T > 32 && t == 32) ? xp[4] : make_double2(0.0, 0.0);
+      if (sl == W - 1) zn = (T > 32 && t == 31) ? xp[5] : make_double2(0.0, 0.0);
+    }
+    mbar_wait(&full[s], ph);
+    // right-hand side in place: r_i = w_c g_i - sb z_i - sa (z_{i-1} + z_{i+1})
+    {
+      const unsigned char* tb = bin[s];
+      double2 zl = zu;
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        const double2 g = *reinterpret_cast<const double2*>(tb + off(row0 + k));
+        const double2 zc = x[k];
+        const double2 zr = k + 1 < R ? x[k + 1] : zn;
+        const double ra = fma(sb.x, zc.x, sa.x * (zl.x + zr.x));
+        const double rb = fma(sb.y, zc.y, sa.y * (zl.y + zr.y));
+        x[k] = k < cnt ? make_double2(fma(wc.x, g.x, -ra), fma(wc.y, g.y, -rb))
+                       : make_double2(0.0, 0.0);
+        zl = zc;
+      }
+    }
+    __syncwarp();
+    if ((tid & 31) == 0) mbar_arrive(&empty[s]);  // this warp's reads of the tile are done
+
+    // zero-start recurrences over the chunk, both directions
+    double2 ef = make_double2(0.0, 0.0), eb = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      if (k < cnt) {
+        ef.x = fma(q.x, ef.x, x[k].x);
+        ef.y = fma(q.y, ef.y, x[k].y);
+      }
+      const int kb = R - 1 - k;
+      if (kb < cnt) {
+        eb.x = fma(q.x, eb.x, x[kb].x);
+        eb.y = fma(q.y, eb.y, x[kb].y);
+      }
+    }
+    if (tid == 0) {
+      // every warp has read tile j: its buffer takes slice j + 2
+      mbar_wait(&empty[s], ph);
+      if (j + 2 < ntc) issue_load(j + 2, s);
+    }
+    // chunk scans (running products of the chunk multipliers q^cnt), both directions
+    double2 wf = qc, wb = qc;
+#pragma unroll
+    for (int k = 0; k < LW; ++k) {
+      const int d = 1 << k;
+      const double2 vf = shfl_up2(ef, d, W), uf = shfl_up2(wf, d, W);
+      const double2 vb = shfl_down2(eb, d, W), ub = shfl_down2(wb, d, W);
+      if (sl >= d) {
+        ef.x = fma(wf.x, vf.x, ef.x);
+        ef.y = fma(wf.y, vf.y, ef.y);
+        wf.x *= uf.x;
+        wf.y *= uf.y;
+      }
+      if (sl + d < W) {
+        eb.x = fma(wb.x, vb.x, eb.x);
+        eb.y = fma(wb.y, vb.y, eb.y);
+        wb.x *= ub.x;
+        wb.y *= ub.y;
+      }
+    }
+    double2 flo = make_double2(0.0, 0.0), bhi = make_double2(0.0, 0.0);  // across the warps
+    double2 an, b1;  // zero-start totals: A at the last row, B at the first
+    if constexpr (T > 32) {
+      if (t == 31) xp[0] = ef;
+      if (t == 32) xp[1] = eb;
+      if (t == 63) xp[2] = ef;
+      if (t == 0) xp[3] = eb;
+      fft_sync<T>(bar);
+      const double2 s0 = xp[0], s1 = xp[1], s2 = xp[2], s3 = xp[3];
+      if (t >= 32) {
+        flo = s0;
+        ef.x = fma(wf.x, s0.x, ef.x);
+        ef.y = fma(wf.y, s0.y, ef.y);
+      } else {
+        bhi = s1;
+        eb.x = fma(wb.x, s1.x, eb.x);
+        eb.y = fma(wb.y, s1.y, eb.y);
+      }
+      an = make_double2(fma(pw1.x, s0.x, s2.x), fma(pw1.y, s0.y, s2.y));
+      b1 = make_double2(fma(pw0.x, s1.x, s3.x), fma(pw0.y, s1.y, s3.y));
+    } else {
+      const int base = (tid & 31) & ~(W - 1);
+      an = make_double2(__shfl_sync(0xffffffffu, ef.x, base + W - 1),
+                        __shfl_sync(0xffffffffu, ef.y, base + W - 1));
+      b1 = make_double2(__shfl_sync(0xffffffffu, eb.x, base), __shfl_sync(0xffffffffu, eb.y, base));
+    }
+    // image start values A_0, B_N and this chunk's carry-ins
+    double2 fc = shfl_up2(ef, 1, W), bc = shfl_down2(eb, 1, W);
+    if (sl == 0) fc = flo;
+    if (sl == W - 1) bc = bhi;
+    {
+      const double aNx = q.x * an.x, aNy = q.y * an.y;
+      const double A0x = (qN.x * aNx - q.x * b1.x) * inv.x, A0y = (qN.y * aNy - q.y * b1.y) * inv.y;
+      const double BNx = -fma(qN.x, A0x, aNx), BNy = -fma(qN.y, A0y, aNy);
+      fc.x = fma(gf.x, A0x, fc.x);
+      fc.y = fma(gf.y, A0y, fc.y);
+      bc.x = fma(gb.x, BNx, bc.x);
+      bc.y = fma(gb.y, BNy, bc.y);
+    }
+    // causal sweep: A_i in place of r_i
+    {
+      double2 a = fc;
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        if (k < cnt) {
+          a.x = fma(q.x, a.x, x[k].x);
+          a.y = fma(q.y, a.y, x[k].y);
+          x[k] = a;
+        }
+      }
+    }
+    // anti-causal sweep: z_i = gamma (A_i + q B_{i+1}),  B_i = A_i + q (B_{i+1} - A_{i-1})
+    {
+      double2 bn = bc;
+#pragma unroll
+      for (int k = R - 1; k >= 0; --k) {
+        if (k < cnt) {
+          const double2 ak = x[k];
+          const double2 am = k > 0 ? x[k - 1] : fc;
+          x[k] = make_double2(gam.x * fma(q.x, bn.x, ak.x), gam.y * fma(q.y, bn.y, ak.y));
+          bn.x = fma(q.x, bn.x - am.x, ak.x);
+          bn.y = fma(q.y, bn.y - am.y, ak.y);
+        }
+      }
+    }
+    if (tid == 0) {  // the previous slice's store has read the output buffer (long ago)
+      asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+      mbar_arrive(ofree);
+    }
+    mbar_wait(ofree, static_cast<unsigned>(j) & 1u);
+#pragma unroll
+    for (int k = 0; k < R; ++k) *reinterpret_cast<double2*>(bout + off(row0 + k)) = x[k];
+    if constexpr (T > 32) {
+      if (t == 31) xp[4] = x[R - 1];
+      if (t == 32) xp[5] = x[0];
+    }
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    __syncthreads();
+    if (tid == 0) {
+#pragma unroll
+      for (int cb = 0; cb < C::NCB; ++cb)
+#pragma unroll
+        for (int rb = 0; rb < C::NRB; ++rb)
+          tma_store_3d(&map, i0 + cb * (CW / 8), rb * C::BR, static_cast<int>(j),
+                       bout + cb * (C::kRows * CW) + rb * (C::BR * CW));
+      asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    const int r = row0 + k;
+    if (r < n) *reinterpret_cast<double2*>(carry + int64_t(r) * inner + ca) = x[k];
+  }
+  if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+}
+
 }  // namespace stkg
