@@ -316,21 +316,12 @@ def run_reference(args):
     return 0
 
 
-def fused_in_use(cfg) -> bool:
-    """Whether the plan runs the time-marching fused axis-0 pass (heat.cu use_fused_axis0:
-    padded half-length layout, tiles of 2P columns of axis 0, at least half a CTA per SM)."""
-    import torch
-    if os.environ.get("STKG_FUSED") == "0" or not half_kernels(cfg):
-        return False
-    N = cfg.n + 1
-    T = N // 16
-    P = 4 if T >= 32 else 128 // T
-    if N == 1024 and os.environ.get("STKG_FUSED_P"):
-        P = int(os.environ["STKG_FUSED_P"])
-    inner0 = N * cfg.n ** (cfg.ndim - 2)
-    sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
-    return inner0 % (2 * P) == 0 and (os.environ.get("STKG_FUSED") == "1"
-                                      or inner0 // (2 * P) >= sms // 2)
+def line_binding_from_profiles():
+    p = ROOT / "profiles" / "traffic.json"
+    try:
+        return json.loads(p.read_text()).get("line_binding_resource")
+    except Exception:
+        return None
 
 
 def fused_binding_from_profiles():
@@ -382,7 +373,9 @@ def _timed_path(stk, inputs, cfg, transform, args, stream, barrier, F, U, with_c
     s_ms, s_n = prof["scan"]
     N = cfg.unknowns
     sec = ms / 1e3 / args.steps
-    fused = transform == "dst" and fused_in_use(cfg)
+    sched = plan.schedule() if transform == "dst" else "separate"
+    fused = sched != "separate"
+    line = sched == "line_solve"
     if transform == "dense":
         flops = 2.0 * cfg.n * N  # 2n flop per unknown per axis transform launch
         achieved = flops / (t_ms / t_n / 1e3) / 1e12
@@ -398,14 +391,44 @@ def _timed_path(stk, inputs, cfg, transform, args, stream, barrier, F, U, with_c
         fft_flops = fft_flop_per_unknown(cfg.n, half)  # per element and axis pass
         t_hbm = 16.0 * N / (HBM_GBS * 1e9)  # read F + write U once
         rec_flops = 12.0  # recurrence: 2 FMA pivot/coupling, Newton reciprocal, update, weight
-        t_fp64 = (2 * cfg.ndim * fft_flops + rec_flops) * N / (FP64_PEAK_TFLOPS * 1e12)
+        # line-solve schedule: axis 0 is not transformed; per unknown 4 ops for the right-hand
+        # side, 2 + 1 + 4 for the zero-start / causal / anti-causal sweeps (FMA = 2 flop)
+        line_flops = 20.0
+        exec_flops = (2 * (cfg.ndim - 1) * fft_flops + line_flops) if line else \
+            (2 * cfg.ndim * fft_flops + rec_flops)
+        t_fp64 = exec_flops * N / (FP64_PEAK_TFLOPS * 1e12)
         passes = (t_n + s_n) / nprof  # HBM passes of the executed schedule per solve
         t_tr = t_ms / t_n  # mean transform-only pass
         contig = {"kernel": "dst_half_kernel (contiguous axis, forward / inverse)",
                   "ms_per_launch": t_tr, "achieved_gbs": 16.0 * N / (t_tr / 1e3) / 1e9,
                   "frac_hbm": 16.0 * N / (t_tr / 1e3) / 1e9 / HBM_GBS,
                   "launches_per_solve": t_n / nprof}
-        if fused:
+        if line:
+            # the contiguous transform passes are the larger share of the step; the line pass
+            # (class 1 of the profile) is reported beside them
+            t_f = s_ms / s_n
+            achieved = 16.0 * N / (t_tr / 1e3) / 1e9
+            roof = {"bound": "hbm",
+                    "kernel": "dst_half_kernel (FP64 half-length DST-I along the contiguous axis, "
+                              "forward and inverse: N-point Stockham FFT per vector pair)",
+                    "achieved": achieved, "peak": HBM_GBS, "unit": "GB/s",
+                    "frac": achieved / HBM_GBS,
+                    "traffic": traffic_from_profiles("dst_half"),
+                    "binding_resource": binding_from_profiles(),
+                    "ms_per_launch": t_tr, "launches_per_solve": t_n / nprof,
+                    "share_of_sequential_step": t_ms / nprof / ms_seq,
+                    "other_kernel": {
+                        "kernel": "heat_tridiag_tma_kernel (time-marching line solves along "
+                                  "axis 0: constant-coefficient causal / anti-causal sweeps, TMA "
+                                  "tile loads and stores; one read + one write of S)",
+                        "ms_per_launch": t_f, "achieved_gbs": 16.0 * N / (t_f / 1e3) / 1e9,
+                        "frac_hbm": 16.0 * N / (t_f / 1e3) / 1e9 / HBM_GBS,
+                        "flop_per_unknown": line_flops,
+                        "traffic": traffic_from_profiles("line"),
+                        "binding_resource": line_binding_from_profiles(),
+                        "launches_per_solve": s_n / nprof,
+                        "share_of_sequential_step": s_ms / nprof / ms_seq}}
+        elif fused:
             t_f = s_ms / s_n
             achieved = 16.0 * N / (t_f / 1e3) / 1e9
             roof = {"bound": "hbm",
@@ -444,8 +467,11 @@ def _timed_path(stk, inputs, cfg, transform, args, stream, barrier, F, U, with_c
     out = {"transform": transform, "ms_per_step": ms / args.steps, "ms": ms,
            "value": N * args.steps / (ms / 1e3), "relres_gpu_k1": relres, "roofline": roof,
            "launches": int(round((t_n + s_n) / nprof * args.steps)),
-           "recurrence_kernel": {"kernel": "heat_fused_axis0_kernel" if fused else
-                                 "heat_scan_kernel", "ms_per_launch": s_ms / s_n,
+           "schedule": sched,
+           "recurrence_kernel": {"kernel": {"line_solve": "heat_tridiag_tma_kernel",
+                                            "fused_dst": "heat_fused_axis0_kernel",
+                                            "separate": "heat_scan_kernel"}[sched],
+                                 "ms_per_launch": s_ms / s_n,
                                  "gbs": 16.0 * N / (s_ms / s_n / 1e3) / 1e9,
                                  "frac_hbm": 16.0 * N / (s_ms / s_n / 1e3) / 1e9 / HBM_GBS}}
     return plan, out, clk
@@ -484,7 +510,11 @@ def heat_config_leg(stk, inputs, name, stream, steps=10, warmup=3, with_cpu=True
                "relres_gpu_k1": relres,
                "launches_per_solve": prof["transform"][1] + prof["scan"][1]}
         half = half_kernels(cfg)
-        fl = (2 * cfg.ndim * fft_flop_per_unknown(cfg.n, half) + 12.0) * N
+        sched = plan.schedule()
+        out["schedule"] = sched
+        fft = fft_flop_per_unknown(cfg.n, half)
+        fl = ((2 * (cfg.ndim - 1) * fft + 20.0) if sched == "line_solve"
+              else (2 * cfg.ndim * fft + 12.0)) * N
         t_roof = max(16.0 * N / (HBM_GBS * 1e9), fl / (FP64_PEAK_TFLOPS * 1e12))
         out["roofline"] = {"bound": "hbm" if 16.0 * N / HBM_GBS / 1e9 >= fl / FP64_PEAK_TFLOPS
                            / 1e12 else "fp64", "roof_ms": 1e3 * t_roof,

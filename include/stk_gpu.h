@@ -123,6 +123,14 @@ int stkg_heat_create(stkg_heat** plan, const stkg_heat_desc* desc, void* cuda_st
 int stkg_heat_destroy(stkg_heat* plan);
 /* Bytes of device workspace the plan holds (scratch + bases). */
 int64_t stkg_heat_workspace_bytes(const stkg_heat* plan);
+/* Which device schedule stkg_heat_solve runs for this plan (no reference counterpart; used by
+ * bench.py and the tests to name the kernels they time):
+ *   0  one transform pass per axis each way + the per-mode recurrence kernel
+ *   1  time-marching fused axis-0 pass (forward DST, recurrence, inverse DST per slice)
+ *   2  time-marching line-solve axis-0 pass (axis 0 is not transformed: one Toeplitz
+ *      tridiagonal solve per column and slice; uniform time grids on uniform P1 axes) */
+enum { STKG_SCHEDULE_SEPARATE = 0, STKG_SCHEDULE_FUSED_DST = 1, STKG_SCHEDULE_LINE_SOLVE = 2 };
+int stkg_heat_schedule(const stkg_heat* plan);
 /* solve_projected_heat_with (stk/sylvester.hpp:117-142): U = X Y~, Y~ from the per-mode
  * bidiagonal recurrence of X^T F.  F, U device, N_h x N_t column-major.  F is not
  * modified; U may not alias F.  STKG_SINGULARITY if |d_j + lambda_i c_j| < 1e-300. */

@@ -219,6 +219,82 @@ def heat_decoupled(eigs, d, c, F, nsteps=None):
     return Y.reshape(nt, -1)
 
 
+def toeplitz_tridiag_solve_images(a, b, r):
+    """Solve tridiag(a, b, a) x = r along axis 0 of r (shape (n, cols); a, b of shape (cols,),
+    b > 2|a|) by the method of images: the restriction of the bi-infinite Toeplitz operator
+    (constant pivot w = (b + sqrt(b^2 - 4a^2))/2, q = -a/w) to odd 2N-periodic sequences is a
+    causal and an anti-causal first-order recurrence with the constant coefficient q whose
+    start values follow from two weighted totals -- the arithmetic of
+    csrc/heat_tridiag.cuh::heat_tridiag_tma_kernel, unchunked."""
+    n = r.shape[0]
+    N = n + 1
+    sq = np.sqrt((b + 2.0 * a) * (b - 2.0 * a))
+    q = -a / (0.5 * (b + sq))
+    gam = 1.0 / sq
+    A = np.empty_like(r)
+    acc = np.zeros_like(a)
+    for i in range(n):
+        acc = r[i] + q * acc
+        A[i] = acc
+    aN = q * acc                       # zero-start causal total at the mirror row N
+    acc = np.zeros_like(a)
+    for i in range(n - 1, -1, -1):
+        acc = r[i] + q * acc
+    b0 = q * acc                       # zero-start anti-causal total at the mirror row 0
+    qN = q ** N
+    A0 = (qN * aN - b0) / (1.0 - qN * qN)
+    BN = -(qN * A0 + aN)
+    A += (q[None, :] ** np.arange(1, n + 1)[:, None]) * A0
+    x = np.empty_like(r)
+    Bn = BN
+    for i in range(n - 1, -1, -1):
+        x[i] = gam * (A[i] + q * Bn)
+        Bn = r[i] + q * Bn
+    return x
+
+
+def heat_line_march(eigs_fast, m0, a0, d, c, F, nsteps=None):
+    """solve_projected_heat_with (stk/sylvester.hpp:117-142) with axis 0 left untransformed:
+    the faster axes are diagonalised by ``eigs_fast`` = [(lam, X)] (X^T M X = I), and each step
+    of the temporal recurrence is, per column, one symmetric Toeplitz tridiagonal solve along
+    axis 0,  [(d_l + lam_c c_l) M_0 + c_l A_0] z_l = g_l - [(d^s + lam_c c^s) M_0 + c^s A_0]
+    z_{l-1}  (m0, a0 = the 1D P1 factors of axis 0, uniform grid).  Equal to heat_decoupled in
+    exact arithmetic; restates the line-solve schedule of csrc/heat_tridiag.cuh."""
+    n0 = m0[0].size
+    ns = [e[0].size for e in eigs_fast]
+    nt = F.shape[0] if nsteps is None else nsteps
+    G = np.asarray(F[:nt], dtype=np.float64).reshape(nt, n0, *ns)
+    for ax, (lam, X) in enumerate(eigs_fast):
+        G = np.moveaxis(np.tensordot(G, X, axes=([ax + 2], [0])), -1, ax + 2)
+    lam_c = np.zeros(ns)
+    for ax, (lam, X) in enumerate(eigs_fast):
+        shape = [1] * len(ns)
+        shape[ax] = ns[ax]
+        lam_c = lam_c + lam.reshape(shape)
+    lam_c = lam_c.reshape(-1)
+    G = G.reshape(nt, n0, -1)
+    md, mo, ad, ao = m0[0][0], m0[1][0], a0[0][0], a0[1][0]
+    assert np.allclose(m0[0], md) and np.allclose(m0[1], mo) and np.allclose(a0[0], ad) \
+        and np.allclose(a0[1], ao), "axis 0 must be a uniform P1 axis (Toeplitz factors)"
+    Z = np.empty_like(G)
+    z = np.zeros_like(G[0])
+    for l in range(nt):
+        p = d[0][l] + lam_c * c[0][l]
+        rhs = G[l]
+        if l > 0:
+            pp = d[1][l - 1] + lam_c * c[1][l - 1]
+            sa, sb = pp * mo + c[1][l - 1] * ao, pp * md + c[1][l - 1] * ad
+            zz = np.zeros((n0 + 2, z.shape[1]))
+            zz[1:-1] = z
+            rhs = rhs - (sb * z + sa * (zz[:-2] + zz[2:]))
+        z = toeplitz_tridiag_solve_images(p * mo + c[0][l] * ao, p * md + c[0][l] * ad, rhs)
+        Z[l] = z
+    Z = Z.reshape(nt, n0, *ns)
+    for ax, (lam, X) in enumerate(eigs_fast):
+        Z = np.moveaxis(np.tensordot(Z, X, axes=([ax + 2], [1])), -1, ax + 2)
+    return Z.reshape(nt, -1)
+
+
 class DecoupledStream:
     """heat_decoupled over consecutive time chunks: the same tensor-form
     solve_projected_heat_with (stk/sylvester.hpp:117-142), with the per-mode recurrence

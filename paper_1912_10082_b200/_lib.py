@@ -101,6 +101,7 @@ SIGNATURES = {
     "stkg_heat_create": (C.c_int, [C.POINTER(C.c_void_p), C.POINTER(HeatDesc), C.c_void_p]),
     "stkg_heat_destroy": (C.c_int, [C.c_void_p]),
     "stkg_heat_workspace_bytes": (C.c_int64, [C.c_void_p]),
+    "stkg_heat_schedule": (C.c_int, [C.c_void_p]),
     "stkg_heat_solve": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "stkg_heat_solve_factored": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
                                            C.c_void_p]),

@@ -1350,6 +1350,18 @@ int stkg_heat_destroy(stkg_heat* h) {
   });
 }
 
+int stkg_heat_schedule(const stkg_heat* h) {
+  if (!h || h->pitch <= 0) return STKG_SCHEDULE_SEPARATE;
+  int64_t inner0 = h->pitch;
+  for (int b = 1; b + 1 < h->ndim; ++b) inner0 *= h->n[b];
+  try {
+    if (!use_fused_axis0(*h, inner0)) return STKG_SCHEDULE_SEPARATE;
+    return use_tridiag(*h, inner0) ? STKG_SCHEDULE_LINE_SOLVE : STKG_SCHEDULE_FUSED_DST;
+  } catch (...) {
+    return STKG_SCHEDULE_SEPARATE;
+  }
+}
+
 int64_t stkg_heat_workspace_bytes(const stkg_heat* h) {
   if (!h) return 0;
   int64_t b = 0;

@@ -180,6 +180,13 @@ class HeatPlan:
     def workspace_bytes(self) -> int:
         return int(lib.stkg_heat_workspace_bytes(self._h))
 
+    def schedule(self) -> str:
+        """The device schedule of :meth:`solve` (``stkg_heat_schedule``): ``"separate"`` (one
+        transform pass per axis each way + the recurrence kernel), ``"fused_dst"`` (time-marching
+        fused axis-0 pass) or ``"line_solve"`` (axis 0 solved by Toeplitz tridiagonal line solves,
+        not transformed)."""
+        return ("separate", "fused_dst", "line_solve")[int(lib.stkg_heat_schedule(self._h))]
+
     def _check_size(self, t):
         n = t.numel() if hasattr(t, "numel") else t.size
         if n != self.nx * self.nt:

@@ -540,7 +540,8 @@ def test_padded_layout_equals_unpadded(tmp_path):
     res = {}
     for pad in ("1", "0"):
         f = tmp_path / f"pad{pad}.npz"
-        env = dict(os.environ, STKG_PAD=pad)
+        # (both with the transform-based passes: this test is about the layout)
+        env = dict(os.environ, STKG_PAD=pad, STKG_TRIDIAG="0")
         subprocess.run([sys.executable, "-c", _PAD_SCRIPT, root, str(f)], check=True, env=env)
         res[pad] = dict(np.load(f))
     for k in res["1"]:
@@ -621,7 +622,8 @@ def test_dst_padded_solve_deterministic(stk, cuda, ndim, n, nt):
                                  {"STKG_SCAN_CHUNKED": "0"}, {"STKG_SCAN_RECIP": "0"},
                                  {"STKG_FUSED": "0"}, {"STKG_FUSED_P": "2"},
                                  {"STKG_FUSED_V": "1"}, {"STKG_FUSED_V": "2"},
-                                 {"STKG_FUSED_V": "3"}, {"STKG_FUSED_V": "8"}])
+                                 {"STKG_FUSED_V": "3"}, {"STKG_FUSED_V": "8"},
+                                 {"STKG_TRIDIAG": "0"}, {"STKG_TRI_V": "0"}])
 def test_tuning_variants_match_default(tmp_path, env):
     """The opt-in tuning variants (strided-tile shapes with and without next-tile prefetch,
     the one-chain scan for small plans, per-step division in the factored scan; the separate
@@ -633,13 +635,19 @@ def test_tuning_variants_match_default(tmp_path, env):
     from pathlib import Path
     root = str(Path(__file__).resolve().parent.parent)
     res = {}
-    for tag, extra in (("v", env), ("d", {})):
+    # the fused-DST-pass variants are compared on plans that run that pass (STKG_TRIDIAG=0:
+    # uniform time grids otherwise take the line-solve pass, which ignores them)
+    base = {"STKG_TRIDIAG": "0"} if any(k.startswith("STKG_FUSED") for k in env) else {}
+    for tag, extra in (("v", dict(base, **env)), ("d", base)):
         f = tmp_path / f"{tag}.npz"
         subprocess.run([sys.executable, "-c", _PAD_SCRIPT, root, str(f)], check=True,
                        env=dict(os.environ, **extra))
         res[tag] = dict(np.load(f))
+    # the line-solve pass and the transform-based passes are different algorithms for the same
+    # solve (tridiagonal line solves vs two more sine transforms): they agree to rounding
+    tol = 5e-12 if any(k.startswith("STKG_TRI") for k in env) else 1e-13
     for k in res["v"]:
-        assert rel(res["v"][k], res["d"][k]) < 1e-13, (k, rel(res["v"][k], res["d"][k]))
+        assert rel(res["v"][k], res["d"][k]) < tol, (k, rel(res["v"][k], res["d"][k]))
 
 
 _FUSED_SCRIPT = r"""
@@ -689,7 +697,7 @@ def test_fused_axis0_pass_matches_separate_passes(tmp_path):
     for v in ("1", "0"):
         f = tmp_path / f"fused{v}.npz"
         subprocess.run([sys.executable, "-c", _FUSED_SCRIPT, root, str(f)], check=True,
-                       env=dict(os.environ, STKG_FUSED=v))
+                       env=dict(os.environ, STKG_FUSED=v, STKG_TRIDIAG="0"))
         res[v] = dict(np.load(f))
     for k in res["1"]:
         a, b = res["1"][k], res["0"][k]
@@ -700,6 +708,80 @@ def test_fused_axis0_pass_matches_separate_passes(tmp_path):
     for k in res["1"]:
         if k[0] == "h":
             assert rel(res["1"][k], res["1"]["u" + k[1:]]) < 1e-13, k
+
+
+_LINE_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_1912_10082_b200 as stk
+out = {}
+for ndim, n, nt in [(2, 1023, 5), (2, 511, 4), (2, 255, 7), (2, 127, 6), (2, 63, 5), (3, 127, 4),
+                    (3, 63, 3)]:
+    rng = np.random.default_rng(7 * n + nt)
+    F = rng.standard_normal((nt, n ** ndim))
+    p = stk.HeatPlan.p1_uniform(ndim, n, nt, transform="dst")
+    out[f"s{ndim}_{n}"] = np.array(["separate", "fused_dst", "line_solve"].index(p.schedule()))
+    Fd = torch.from_numpy(F).cuda()
+    U = p.solve(Fd)
+    out[f"u{ndim}_{n}"] = U.cpu().numpy()
+    out[f"r{ndim}_{n}"] = np.array(p.residual(U, Fd)[0])
+    # host-buffer path in 2-slice time chunks: every launch starts from the carried z_{l0-1}
+    pc = stk.HeatPlan.p1_uniform(ndim, n, nt, transform="dst", time_chunk=2)
+    out[f"h{ndim}_{n}"] = pc.solve_host(F)
+# a longer time axis on a domain / horizon that is not the unit one (other stencil scales)
+p = stk.HeatPlan.p1_uniform(2, 255, 96, T=10.0, a=-1.0, b=1.0, transform="dst")
+F = np.random.default_rng(5).standard_normal((96, 255 * 255))
+Fd = torch.from_numpy(F).cuda()
+U = p.solve(Fd)
+out["s_long"] = np.array(["separate", "fused_dst", "line_solve"].index(p.schedule()))
+out["u_long"] = U.cpu().numpy()
+out["r_long"] = np.array(p.residual(U, Fd)[0])
+# non-uniform temporal bidiagonals: the plan must keep the transform-based pass
+rng = np.random.default_rng(11)
+g = stk.SpaceGrid1D(0.0, 1.0, 255)
+e = stk.p1_eigpair(g)
+M, A = stk.fem1d_matrices(g)
+D = stk.Bidiagonal(rng.uniform(1.0, 2.0, 6), rng.uniform(-1.0, -0.2, 5))
+Cm = stk.Bidiagonal(rng.uniform(0.01, 0.1, 6), rng.uniform(0.01, 0.1, 5))
+pn = stk.HeatPlan(stk.TensorEigPair([e, e]), D, Cm, [M, M], [A, A], transform="dst",
+                  p1_h=[g.fem_h] * 2)
+out["s_nonuniform"] = np.array(["separate", "fused_dst", "line_solve"].index(pn.schedule()))
+np.savez(sys.argv[2], **out)
+"""
+
+
+def test_line_solve_pass_matches_transform_passes(tmp_path):
+    """The time-marching line-solve axis-0 pass (heat_tridiag.cuh: axis 0 is not transformed;
+    per column and slice one Toeplitz tridiagonal solve by constant-coefficient causal /
+    anti-causal sweeps, TMA tile loads and stores; STKG_FUSED=1 forces the time-marching
+    schedule for every tile geometry) against the transform-based schedule (STKG_TRIDIAG=0)
+    and against the cp.async LDL^T variant of the same pass (STKG_TRI_V=0): device solves,
+    host-buffer solves in 2-slice chunks (carried state, l0 > 0), 2D and 3D, N = 64 ... 1024,
+    a non-unit domain and horizon.  Agreement to 5e-12 (different algorithms for the same
+    solve), GPU residuals <= 1e-11; plans with non-uniform time grids keep the transform pass."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = str(Path(__file__).resolve().parent.parent)
+    res = {}
+    for tag, env in (("line", {}), ("dst", {"STKG_TRIDIAG": "0"}), ("ldl", {"STKG_TRI_V": "0"})):
+        f = tmp_path / f"{tag}.npz"
+        subprocess.run([sys.executable, "-c", _LINE_SCRIPT, root, str(f)], check=True,
+                       env=dict(os.environ, STKG_FUSED="1", **env))
+        res[tag] = dict(np.load(f))
+    for k, a in res["line"].items():
+        if k[0] == "s":
+            want = 1 if k == "s_nonuniform" else 2
+            assert int(a) == want and int(res["ldl"][k]) == want and int(res["dst"][k]) == 1, k
+        elif k[0] == "r":
+            assert float(a) < 1e-11 and float(res["ldl"][k]) < 1e-11, (k, float(a))
+        else:
+            assert rel(a, res["dst"][k]) < 5e-12, (k, rel(a, res["dst"][k]))
+            assert rel(res["ldl"][k], res["dst"][k]) < 5e-12, (k, rel(res["ldl"][k], res["dst"][k]))
+    for k in res["line"]:
+        if k[0] == "h":
+            assert rel(res["line"][k], res["line"]["u" + k[1:]]) < 1e-13, k
 
 
 _OVERLAP_SCRIPT = r"""

@@ -214,6 +214,29 @@ def test_oracle_cn_equals_decoupled(orc):
     assert np.array_equal(orc.fill_uniform(777, 5, 48, 3), inputs.uniform_pm1(777, 5, 48, 3))
 
 
+@pytest.mark.parametrize("ndim,n,nt", [(2, 31, 9), (2, 63, 6), (3, 15, 5)])
+def test_oracle_line_march_equals_decoupled(orc, ndim, n, nt):
+    """The line-solve schedule (axis 0 untransformed: one Toeplitz tridiagonal solve per column
+    and step, solved by the method-of-images recurrences of csrc/heat_tridiag.cuh) against the
+    reference algorithm, solve_projected_heat_with in tensor form (all axes diagonalised), and
+    the tridiagonal solver alone against a dense solve -- including a column with a ~ 0."""
+    rng = np.random.default_rng(n + nt)
+    m, a = orc.fem1d_matrices(0.0, 1.0, n)
+    d, c = orc.heat_time_matrices(nt, 1.0)
+    e = orc.p1_pencil_eig(m, a)
+    F = rng.uniform(-1.0, 1.0, (nt, n ** ndim))
+    ref = orc.heat_decoupled([e] * ndim, d, c, F)
+    got = orc.heat_line_march([e] * (ndim - 1), m, a, d, c, F)
+    assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max()
+    aa = np.array([-1.0, 0.3, 0.0, 1e-9, -0.49999])
+    bb = np.array([2.0001, 1.0, 1.0, 1.0, 1.0])
+    r = rng.standard_normal((n, aa.size))
+    x = orc.toeplitz_tridiag_solve_images(aa, bb, r)
+    for k in range(aa.size):
+        T = bb[k] * np.eye(n) + aa[k] * (np.eye(n, k=1) + np.eye(n, k=-1))
+        assert np.abs(T @ x[:, k] - r[:, k]).max() <= 1e-10 * np.abs(r[:, k]).max()
+
+
 def test_oracle_wave_gmres_matches_direct(orc, ref_bands):
     sb, tb = ref_bands["space_16_3"], ref_bands["time_16_3"]
     W = orc.WaveSystemNP(sb, tb)
