@@ -804,6 +804,7 @@ def run_ours(args):
         "roofline": res["roofline"],
         "e2e": e2e,
         "gpu_launches": res["launches"],
+        "schedule": res.get("schedule"),
         "k1_residual": {"ms": k1_ms, "gbs": 16.0 * N / (k1_ms / 1e3) / 1e9,
                         "frac_hbm": 16.0 * N / (k1_ms / 1e3) / 1e9 / HBM_GBS,
                         "bytes_alg": 16 * N},

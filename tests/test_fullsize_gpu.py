@@ -16,8 +16,9 @@ def rel(a, b):
 
 @pytest.fixture(scope="module")
 def cfg3_solution(stk, cuda):
-    """The headline device solve of cfg3 (default backend: half-length DST passes + the fused
-    axis-0 pass), U copied to the host, and the GPU residual."""
+    """The headline device solve of cfg3 (default backend: half-length DST passes along the
+    contiguous axis + the time-marching line-solve pass along axis 0), U copied to the host,
+    and the GPU residual."""
     import torch
     from paper_1912_10082_b200 import inputs
     cfg = inputs.CONFIGS["cfg3"]
@@ -25,7 +26,8 @@ def cfg3_solution(stk, cuda):
     F = inputs.heat_rhs_device(cfg)
     U = plan.solve(F)
     relres, _ = plan.residual(U, F)
-    # the overlapped two-stream schedule is deterministic: a second solve is bit-identical
+    assert plan.schedule() == "line_solve"
+    # a second solve is bit-identical (no atomics / order dependence anywhere on the path)
     U2 = plan.solve(F)
     assert bool(torch.equal(U, U2))
     del U2

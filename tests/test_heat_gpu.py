@@ -811,7 +811,9 @@ def test_overlapped_schedule_bit_identical(tmp_path, k):
     """The overlapped 2D schedule (time chunks; contiguous passes with ticketed items on a
     low-priority stream beside the fused pass on a high-priority stream, carries across
     chunks) computes exactly what the sequential passes compute: same arithmetic per slice,
-    only the launch order differs.  Uneven chunks (n_t = 37), repeated solves."""
+    only the launch order differs.  Uneven chunks (n_t = 37), repeated solves.  (Plans that
+    take the line-solve pass keep the plain order; STKG_TRIDIAG=0 selects the fused DST pass,
+    the schedule of non-uniform time grids.)"""
     import os
     import subprocess
     import sys
@@ -821,7 +823,7 @@ def test_overlapped_schedule_bit_identical(tmp_path, k):
     for v in (k, "0"):
         f = tmp_path / f"ov{v}.npz"
         subprocess.run([sys.executable, "-c", _OVERLAP_SCRIPT, root, str(f)], check=True,
-                       env=dict(os.environ, STKG_OVERLAP=v))
+                       env=dict(os.environ, STKG_OVERLAP=v, STKG_TRIDIAG="0"))
         res[v] = dict(np.load(f))
     for key in res["0"]:
         a, b = res[k][key], res["0"][key]
