@@ -235,6 +235,9 @@ class HeatPlan {
   }
 
   int64_t space_dim() const { return nx_; }
+  // STKG_SCHEDULE_* of stkg_heat_solve for this plan (separate passes / fused transform pass /
+  // line-solve pass)
+  int schedule() const { return stkg_heat_schedule(h_); }
   int64_t time_dim() const { return nt_; }
 
   void solve(const double* F_dev, double* U_dev) { check(stkg_heat_solve(h_, F_dev, U_dev)); }

@@ -416,7 +416,6 @@ __global__ void __launch_bounds__(TriTmaCfg<N, PP>::kThreads, 1)
   constexpr int R = C::R, T = C::T, n = C::n, W = C::W, LW = C::LW, CW = C::CW;
   extern __shared__ __align__(1024) unsigned char tmraw[];
   if ((static_cast<unsigned>(__cvta_generic_to_shared(tmraw)) & 1023u) != 0u) __trap();
-  unsigned char* bin[2] = {tmraw, tmraw + C::kBufBytes};
   unsigned char* bout = tmraw + 2 * C::kBufBytes;
   double2* xch = reinterpret_cast<double2*>(tmraw + C::kXchOff);  // [P][8]
   uint64_t* bars = reinterpret_cast<uint64_t*>(tmraw + C::kBarOff);
@@ -494,7 +493,7 @@ __global__ void __launch_bounds__(TriTmaCfg<N, PP>::kThreads, 1)
     for (int cb = 0; cb < C::NCB; ++cb)
 #pragma unroll
       for (int rb = 0; rb < C::NRB; ++rb)
-        tma_load_3d(bin[s] + cb * (C::kRows * CW) + rb * (C::BR * CW), &map,
+        tma_load_3d(tmraw + s * C::kBufBytes + cb * (C::kRows * CW) + rb * (C::BR * CW), &map,
                     i0 + cb * (CW / 8), rb * C::BR, static_cast<int>(j), &full[s]);
   };
   if (tid == 0) {
@@ -528,7 +527,7 @@ __global__ void __launch_bounds__(TriTmaCfg<N, PP>::kThreads, 1)
     mbar_wait(&full[s], ph);
     // right-hand side in place: r_i = w_c g_i - sb z_i - sa (z_{i-1} + z_{i+1})
     {
-      const unsigned char* tb = bin[s];
+      const unsigned char* tb = tmraw + s * C::kBufBytes;
       double2 zl = zu;
 #pragma unroll
       for (int k = 0; k < R; ++k) {
