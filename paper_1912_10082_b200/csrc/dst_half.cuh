@@ -511,8 +511,13 @@ __global__ void __launch_bounds__(HalfCfg<N>::kThreads, HalfCfg<N>::kMinBlocks)
       if (m > 0 && has_a) {
         const int mm = N - m;  // in 1..N-1 as well
         const double s = -__ldg(&tw2[m].y);
+#ifdef STKG_DBG_NOLDG  // (measurement only: what the global loads cost)
+        const double xb = double(m) * hs, xbm = double(mm) * hs;
+        x[p] = half_pre(s, xb + 1.0, xbm - 1.0, xb, xbm);
+#else
         const double xb = has_b ? sb[m - 1] : 0.0, xbm = has_b ? sb[mm - 1] : 0.0;
         x[p] = half_pre(s, sa[m - 1], sa[mm - 1], xb, xbm);
+#endif
       }
     }
     if (STKG_DST_PREFETCH > 0 && !DYN) {  // a later item's 2F vectors into L2
@@ -542,6 +547,9 @@ __global__ void __launch_bounds__(HalfCfg<N>::kThreads, HalfCfg<N>::kMinBlocks)
           prefetch_l2(base + o);
       }
     }
+#ifdef STKG_DBG_NOSTG  // (measurement only: what the copy-out costs)
+    if (hs == 123.456)
+#endif
     if constexpr (F == 1) {
       double* da = dst + g0 * ld_dst;
       for (int e = t; e < ldo; e += T) da[e] = e < n ? oa[opad<V>(e)] : 0.0;

@@ -523,6 +523,10 @@ bool use_fused_axis0(const stkg_heat& h, int64_t inner) {
   const int m = fused_mode();
   if (m == 0) return false;
   if (m > 0) return true;
+  // the line-solve pass costs ~2 us per slice whatever the tile count, so it pays from 32 tiles
+  // on (measured: 2D 511^2 x 1024 4.52 vs 5.56 ms, 3D 63^3 x 512 3.34 vs 3.91 ms; 8 tiles at
+  // 255^2 lose 2.7 vs 1.5 ms); the fused transform pass needs half a CTA per SM
+  if (use_tridiag(h, inner)) return inner / G >= 32;
   return inner / G >= num_sms() / 2;
 }
 

@@ -430,6 +430,13 @@ __global__ void __launch_bounds__(TriTmaCfg<N, PP>::kThreads, 1)
   const int64_t ca = i0 + 2 * f;
   const int row0 = R * t;
   const int cnt = n - row0 < 0 ? 0 : (n - row0 > R ? R : n - row0);  // real rows of this chunk
+  // Lanes t < TF hold R real rows, lane TF the TAIL = n mod R last ones (then phantom rows),
+  // later lanes only phantom rows.  The sweeps below run unguarded over all R rows: phantom
+  // rows have zero right-hand sides (zero-filled tile rows, zero z) and their outputs are
+  // multiplied by a zero gamma, so they stay exact zeros; the three places where the tail
+  // lane's phantom rows would leak into real rows are patched at compile-time positions.
+  constexpr int TF = n / R, TAIL = n % R;
+  const bool tail_lane = t == TF;
   double2* xp = xch + f * 8;
   // byte offset of this pair's 16-byte chunk in row r of a tile buffer (TMA swizzle)
   const int cbase = (f / C::CPB) * (C::kRows * CW), cc = f % C::CPB;
@@ -439,7 +446,7 @@ __global__ void __launch_bounds__(TriTmaCfg<N, PP>::kThreads, 1)
   };
 
   // per-column constants (.x / .y: the pair's two columns)
-  double2 q, gam, sa, sb, wc, qc, gf, gb, qN, inv, pw0, pw1;
+  double2 q, gam, gamA, gamB, sa, sb, wc, qc, gf, gb, qN, inv, pw0, pw1;
   {
     double qq[2], gg[2], s1[2], s2[2];
 #pragma unroll
@@ -461,6 +468,8 @@ __global__ void __launch_bounds__(TriTmaCfg<N, PP>::kThreads, 1)
     sa = make_double2(s1[0], s1[1]);
     sb = make_double2(s2[0], s2[1]);
     wc = make_double2(w_col[ca], w_col[ca + 1]);
+    gamA = t <= TF ? gam : make_double2(0.0, 0.0);  // rows k < TAIL of the chunk
+    gamB = t < TF ? gam : make_double2(0.0, 0.0);   // rows k >= TAIL
     const int above = row0 < n ? row0 : n;                      // real rows above the chunk
     const int below = n - row0 - R > 0 ? n - row0 - R : 0;      // real rows below it
     qc = make_double2(tri_ipow(q.x, cnt), tri_ipow(q.y, cnt));
@@ -534,10 +543,11 @@ __global__ void __launch_bounds__(TriTmaCfg<N, PP>::kThreads, 1)
         const double2 g = *reinterpret_cast<const double2*>(tb + off(row0 + k));
         const double2 zc = x[k];
         const double2 zr = k + 1 < R ? x[k + 1] : zn;
+        // (the first phantom row of the tail lane must not see the last real row above it)
+        if (k == TAIL && tail_lane) zl = make_double2(0.0, 0.0);
         const double ra = fma(sb.x, zc.x, sa.x * (zl.x + zr.x));
         const double rb = fma(sb.y, zc.y, sa.y * (zl.y + zr.y));
-        x[k] = k < cnt ? make_double2(fma(wc.x, g.x, -ra), fma(wc.y, g.y, -rb))
-                       : make_double2(0.0, 0.0);
+        x[k] = make_double2(fma(wc.x, g.x, -ra), fma(wc.y, g.y, -rb));
         zl = zc;
       }
     }
@@ -546,18 +556,17 @@ __global__ void __launch_bounds__(TriTmaCfg<N, PP>::kThreads, 1)
 
     // zero-start recurrences over the chunk, both directions
     double2 ef = make_double2(0.0, 0.0), eb = make_double2(0.0, 0.0);
+    double2 cap = make_double2(0.0, 0.0);  // the causal value after the tail lane's real rows
 #pragma unroll
     for (int k = 0; k < R; ++k) {
-      if (k < cnt) {
-        ef.x = fma(q.x, ef.x, x[k].x);
-        ef.y = fma(q.y, ef.y, x[k].y);
-      }
+      ef.x = fma(q.x, ef.x, x[k].x);
+      ef.y = fma(q.y, ef.y, x[k].y);
+      if (k == TAIL - 1) cap = ef;
       const int kb = R - 1 - k;
-      if (kb < cnt) {
-        eb.x = fma(q.x, eb.x, x[kb].x);
-        eb.y = fma(q.y, eb.y, x[kb].y);
-      }
+      eb.x = fma(q.x, eb.x, x[kb].x);
+      eb.y = fma(q.y, eb.y, x[kb].y);
     }
+    if (tail_lane) ef = cap;  // (zero-start values of phantom rows are zero: eb needs no patch)
     if (tid == 0) {
       // every warp has read tile j: its buffer takes slice j + 2
       mbar_wait(&empty[s], ph);
@@ -627,25 +636,26 @@ __global__ void __launch_bounds__(TriTmaCfg<N, PP>::kThreads, 1)
       double2 a = fc;
 #pragma unroll
       for (int k = 0; k < R; ++k) {
-        if (k < cnt) {
-          a.x = fma(q.x, a.x, x[k].x);
-          a.y = fma(q.y, a.y, x[k].y);
-          x[k] = a;
-        }
+        a.x = fma(q.x, a.x, x[k].x);
+        a.y = fma(q.y, a.y, x[k].y);
+        x[k] = a;
       }
     }
-    // anti-causal sweep: z_i = gamma (A_i + q B_{i+1}),  B_i = A_i + q (B_{i+1} - A_{i-1})
+    // anti-causal sweep: z_i = gamma (A_i + q B_{i+1}),  B_i = r_i + q B_{i+1}, r_i = A_i - q A_{i-1}
     {
       double2 bn = bc;
 #pragma unroll
       for (int k = R - 1; k >= 0; --k) {
-        if (k < cnt) {
-          const double2 ak = x[k];
-          const double2 am = k > 0 ? x[k - 1] : fc;
-          x[k] = make_double2(gam.x * fma(q.x, bn.x, ak.x), gam.y * fma(q.y, bn.y, ak.y));
-          bn.x = fma(q.x, bn.x - am.x, ak.x);
-          bn.y = fma(q.y, bn.y - am.y, ak.y);
-        }
+        // (the tail lane's sweep enters its last real row with the carry-in itself)
+        if (k == TAIL - 1 && tail_lane) bn = bc;
+        const double2 ak = x[k];
+        const double2 am = k > 0 ? x[k - 1] : fc;
+        const double2 gk = k < TAIL ? gamA : gamB;
+        // r_k = A_k - q A_{k-1} off the chain: one dependent FMA per row on B
+        const double rx = fma(-q.x, am.x, ak.x), ry = fma(-q.y, am.y, ak.y);
+        x[k] = make_double2(gk.x * fma(q.x, bn.x, ak.x), gk.y * fma(q.y, bn.y, ak.y));
+        bn.x = fma(q.x, bn.x, rx);
+        bn.y = fma(q.y, bn.y, ry);
       }
     }
     if (tid == 0) {  // the previous slice's store has read the output buffer (long ago)
