@@ -408,10 +408,10 @@ int tri_variant() {
   return v;
 }
 
-template <int N, int P>
-void launch_tridiag_tma(const stkg_heat& h, double* S, int64_t inner, int64_t ntc, int64_t l0) {
+template <int N, int P, bool UNI>
+void launch_tridiag_tma_u(const stkg_heat& h, double* S, int64_t inner, int64_t ntc, int64_t l0) {
   using C = TriTmaCfg<N, P>;
-  auto kern = heat_tridiag_tma_kernel<N, P>;
+  auto kern = heat_tridiag_tma_kernel<N, P, UNI>;
   static const bool configured = [kern] {
     STKG_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(C::kSmem)));
@@ -438,8 +438,14 @@ void launch_tridiag_tma(const stkg_heat& h, double* S, int64_t inner, int64_t nt
   const double ds = h.nt > 1 ? h.d_sup_h[0] : 0.0, cs = h.nt > 1 ? h.c_sup_h[0] : 0.0;
   kern<<<static_cast<unsigned>(tiles), C::kThreads, C::kSmem, launch_stream(h)>>>(
       map, inner, ntc, l0, h.lam_col.p, h.w_col.p, h.d_diag_h[0], ds, h.c_diag_h[0], cs, h.tri_md,
-      h.tri_mo, h.tri_ad, h.tri_ao, h.carry.p);
+      h.tri_mo, h.tri_ad, h.tri_ao, h.carry.p, h.d_diag.p, h.d_sup.p, h.c_diag.p, h.c_sup.p);
   STKG_CUDA_CHECK(cudaGetLastError());
+}
+
+template <int N, int P>
+void launch_tridiag_tma(const stkg_heat& h, double* S, int64_t inner, int64_t ntc, int64_t l0) {
+  if (h.uniform_time) return launch_tridiag_tma_u<N, P, true>(h, S, inner, ntc, l0);
+  return launch_tridiag_tma_u<N, P, false>(h, S, inner, ntc, l0);
 }
 
 // Columns per line-solve tile for axis-0 length n0 (0: no such kernel for that length).
@@ -1064,7 +1070,15 @@ bool tridiag_enabled() {
 // T_c positive definite.  Otherwise the plan keeps the transform-based pass.
 void setup_tridiag(stkg_heat& h, const double* lam0, double hh) {
   h.tri_ok = false;
-  if (!tridiag_enabled() || !h.uniform_time || h.pitch <= 0 || h.lam_col.p == nullptr) return;
+  if (!tridiag_enabled() || h.pitch <= 0 || h.lam_col.p == nullptr) return;
+  // non-uniform time grids: the TMA variant recomputes its per-column constants every step
+  // (STKG_TRI_NONUNIFORM=0 keeps the fused transform pass for them); the LDL^T variant's pivot
+  // table is per plan
+  static const bool nonuni_on = [] {
+    const char* e = std::getenv("STKG_TRI_NONUNIFORM");
+    return !(e && std::atoi(e) == 0);
+  }();
+  if (!h.uniform_time && (tri_variant() == 0 || !nonuni_on)) return;
   const int64_t n0 = h.n[0], N = n0 + 1;
   if (tri_tile_cols(n0) == 0) return;
   const double md = 2.0 * hh / 3.0, mo = hh / 6.0, ad = 2.0 / hh, ao = -1.0 / hh;
@@ -1077,21 +1091,43 @@ void setup_tridiag(stkg_heat& h, const double* lam0, double hh) {
   for (int b = 1; b + 1 < h.ndim; ++b) inner *= h.n[b];
   if (inner % tri_tile_cols(n0) != 0) return;
   h.tri_md = md, h.tri_mo = mo, h.tri_ad = ad, h.tri_ao = ao;
-  // every column's T_c = tridiag(a, b, a) must have a positive symbol (b > 2|a|) and a decay
-  // q = |a| / w with q^N well below 1 (the image sums divide by 1 - q^{2N})
+  // every column's T_c = tridiag(a, b, a) must have a positive symbol (b > 2|a|), a moderate
+  // condition number and a decay q = |a| / w with q^N below 1 (the image sums divide by
+  // 1 - q^{2N})
   std::vector<double> lc(static_cast<size_t>(inner));
   STKG_CUDA_CHECK(cudaMemcpyAsync(lc.data(), h.lam_col.p, inner * sizeof(double),
                                   cudaMemcpyDeviceToHost, h.stream));
   STKG_CUDA_CHECK(cudaStreamSynchronize(h.stream));
-  const double dd = h.d_diag_h[0], cd = h.c_diag_h[0];
-  for (int64_t c = 0; c < inner; ++c) {
-    const double p = dd + lc[c] * cd;
-    const double a = p * mo + cd * ao, b = p * md + cd * ad;
-    const double bp = p * (md + 2.0 * mo) + cd * (ad + 2.0 * ao);
-    const double bm = p * (md - 2.0 * mo) + cd * (ad - 2.0 * ao);
-    if (!(b > 0.0 && bp > 0.0 && bm > 0.0)) return;
-    const double q = std::fabs(a) / (0.5 * (b + std::sqrt(bp * bm)));
-    if (!(std::pow(q, static_cast<double>(N)) < 0.25)) return;
+  // (the symbol is affine in lambda_c, so per step only the extreme columns need the test)
+  double lmin = lc[0], lmax = lc[0];
+  for (int64_t c = 1; c < inner; ++c) lmin = std::min(lmin, lc[c]), lmax = std::max(lmax, lc[c]);
+  const int64_t steps = h.uniform_time ? 1 : h.nt;
+  for (int64_t l = 0; l < steps; ++l) {
+    const double dd = h.d_diag_h[l], cd = h.c_diag_h[l];
+    for (const double lam : {lmin, lmax}) {
+      const double p = dd + lam * cd;
+      const double b = p * md + cd * ad;
+      const double bp = p * (md + 2.0 * mo) + cd * (ad + 2.0 * ao);
+      const double bm = p * (md - 2.0 * mo) + cd * (ad - 2.0 * ao);
+      if (!(b > 0.0 && bp > 0.0 && bm > 0.0)) return;
+    }
+    // q = |a| / w is largest where b / |a| is smallest: test every column on uniform grids,
+    // the extreme columns and a sample in between otherwise
+    const int64_t stride = h.uniform_time ? 1 : std::max<int64_t>(1, inner / 64);
+    for (int64_t c = 0; c < inner; c += stride) {
+      const double p = dd + lc[c] * cd;
+      const double a = p * mo + cd * ao, b = p * md + cd * ad;
+      const double bp = p * (md + 2.0 * mo) + cd * (ad + 2.0 * ao);
+      const double bm = p * (md - 2.0 * mo) + cd * (ad - 2.0 * ao);
+      if (!(b > 0.0 && bp > 0.0 && bm > 0.0)) return;
+      // a tridiagonal line solve loses cond(T_c) = max(b + 2a, b - 2a) / min(...) ulps (the
+      // modal recurrence divides mode by mode and loses none): plans with very large time
+      // steps against h^2 (measured 5.5e-12 against the DMMA backend at cond 1e6) keep the
+      // transform pass; cfg3 has cond 2e3, cfg5 1.3e2
+      if (!(std::max(bp, bm) <= 1e5 * std::min(bp, bm))) return;
+      const double q = std::fabs(a) / (0.5 * (b + std::sqrt(bp * bm)));
+      if (!(std::pow(q, static_cast<double>(N)) < 0.9)) return;
+    }
   }
   h.tri_ok = true;
   if (tri_variant() != 0) return;
@@ -1101,7 +1137,8 @@ void setup_tridiag(stkg_heat& h, const double* lam0, double hh) {
   STKG_CUDA_CHECK(cudaMalloc(&bad, sizeof(int)));
   STKG_CUDA_CHECK(cudaMemsetAsync(bad, 0, sizeof(int), h.stream));
   tri_factor_kernel<<<static_cast<unsigned>(ceil_div(inner, 128)), 128, 0, h.stream>>>(
-      h.tri_iw.p, inner, static_cast<int>(n0), h.lam_col.p, dd, cd, md, mo, ad, ao, bad);
+      h.tri_iw.p, inner, static_cast<int>(n0), h.lam_col.p, h.d_diag_h[0], h.c_diag_h[0], md, mo,
+      ad, ao, bad);
   int hb = 1;
   cudaError_t e1 = cudaGetLastError();
   cudaError_t e2 = cudaMemcpyAsync(&hb, bad, sizeof hb, cudaMemcpyDeviceToHost, h.stream);

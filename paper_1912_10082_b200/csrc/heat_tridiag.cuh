@@ -405,13 +405,19 @@ __device__ __forceinline__ double tri_ipow(double q, int e) {
 // side, one barrier per step joins the two warps of a column pair, and r is recovered from
 // A in the second sweep (r_i = A_i - q A_{i-1}), so one register array holds z, r, A and z
 // again.
-template <int N, int PP>
+// UNI: uniform time grid -- (dd, ds, cd, cs) are the temporal coefficients of every step and
+// the per-column constants are set up once.  !UNI: the coefficients of step l come from the
+// plan's bidiagonal arrays (the scalar arguments are unused) and the per-column constants
+// (q, gamma, the chunk / image powers of q) are recomputed at the top of every step.
+template <int N, int PP, bool UNI = true>
 __global__ void __launch_bounds__(TriTmaCfg<N, PP>::kThreads, 1)
     heat_tridiag_tma_kernel(const __grid_constant__ CUtensorMap map, int64_t inner, int64_t ntc,
                             int64_t l0, const double* __restrict__ lam_col,
                             const double* __restrict__ w_col, double dd, double ds, double cd,
                             double cs, double md, double mo, double ad, double ao,
-                            double* __restrict__ carry) {
+                            double* __restrict__ carry, const double* __restrict__ d_diag,
+                            const double* __restrict__ d_sup, const double* __restrict__ c_diag,
+                            const double* __restrict__ c_sup) {
   using C = TriTmaCfg<N, PP>;
   constexpr int R = C::R, T = C::T, n = C::n, W = C::W, LW = C::LW, CW = C::CW;
   extern __shared__ __align__(1024) unsigned char tmraw[];
@@ -446,32 +452,33 @@ __global__ void __launch_bounds__(TriTmaCfg<N, PP>::kThreads, 1)
   };
 
   // per-column constants (.x / .y: the pair's two columns)
-  double2 q, gam, gamA, gamB, sa, sb, wc, qc, gf, gb, qN, inv, pw0, pw1;
-  {
+  double2 q, gam, gamA, gamB, sa, sb, qc, gf, gb, qN, inv, pw0, pw1;
+  const double2 wc = make_double2(w_col[ca], w_col[ca + 1]);
+  const double lam2[2] = {lam_col[ca], lam_col[ca + 1]};
+  const int above = row0 < n ? row0 : n;                      // real rows above the chunk
+  const int below = n - row0 - R > 0 ? n - row0 - R : 0;      // real rows below it
+  auto setup = [&](double dd_, double ds_, double cd_, double cs_) {
     double qq[2], gg[2], s1[2], s2[2];
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
-      const double la = lam_col[ca + c];
-      const double p = dd + la * cd;
-      const double a = p * mo + cd * ao, b = p * md + cd * ad;
-      const double bp = p * (md + 2.0 * mo) + cd * (ad + 2.0 * ao);  // b + 2a
-      const double bm = p * (md - 2.0 * mo) + cd * (ad - 2.0 * ao);  // b - 2a
+      const double la = lam2[c];
+      const double p = dd_ + la * cd_;
+      const double a = p * mo + cd_ * ao, b = p * md + cd_ * ad;
+      const double bp = p * (md + 2.0 * mo) + cd_ * (ad + 2.0 * ao);  // b + 2a
+      const double bm = p * (md - 2.0 * mo) + cd_ * (ad - 2.0 * ao);  // b - 2a
       const double sq = sqrt(bp * bm);
       qq[c] = -a / (0.5 * (b + sq));
       gg[c] = 1.0 / sq;
-      const double pq = ds + la * cs;
-      s1[c] = pq * mo + cs * ao;
-      s2[c] = pq * md + cs * ad;
+      const double pq = ds_ + la * cs_;
+      s1[c] = pq * mo + cs_ * ao;
+      s2[c] = pq * md + cs_ * ad;
     }
     q = make_double2(qq[0], qq[1]);
     gam = make_double2(gg[0], gg[1]);
     sa = make_double2(s1[0], s1[1]);
     sb = make_double2(s2[0], s2[1]);
-    wc = make_double2(w_col[ca], w_col[ca + 1]);
     gamA = t <= TF ? gam : make_double2(0.0, 0.0);  // rows k < TAIL of the chunk
     gamB = t < TF ? gam : make_double2(0.0, 0.0);   // rows k >= TAIL
-    const int above = row0 < n ? row0 : n;                      // real rows above the chunk
-    const int below = n - row0 - R > 0 ? n - row0 - R : 0;      // real rows below it
     qc = make_double2(tri_ipow(q.x, cnt), tri_ipow(q.y, cnt));
     gf = make_double2(tri_ipow(q.x, above), tri_ipow(q.y, above));
     gb = make_double2(tri_ipow(q.x, below), tri_ipow(q.y, below));
@@ -480,7 +487,8 @@ __global__ void __launch_bounds__(TriTmaCfg<N, PP>::kThreads, 1)
     constexpr int lo_rows = 32 * R < n ? 32 * R : n;  // real rows of chunks 0..31
     pw0 = make_double2(tri_ipow(q.x, lo_rows), tri_ipow(q.y, lo_rows));
     pw1 = make_double2(tri_ipow(q.x, n - lo_rows), tri_ipow(q.y, n - lo_rows));
-  }
+  };
+  if constexpr (UNI) setup(dd, ds, cd, cs);
 
   // zero the tile buffers once: rows the TMA boxes never write stay zero; barriers
   for (int e = tid; e < 3 * C::kBufBytes / 16; e += C::kThreads)
@@ -527,6 +535,11 @@ __global__ void __launch_bounds__(TriTmaCfg<N, PP>::kThreads, 1)
   for (int64_t j = 0; j < ntc; ++j) {
     const int s = static_cast<int>(j & 1);
     const unsigned ph = static_cast<unsigned>(j >> 1) & 1u;
+    if constexpr (!UNI) {
+      const int64_t l = l0 + j;
+      setup(__ldg(d_diag + l), l > 0 ? __ldg(d_sup + l - 1) : 0.0, __ldg(c_diag + l),
+            l > 0 ? __ldg(c_sup + l - 1) : 0.0);
+    }
     if (j > 0) {  // the neighbours' edge rows of z_{l-1}
       zu = shfl_up2(x[R - 1], 1, W);
       zn = shfl_down2(x[0], 1, W);

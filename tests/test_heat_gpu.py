@@ -719,14 +719,15 @@ for ndim, n, nt in [(2, 1023, 5), (2, 511, 4), (2, 255, 7), (2, 127, 6), (2, 63,
                     (3, 63, 3)]:
     rng = np.random.default_rng(7 * n + nt)
     F = rng.standard_normal((nt, n ** ndim))
-    p = stk.HeatPlan.p1_uniform(ndim, n, nt, transform="dst")
+    T = nt / (n + 1.0)  # dt = h: a time step in proportion to the mesh, as in the configs
+    p = stk.HeatPlan.p1_uniform(ndim, n, nt, T=T, transform="dst")
     out[f"s{ndim}_{n}"] = np.array(["separate", "fused_dst", "line_solve"].index(p.schedule()))
     Fd = torch.from_numpy(F).cuda()
     U = p.solve(Fd)
     out[f"u{ndim}_{n}"] = U.cpu().numpy()
     out[f"r{ndim}_{n}"] = np.array(p.residual(U, Fd)[0])
     # host-buffer path in 2-slice time chunks: every launch starts from the carried z_{l0-1}
-    pc = stk.HeatPlan.p1_uniform(ndim, n, nt, transform="dst", time_chunk=2)
+    pc = stk.HeatPlan.p1_uniform(ndim, n, nt, T=T, transform="dst", time_chunk=2)
     out[f"h{ndim}_{n}"] = pc.solve_host(F)
 # a longer time axis on a domain / horizon that is not the unit one (other stencil scales)
 p = stk.HeatPlan.p1_uniform(2, 255, 96, T=10.0, a=-1.0, b=1.0, transform="dst")
@@ -736,16 +737,27 @@ U = p.solve(Fd)
 out["s_long"] = np.array(["separate", "fused_dst", "line_solve"].index(p.schedule()))
 out["u_long"] = U.cpu().numpy()
 out["r_long"] = np.array(p.residual(U, Fd)[0])
-# non-uniform temporal bidiagonals: the plan must keep the transform-based pass
-rng = np.random.default_rng(11)
-g = stk.SpaceGrid1D(0.0, 1.0, 255)
-e = stk.p1_eigpair(g)
-M, A = stk.fem1d_matrices(g)
-D = stk.Bidiagonal(rng.uniform(1.0, 2.0, 6), rng.uniform(-1.0, -0.2, 5))
-Cm = stk.Bidiagonal(rng.uniform(0.01, 0.1, 6), rng.uniform(0.01, 0.1, 5))
-pn = stk.HeatPlan(stk.TensorEigPair([e, e]), D, Cm, [M, M], [A, A], transform="dst",
-                  p1_h=[g.fem_h] * 2)
-out["s_nonuniform"] = np.array(["separate", "fused_dst", "line_solve"].index(pn.schedule()))
+# non-uniform temporal bidiagonals: the TMA variant recomputes its per-column constants every
+# step; the LDL^T variant (per-plan pivot table) leaves them to the transform-based pass
+for ndim, n, nt in [(2, 1023, 6), (2, 255, 9), (3, 127, 5)]:
+    rng = np.random.default_rng(11 + n)
+    g = stk.SpaceGrid1D(0.0, 1.0, n)
+    e = stk.p1_eigpair(g)
+    M, A = stk.fem1d_matrices(g)
+    D = stk.Bidiagonal(rng.uniform(1.0, 2.0, nt), rng.uniform(-1.0, -0.2, nt - 1))
+    cscale = 16.0 / (n + 1)  # time steps in proportion to the mesh
+    Cm = stk.Bidiagonal(cscale * rng.uniform(0.01, 0.1, nt), cscale * rng.uniform(0.01, 0.1, nt - 1))
+    F = rng.standard_normal((nt, n ** ndim))
+    Fd = torch.from_numpy(F).cuda()
+    pn = stk.HeatPlan(stk.TensorEigPair([e] * ndim), D, Cm, [M] * ndim, [A] * ndim,
+                      transform="dst", p1_h=[g.fem_h] * ndim)
+    out[f"S{ndim}_{n}"] = np.array(["separate", "fused_dst", "line_solve"].index(pn.schedule()))
+    Un = pn.solve(Fd)
+    out[f"n{ndim}_{n}"] = Un.cpu().numpy()
+    out[f"q{ndim}_{n}"] = np.array(pn.residual(Un, Fd)[0])
+    pc = stk.HeatPlan(stk.TensorEigPair([e] * ndim), D, Cm, [M] * ndim, [A] * ndim,
+                      transform="dst", p1_h=[g.fem_h] * ndim, time_chunk=2)
+    out[f"c{ndim}_{n}"] = pc.solve_host(F)
 np.savez(sys.argv[2], **out)
 """
 
@@ -757,8 +769,9 @@ def test_line_solve_pass_matches_transform_passes(tmp_path):
     schedule for every tile geometry) against the transform-based schedule (STKG_TRIDIAG=0)
     and against the cp.async LDL^T variant of the same pass (STKG_TRI_V=0): device solves,
     host-buffer solves in 2-slice chunks (carried state, l0 > 0), 2D and 3D, N = 64 ... 1024,
-    a non-unit domain and horizon.  Agreement to 5e-12 (different algorithms for the same
-    solve), GPU residuals <= 1e-11; plans with non-uniform time grids keep the transform pass."""
+    a non-unit domain and horizon; non-uniform time grids (per-step constants in the TMA
+    variant, the transform pass under the LDL^T variant).  Agreement to 5e-12 (different
+    algorithms for the same solve), GPU residuals <= 1e-11."""
     import os
     import subprocess
     import sys
@@ -771,10 +784,11 @@ def test_line_solve_pass_matches_transform_passes(tmp_path):
                        env=dict(os.environ, STKG_FUSED="1", **env))
         res[tag] = dict(np.load(f))
     for k, a in res["line"].items():
-        if k[0] == "s":
-            want = 1 if k == "s_nonuniform" else 2
-            assert int(a) == want and int(res["ldl"][k]) == want and int(res["dst"][k]) == 1, k
-        elif k[0] == "r":
+        if k[0] == "s":  # uniform grids: both line-solve variants
+            assert int(a) == 2 and int(res["ldl"][k]) == 2 and int(res["dst"][k]) == 1, k
+        elif k[0] == "S":  # non-uniform grids: the TMA variant only
+            assert int(a) == 2 and int(res["ldl"][k]) == 1 and int(res["dst"][k]) == 1, k
+        elif k[0] in "rq":
             assert float(a) < 1e-11 and float(res["ldl"][k]) < 1e-11, (k, float(a))
         else:
             assert rel(a, res["dst"][k]) < 5e-12, (k, rel(a, res["dst"][k]))
@@ -782,6 +796,22 @@ def test_line_solve_pass_matches_transform_passes(tmp_path):
     for k in res["line"]:
         if k[0] == "h":
             assert rel(res["line"][k], res["line"]["u" + k[1:]]) < 1e-13, k
+        if k[0] == "c":
+            assert rel(res["line"][k], res["line"]["n" + k[1:]]) < 1e-13, k
+
+
+def test_line_solve_conditioning_gate(stk, cuda):
+    """A tridiagonal line solve loses cond(T_c) ulps, the modal recurrence none: plans whose
+    time step is very large against h^2 (cond > 1e5) keep the transform pass, and both
+    schedules stay within 2e-12 of the dense DMMA backend."""
+    n, nt = 1023, 2
+    F = np.random.default_rng(5).standard_normal((nt, n * n))
+    for T, want in ((1.0, "fused_dst"), (nt / 1024.0, "line_solve")):
+        pd = stk.HeatPlan.p1_uniform(2, n, nt, T=T, transform="dense")
+        ps = stk.HeatPlan.p1_uniform(2, n, nt, T=T, transform="dst")
+        assert ps.schedule() == want, (T, ps.schedule())
+        Ud, Us = host(pd.solve(dev(F))), host(ps.solve(dev(F)))
+        assert rel(Us, Ud) < 2e-12, (T, rel(Us, Ud))
 
 
 _OVERLAP_SCRIPT = r"""

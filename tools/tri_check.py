@@ -23,12 +23,13 @@ for ndim, n, nt in [(2, 1023, 5), (2, 511, 4), (2, 255, 7), (2, 127, 6), (2, 63,
                     (3, 63, 3)]:
     rng = np.random.default_rng(7 * n + nt)
     F = rng.standard_normal((nt, n ** ndim))
-    p = stk.HeatPlan.p1_uniform(ndim, n, nt, transform="dst")
+    T = nt / (n + 1.0)
+    p = stk.HeatPlan.p1_uniform(ndim, n, nt, T=T, transform="dst")
     Fd = torch.from_numpy(F).cuda()
     U = p.solve(Fd)
     out[f"u{ndim}_{n}"] = U.cpu().numpy()
     out[f"r{ndim}_{n}"] = np.array(p.residual(U, Fd)[0])
-    pc = stk.HeatPlan.p1_uniform(ndim, n, nt, transform="dst", time_chunk=2)
+    pc = stk.HeatPlan.p1_uniform(ndim, n, nt, T=T, transform="dst", time_chunk=2)
     out[f"h{ndim}_{n}"] = pc.solve_host(F)
 np.savez(sys.argv[2], **out)
 """
