@@ -408,10 +408,10 @@ int tri_variant() {
   return v;
 }
 
-template <int N, int P, bool UNI>
+template <int N, int P, bool UNI, bool GUARD>
 void launch_tridiag_tma_u(const stkg_heat& h, double* S, int64_t inner, int64_t ntc, int64_t l0) {
   using C = TriTmaCfg<N, P>;
-  auto kern = heat_tridiag_tma_kernel<N, P, UNI>;
+  auto kern = heat_tridiag_tma_kernel<N, P, UNI, GUARD>;
   static const bool configured = [kern] {
     STKG_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(C::kSmem)));
@@ -444,8 +444,16 @@ void launch_tridiag_tma_u(const stkg_heat& h, double* S, int64_t inner, int64_t 
 
 template <int N, int P>
 void launch_tridiag_tma(const stkg_heat& h, double* S, int64_t inner, int64_t ntc, int64_t l0) {
-  if (h.uniform_time) return launch_tridiag_tma_u<N, P, true>(h, S, inner, ntc, l0);
-  return launch_tridiag_tma_u<N, P, false>(h, S, inner, ntc, l0);
+  // STKG_TRI_GUARD: 0 / 1 forces the unguarded / guarded kernel; unset: guarded when the
+  // tiles fill most of the GPU (the HBM-bound regime, see heat_tridiag_tma_kernel)
+  static const int force = [] {
+    const char* e = std::getenv("STKG_TRI_GUARD");
+    return e ? std::atoi(e) : -1;
+  }();
+  const bool guard = force >= 0 ? force != 0 : inner / TriTmaCfg<N, P>::G >= (3 * num_sms()) / 4;
+  if (!h.uniform_time) return launch_tridiag_tma_u<N, P, false, false>(h, S, inner, ntc, l0);
+  if (guard) return launch_tridiag_tma_u<N, P, true, true>(h, S, inner, ntc, l0);
+  return launch_tridiag_tma_u<N, P, true, false>(h, S, inner, ntc, l0);
 }
 
 // Columns per line-solve tile for axis-0 length n0 (0: no such kernel for that length).

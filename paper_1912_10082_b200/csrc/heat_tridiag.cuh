@@ -334,6 +334,11 @@ __global__ void __launch_bounds__(TriCfg<N, PP, ST>::kThreads, 1)
 // A thread owns R = 17 rows (odd): rows 17 t + k of 8 consecutive t differ in their low three
 // bits, so TMA's own SWIZZLE_64B / SWIZZLE_128B row mirrors are read and written
 // bank-conflict free (with 16-row chunks every lane of a quarter-warp would hit one bank group).
+#ifndef STKG_TRI_PF
+#define STKG_TRI_PF 0  // L2 prefetch distance of the line-solve pass in slices (<= 2: off;
+                       // measured on cfg3: 3 neutral within noise, 5 and 8 slower)
+#endif
+
 template <int N, int PP>
 struct TriTmaCfg {
   static constexpr int R = 17, T = N / 16, P = PP, G = 2 * PP, kThreads = PP * T, n = N - 1;
@@ -374,6 +379,12 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, int c0, int
       "r"(c0), "r"(c1), "r"(c2), "r"(s)
       : "memory");
 }
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];\n" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(a) : "memory");
@@ -409,7 +420,14 @@ __device__ __forceinline__ double tri_ipow(double q, int e) {
 // the per-column constants are set up once.  !UNI: the coefficients of step l come from the
 // plan's bidiagonal arrays (the scalar arguments are unused) and the per-column constants
 // (q, gamma, the chunk / image powers of q) are recomputed at the top of every step.
-template <int N, int PP, bool UNI = true>
+// GUARD: every row update is predicated on the row being real (k < cnt) on top of the
+// phantom-row neutralisation.  The guards cost 450 instructions per warp and step and are
+// redundant arithmetically, but plans with a full wave of tiles (cfg3: 128) run FASTER with
+// them (3.0 vs 3.3 ms per launch, same box, alternating runs): the longer step keeps the
+// demand just under HBM saturation, while the unguarded kernel runs ahead, waits on its tile
+// loads and then bursts.  Plans with fewer tiles are bound by the step latency and take the
+// unguarded kernel (511^2 x 1024: 2.1 vs 2.6 ms per launch).
+template <int N, int PP, bool UNI = true, bool GUARD = false>
 __global__ void __launch_bounds__(TriTmaCfg<N, PP>::kThreads, 1)
     heat_tridiag_tma_kernel(const __grid_constant__ CUtensorMap map, int64_t inner, int64_t ntc,
                             int64_t l0, const double* __restrict__ lam_col,
@@ -513,9 +531,21 @@ __global__ void __launch_bounds__(TriTmaCfg<N, PP>::kThreads, 1)
         tma_load_3d(tmraw + s * C::kBufBytes + cb * (C::kRows * CW) + rb * (C::BR * CW), &map,
                     i0 + cb * (CW / 8), rb * C::BR, static_cast<int>(j), &full[s]);
   };
+  // The two input buffers bound the load distance to under two steps, less than the DRAM
+  // latency under load once a step is short: tiles kPfDist slices ahead are pulled into L2 by
+  // TMA prefetches (no shared memory, no barrier), so the loads proper hit L2.
+  constexpr int kPfDist = STKG_TRI_PF;
+  auto issue_prefetch = [&](int64_t j) {  // one thread
+#pragma unroll
+    for (int cb = 0; cb < C::NCB; ++cb)
+#pragma unroll
+      for (int rb = 0; rb < C::NRB; ++rb)
+        tma_prefetch_3d(&map, i0 + cb * (CW / 8), rb * C::BR, static_cast<int>(j));
+  };
   if (tid == 0) {
     if (ntc > 0) issue_load(0, 0);
     if (ntc > 1) issue_load(1, 1);
+    for (int64_t j = 2; j < kPfDist && j < ntc; ++j) issue_prefetch(j);
   }
 
   // z_{l0-1}: this thread's rows, the row above its first (zu) and below its last (zn)
@@ -560,7 +590,8 @@ __global__ void __launch_bounds__(TriTmaCfg<N, PP>::kThreads, 1)
         if (k == TAIL && tail_lane) zl = make_double2(0.0, 0.0);
         const double ra = fma(sb.x, zc.x, sa.x * (zl.x + zr.x));
         const double rb = fma(sb.y, zc.y, sa.y * (zl.y + zr.y));
-        x[k] = make_double2(fma(wc.x, g.x, -ra), fma(wc.y, g.y, -rb));
+        x[k] = (!GUARD || k < cnt) ? make_double2(fma(wc.x, g.x, -ra), fma(wc.y, g.y, -rb))
+                                   : make_double2(0.0, 0.0);
         zl = zc;
       }
     }
@@ -572,18 +603,23 @@ __global__ void __launch_bounds__(TriTmaCfg<N, PP>::kThreads, 1)
     double2 cap = make_double2(0.0, 0.0);  // the causal value after the tail lane's real rows
 #pragma unroll
     for (int k = 0; k < R; ++k) {
-      ef.x = fma(q.x, ef.x, x[k].x);
-      ef.y = fma(q.y, ef.y, x[k].y);
+      if (!GUARD || k < cnt) {
+        ef.x = fma(q.x, ef.x, x[k].x);
+        ef.y = fma(q.y, ef.y, x[k].y);
+      }
       if (k == TAIL - 1) cap = ef;
       const int kb = R - 1 - k;
-      eb.x = fma(q.x, eb.x, x[kb].x);
-      eb.y = fma(q.y, eb.y, x[kb].y);
+      if (!GUARD || kb < cnt) {
+        eb.x = fma(q.x, eb.x, x[kb].x);
+        eb.y = fma(q.y, eb.y, x[kb].y);
+      }
     }
     if (tail_lane) ef = cap;  // (zero-start values of phantom rows are zero: eb needs no patch)
     if (tid == 0) {
       // every warp has read tile j: its buffer takes slice j + 2
       mbar_wait(&empty[s], ph);
       if (j + 2 < ntc) issue_load(j + 2, s);
+      if (kPfDist > 2 && j + kPfDist < ntc) issue_prefetch(j + kPfDist);
     }
     // chunk scans (running products of the chunk multipliers q^cnt), both directions
     double2 wf = qc, wb = qc;
@@ -649,9 +685,11 @@ __global__ void __launch_bounds__(TriTmaCfg<N, PP>::kThreads, 1)
       double2 a = fc;
 #pragma unroll
       for (int k = 0; k < R; ++k) {
-        a.x = fma(q.x, a.x, x[k].x);
-        a.y = fma(q.y, a.y, x[k].y);
-        x[k] = a;
+        if (!GUARD || k < cnt) {
+          a.x = fma(q.x, a.x, x[k].x);
+          a.y = fma(q.y, a.y, x[k].y);
+          x[k] = a;
+        }
       }
     }
     // anti-causal sweep: z_i = gamma (A_i + q B_{i+1}),  B_i = r_i + q B_{i+1}, r_i = A_i - q A_{i-1}
@@ -661,14 +699,16 @@ __global__ void __launch_bounds__(TriTmaCfg<N, PP>::kThreads, 1)
       for (int k = R - 1; k >= 0; --k) {
         // (the tail lane's sweep enters its last real row with the carry-in itself)
         if (k == TAIL - 1 && tail_lane) bn = bc;
-        const double2 ak = x[k];
-        const double2 am = k > 0 ? x[k - 1] : fc;
-        const double2 gk = k < TAIL ? gamA : gamB;
-        // r_k = A_k - q A_{k-1} off the chain: one dependent FMA per row on B
-        const double rx = fma(-q.x, am.x, ak.x), ry = fma(-q.y, am.y, ak.y);
-        x[k] = make_double2(gk.x * fma(q.x, bn.x, ak.x), gk.y * fma(q.y, bn.y, ak.y));
-        bn.x = fma(q.x, bn.x, rx);
-        bn.y = fma(q.y, bn.y, ry);
+        if (!GUARD || k < cnt) {
+          const double2 ak = x[k];
+          const double2 am = k > 0 ? x[k - 1] : fc;
+          const double2 gk = k < TAIL ? gamA : gamB;
+          // r_k = A_k - q A_{k-1} off the chain: one dependent FMA per row on B
+          const double rx = fma(-q.x, am.x, ak.x), ry = fma(-q.y, am.y, ak.y);
+          x[k] = make_double2(gk.x * fma(q.x, bn.x, ak.x), gk.y * fma(q.y, bn.y, ak.y));
+          bn.x = fma(q.x, bn.x, rx);
+          bn.y = fma(q.y, bn.y, ry);
+        }
       }
     }
     if (tid == 0) {  // the previous slice's store has read the output buffer (long ago)
