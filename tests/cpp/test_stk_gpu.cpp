@@ -117,6 +117,27 @@ int main() {
     }
     EXPECT(threw);  // P1Dst without p1_h
   }
+  // the line-solve schedule (stkg_heat_schedule): a 2D plan with at least 32 column tiles and
+  // a mesh-proportional time step takes it, a small plan does not; same solve as Dense
+  {
+    const int n = 511, nt = 4;
+    const double T = nt / 512.0;
+    auto pd = heat_plan_p1_uniform(2, n, nt, T, 0.0, 1.0, Transform::Dense);
+    auto ps = heat_plan_p1_uniform(2, n, nt, T, 0.0, 1.0, Transform::P1Dst);
+    EXPECT(ps->schedule() == STKG_SCHEDULE_LINE_SOLVE);
+    EXPECT(pd->schedule() == STKG_SCHEDULE_SEPARATE);
+    EXPECT(heat_plan_p1_uniform(2, 63, 8, 1.0, 0.0, 1.0, Transform::P1Dst)->schedule() ==
+           STKG_SCHEDULE_SEPARATE);
+    std::mt19937_64 rng(13);
+    std::normal_distribution<double> nd;
+    std::vector<double> F(static_cast<size_t>(n) * n * nt);
+    for (auto& v : F) v = nd(rng);
+    DeviceBuffer dF(F), u1(F.size()), u2(F.size());
+    pd->solve(dF.data(), u1.data());
+    ps->solve(dF.data(), u2.data());
+    EXPECT(rel(u2.download(), u1.download()) < 2e-12);
+    EXPECT(ps->residual(u2.data(), dF.data()) < 1e-11);
+  }
   // SingularityError (stk/sylvester.hpp:133-135)
   {
     EigPair e{{2.0}, {1.0}};
