@@ -13,18 +13,24 @@
 //
 // z_l is exactly what heat_fused_axis0_kernel writes (inverse transform of the weighted modal
 // solution), with O(n) instead of O(n log n) work per column and two shared-memory accesses
-// per value instead of two FFTs' worth: the pass becomes an HBM stream.  On a uniform time
-// grid T is the same for every step, so its LDL^T pivots 1/w_i are computed once per plan
-// (tri_factor_kernel) and held in registers.
+// per value instead of two FFTs' worth: the pass becomes an HBM stream.
 //
-// One CTA owns G = 2P neighbouring columns of axis 0 (all n_0 rows) and marches through the
-// time slices.  T = N/16 threads share a column pair; thread t holds rows 16t .. 16t+15 of
-// both columns.  The two triangular solves are first-order linear recurrences along the
-// rows, run as a chunked scan: every thread runs its 16 rows with zero carry-in, the chunk
-// end values are combined across the T threads by a Kogge-Stone scan whose weights (products
-// of the chunks' multipliers) are per-plan constants in registers, and every thread reruns
-// its rows from its carry-in.  No division, no transform, z_{l-1} stays in registers.
+// Two kernels:
+//  * heat_tridiag_tma_kernel (the default; second half of this file): TMA tile loads and
+//    stores, the solve as constant-coefficient causal / anti-causal sweeps (method of images
+//    for the Toeplitz tridiagonal: no per-row data at all), uniform or non-uniform time grids;
+//  * heat_tridiag_axis0_kernel (STKG_TRI_V=0; the first version, kept as an independent
+//    cross-check): cp.async staging, the solve as an LDL^T chunked scan whose reciprocal
+//    pivots 1/w_i are computed once per plan (tri_factor_kernel) and held in registers;
+//    uniform time grids only.  Described next.
 //
+// LDL^T kernel.  One CTA owns G = 2P neighbouring columns of axis 0 (all n_0 rows) and marches
+// through the time slices.  T = N/16 threads share a column pair; thread t holds rows
+// 16t .. 16t+15 of both columns.  The two triangular solves are first-order linear recurrences
+// along the rows, run as a chunked scan: every thread runs its 16 rows with zero carry-in, the
+// chunk end values are combined across the T threads by a Kogge-Stone scan whose weights
+// (products of the chunks' multipliers) are per-plan constants in registers, and every thread
+// reruns its rows from its carry-in.  No division, no transform, z_{l-1} stays in registers.
 // Tiles are staged by 16-byte cp.async into ST buffers (two slices in flight while one is
 // solved); a 16-row block of the tile is followed by 16 bytes of skew so that the 8 threads
 // of a quarter-warp (row chunks 16 rows apart) read 8 distinct bank groups.
