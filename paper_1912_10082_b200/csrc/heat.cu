@@ -799,7 +799,12 @@ void run_chunk_padded(stkg_heat& h, const double* F, double* U, double* S, int64
   const bool fused = use_fused_axis0(h, inner0);
   // (the line-solve pass is an HBM stream: running the contiguous passes beside it only
   // splits the bandwidth -- measured 12.0 vs 10.8 ms on cfg3 -- so it keeps the plain order)
-  if (fused && !use_tridiag(h, inner0) && d == 2 && !h.prof_on && overlap_chunks() > 1 &&
+  static const bool overlap_line = [] {  // STKG_OVERLAP_LINE=1: the overlap for line-solve plans too
+    const char* e = std::getenv("STKG_OVERLAP_LINE");
+    return e && std::atoi(e) != 0;
+  }();
+  if (fused && (overlap_line || !use_tridiag(h, inner0)) && d == 2 && !h.prof_on &&
+      overlap_chunks() > 1 &&
       ntc >= 8 * overlap_chunks() && inner0 / axis0_tile_cols(h, inner0) < num_sms()) {
     run_chunk_padded_overlap(h, F, U, S, l0, ntc, overlap_chunks(), inner0);
     return;
