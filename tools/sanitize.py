@@ -33,6 +33,26 @@ for ndim, n, nt in [(2, 127, 5), (2, 63, 70), (3, 31, 4), (2, 1023, 2), (3, 15, 
         p.apply(U)
         print(ndim, n, nt, tr, "relres", rr, flush=True)
 
+# the line-solve schedule (mesh-proportional time steps; 2D full wave of tiles, 2D / 3D
+# latency-bound tile counts, carried chunks, a non-uniform time grid)
+for ndim, n, nt in [(2, 1023, 5), (2, 511, 4), (3, 127, 3)]:
+    p = stk.HeatPlan.p1_uniform(ndim, n, nt, T=nt / (n + 1.0), transform="dst", time_chunk=2)
+    F = rng.standard_normal((nt, n ** ndim))
+    U = p.solve(dev(F))
+    rr, _ = p.residual(U, dev(F))
+    p.solve_host(F)
+    print(ndim, n, nt, p.schedule(), "relres", rr, flush=True)
+    assert p.schedule() == "line_solve"
+g = stk.SpaceGrid1D(0.0, 1.0, 511)
+e = stk.p1_eigpair(g)
+M, A = stk.fem1d_matrices(g)
+D = stk.Bidiagonal(rng.uniform(1.0, 2.0, 4), rng.uniform(-1.0, -0.2, 3))
+Cm = stk.Bidiagonal(rng.uniform(1e-3, 2e-3, 4), rng.uniform(1e-3, 2e-3, 3))
+pn = stk.HeatPlan(stk.TensorEigPair([e, e]), D, Cm, [M, M], [A, A], transform="dst",
+                  p1_h=[g.fem_h] * 2)
+F = rng.standard_normal((4, 511 * 511))
+print("non-uniform", pn.schedule(), "relres", pn.residual(pn.solve(dev(F)), dev(F))[0], flush=True)
+
 sm = stk.wave_space_matrices(stk.SpaceGrid1D(0.0, 1.0, 31))
 tm = stk.wave_time_matrices(stk.TimeGrid(32, 1.0))
 wp = stk.WavePlan(sm, tm)
