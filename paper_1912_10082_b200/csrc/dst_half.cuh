@@ -818,6 +818,16 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
       "}\n" ::"r"(a), "r"(parity)
       : "memory");
 }
+__device__ __forceinline__ void bulk_load_1d(void* smem, const void* gmem, unsigned bytes,
+                                             uint64_t* bar) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  const unsigned b = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::
+          "r"(s),
+      "l"(gmem), "r"(bytes), "r"(b)
+      : "memory");
+}
 __device__ __forceinline__ void tma_load_2d(void* smem, const CUtensorMap* map, int c0, int c1,
                                             uint64_t* bar) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -904,6 +914,110 @@ __global__ void __launch_bounds__(HalfStrided2Cfg<N, 4, false>::kThreads,
       __stcs(reinterpret_cast<double2*>(dst + base + int64_t(kk) * inner + 2 * q),
              sreg[q * RG + OutPair<N>::idx(kk)]);
     }
+  }
+}
+
+// Contiguous axis, bulk-copy input (one vector pair per CTA, T >= 64): the pair's two vectors
+// are one contiguous, 16-byte aligned region of the source (pairs start at even vectors), so
+// a single cp.async.bulk brings them into the FFT buffer and the pre-processing reads shared
+// memory instead of issuing 4 V global loads per thread against rows that are only 8-byte
+// aligned.  A later item is prefetched into L2 as in dst_half_kernel.  The last vector of an
+// odd count keeps the per-thread loads.
+// SEP (measurement variant, off): the pair lands in its own buffer behind the FFT buffer
+// (16 N more bytes per CTA, 6 instead of 8 CTAs per SM), and the next item's copy is issued as
+// soon as this item's inputs are in registers, so it lands while the FFT and the copy-out
+// run.  Measured slower (cfg3 11.08 vs 10.38 ms): the lost occupancy costs more than the
+// overlap inside one CTA gains -- the other CTAs of the SM already cover the landing time.
+#ifndef STKG_DST_BULK_SEP
+#define STKG_DST_BULK_SEP 0
+#endif
+template <int N, bool SEP = (STKG_DST_BULK_SEP != 0)>
+__global__ void __launch_bounds__(HalfCfg<N>::kThreads, SEP ? 6 : HalfCfg<N>::kMinBlocks)
+    dst_half_bulk_kernel(const double* src, double* dst, int64_t nvec,
+                         const double2* __restrict__ tw2, double scale, int64_t ld_src,
+                         int64_t ld_dst) {
+  using C = HalfCfg<N>;
+  constexpr int V = C::V, T = C::T, n = N - 1;
+  static_assert(C::F == 1, "one pair per CTA");
+  extern __shared__ __align__(16) double2 hbuf[];
+  __shared__ double red[T > 32 ? 2 * (T / 32) : 2];
+  __shared__ __align__(8) uint64_t bar;
+  const int t = static_cast<int>(threadIdx.x);
+  double2* fbuf = hbuf;
+  double* oa = reinterpret_cast<double*>(fbuf);
+  double* ob = oa + opad<V>(N);
+  // the landed pair, linear
+  const double* lin = reinterpret_cast<const double*>(SEP ? hbuf + C::kBuf : fbuf);
+  const int64_t nitems = (nvec + 1) / 2;
+  const double hs = 0.5 * scale;
+  const int ldo = static_cast<int>(ld_dst), ldi = static_cast<int>(ld_src);
+  if (t == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  unsigned phase = 0;
+  auto issue = [&](int64_t it) {  // thread 0: the pair of item `it` (complete pairs only)
+    const unsigned bytes = static_cast<unsigned>(2 * ld_src * sizeof(double));
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    mbar_arrive_expect_tx(&bar, bytes);
+    bulk_load_1d(const_cast<double*>(lin), src + 2 * it * ld_src, bytes, &bar);
+  };
+  if (SEP && t == 0 && int64_t(blockIdx.x) < nitems && 2 * int64_t(blockIdx.x) + 1 < nvec)
+    issue(blockIdx.x);
+  for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x) {
+    const int64_t g0 = 2 * item;
+    const bool has_b = g0 + 1 < nvec;
+    const double* sa = src + g0 * ld_src;
+    double2 x[V];
+    if (has_b) {
+      if (!SEP && t == 0) issue(item);
+      if (STKG_DST_PREFETCH > 0) {  // a later item's pair into L2 while this one lands
+        const int64_t nitem = item + STKG_DST_PREFETCH * int64_t(gridDim.x);
+        if (nitem < nitems) {
+          const char* base = reinterpret_cast<const char*>(src + 2 * nitem * ld_src);
+          const int64_t bytes = (nvec - 2 * nitem < 2 ? 1 : 2) * ld_src * int64_t(sizeof(double));
+          for (int64_t o = int64_t(t) * 128; o < bytes; o += int64_t(C::kThreads) * 128)
+            prefetch_l2(base + o);
+        }
+      }
+      mbar_wait(&bar, phase);
+      phase ^= 1u;
+#pragma unroll
+      for (int p = 0; p < V; ++p) {
+        const int m = t + T * p;
+        x[p] = make_double2(0.0, 0.0);
+        if (m > 0) {
+          const int mm = N - m;
+          const double s = -__ldg(&tw2[m].y);
+          x[p] = half_pre(s, lin[m - 1], lin[mm - 1], lin[ldi + m - 1], lin[ldi + mm - 1]);
+        }
+      }
+      if constexpr (SEP) {
+        __syncthreads();  // every thread holds its inputs: the next pair may land
+        const int64_t nx = item + gridDim.x;
+        if (t == 0 && nx < nitems && 2 * nx + 1 < nvec) issue(nx);
+      }
+    } else {
+#pragma unroll
+      for (int p = 0; p < V; ++p) {
+        const int m = t + T * p;
+        x[p] = make_double2(0.0, 0.0);
+        if (m > 0) {
+          const double s = -__ldg(&tw2[m].y);
+          x[p] = half_pre(s, sa[m - 1], sa[N - m - 1], 0.0, 0.0);
+        }
+      }
+    }
+    // (half_fft_post's first barrier orders the reads of the landed pair before fbuf is
+    // overwritten by the first stage)
+    half_fft_post<N, V, true>(x, fbuf, tw2, t, hs, red, OutSplit<V>{oa, ob});
+    __syncthreads();
+    double* da = dst + g0 * ld_dst;
+    for (int e = t; e < ldo; e += T) da[e] = e < n ? oa[opad<V>(e)] : 0.0;
+    if (has_b)
+      for (int e = t; e < ldo; e += T) da[ld_dst + e] = e < n ? ob[opad<V>(e)] : 0.0;
+    __syncthreads();  // the staging was read: the next pair may land in fbuf
   }
 }
 

@@ -233,6 +233,17 @@ void launch_dst_half_strided2(const stkg_heat& h, const double* src, double* dst
 // (inner == 1): vector g at src + g ld_src -> dst + g ld_dst (ld 0 = n).  Strided axes:
 // dst_half_strided_kernel, or the 16-byte dst_half_strided2_kernel when `wide` (the padded
 // layout: inner a multiple of its tile width, 16-byte aligned buffers).
+// The contiguous pass of one-pair-per-CTA plans (N = 1024) takes its input by one bulk copy
+// per pair (dst_half_bulk_kernel) instead of per-thread loads: bit-identical, cfg3 solve
+// 10.60 -> 10.37 ms (same box, alternating runs).  STKG_DST_BULK=0 keeps the per-thread loads.
+bool dst_bulk_input() {
+  static const bool on = [] {
+    const char* e = std::getenv("STKG_DST_BULK");
+    return !(e && std::atoi(e) == 0);
+  }();
+  return on;
+}
+
 template <int N>
 void launch_dst_half(const stkg_heat& h, int a, const double* src, double* dst, int64_t inner,
                      int64_t outer, int64_t ld_src = 0, int64_t ld_dst = 0, bool wide = false) {
@@ -263,6 +274,24 @@ void launch_dst_half(const stkg_heat& h, int a, const double* src, double* dst, 
       dst_half_kernel<N, true><<<static_cast<unsigned>(blocks), C::kThreads, C::kSmem,
                                  launch_stream(h)>>>(src, dst, nvec, tw2, scale, lds, ldd,
                                                      h.run_ticket);
+    } else if (C::F == 1 && dst_bulk_input() && (reinterpret_cast<uintptr_t>(src) & 15) == 0 &&
+               src != dst) {
+      if constexpr (C::F == 1) {
+        constexpr size_t bsmem = C::kSmem + (STKG_DST_BULK_SEP ? size_t(16) * N : 0);
+        static const int bulk_per_sm = [] {
+          STKG_CUDA_CHECK(cudaFuncSetAttribute(dst_half_bulk_kernel<N>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               static_cast<int>(bsmem)));
+          int b = 0;
+          STKG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+              &b, dst_half_bulk_kernel<N>, C::kThreads, bsmem));
+          return std::max(b, 1);
+        }();
+        const int64_t bblocks =
+            std::min<int64_t>(ceil_div(nvec, 2), int64_t(num_sms()) * bulk_per_sm);
+        dst_half_bulk_kernel<N><<<static_cast<unsigned>(bblocks), C::kThreads, bsmem,
+                                  launch_stream(h)>>>(src, dst, nvec, tw2, scale, lds, ldd);
+      }
     } else {
       dst_half_kernel<N><<<static_cast<unsigned>(blocks), C::kThreads, C::kSmem,
                            launch_stream(h)>>>(src, dst, nvec, tw2, scale, lds, ldd);

@@ -623,7 +623,8 @@ def test_dst_padded_solve_deterministic(stk, cuda, ndim, n, nt):
                                  {"STKG_FUSED": "0"}, {"STKG_FUSED_P": "2"},
                                  {"STKG_FUSED_V": "1"}, {"STKG_FUSED_V": "2"},
                                  {"STKG_FUSED_V": "3"}, {"STKG_FUSED_V": "8"},
-                                 {"STKG_TRIDIAG": "0"}, {"STKG_TRI_V": "0"}])
+                                 {"STKG_TRIDIAG": "0"}, {"STKG_TRI_V": "0"},
+                                 {"STKG_DST_BULK": "0"}])
 def test_tuning_variants_match_default(tmp_path, env):
     """The opt-in tuning variants (strided-tile shapes with and without next-tile prefetch,
     the one-chain scan for small plans, per-step division in the factored scan; the separate
