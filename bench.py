@@ -409,8 +409,9 @@ def _timed_path(stk, inputs, cfg, transform, args, stream, barrier, F, U, with_c
             t_f = s_ms / s_n
             achieved = 16.0 * N / (t_tr / 1e3) / 1e9
             roof = {"bound": "hbm",
-                    "kernel": "dst_half_kernel (FP64 half-length DST-I along the contiguous axis, "
-                              "forward and inverse: N-point Stockham FFT per vector pair)",
+                    "kernel": "dst_half_bulk_kernel / dst_half_kernel (FP64 half-length DST-I along "
+                              "the contiguous axis, forward and inverse: N-point Stockham FFT per "
+                              "vector pair; N = 1024 takes each pair by one bulk copy)",
                     "achieved": achieved, "peak": HBM_GBS, "unit": "GB/s",
                     "frac": achieved / HBM_GBS,
                     "traffic": traffic_from_profiles("dst_half"),
